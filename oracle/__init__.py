@@ -1,0 +1,218 @@
+"""CPU oracle of the Hydraulis two-stage assignment (HYD-H1) -- ctypes wrapper.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s cpu_baseline / ``--impl reference`` leg may import this package.
+The product path (``paper_2412_07894_b200``) never imports it and shares no code
+with it; the two meet only in ``workload`` (seeded inputs, no method arithmetic).
+
+The arithmetic lives in ``oracle/hydref.c`` (plain C11, cited to PAPER.md).
+This wrapper only marshals numpy arrays.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "hydref.c")
+_HDR = os.path.join(_HERE, "hydref.h")
+_LIB = os.path.join(_HERE, "libhydref.so")
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle/libhydref.so with gcc (idempotent)."""
+    stale = not os.path.exists(_LIB) or max(os.path.getmtime(_SRC), os.path.getmtime(_HDR)) > os.path.getmtime(_LIB)
+    if force or stale:
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(
+            ["gcc", "-std=gnu11", "-O2", "-g", "-Wall", "-Wextra", "-shared", "-fPIC", "-pthread", _SRC, "-o", tmp]
+        )
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+_u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+_u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+_i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+_i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+_u16p = np.ctypeslib.ndpointer(np.uint16, flags="C_CONTIGUOUS")
+_u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+_voidp = C.c_void_p
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = C.CDLL(build())
+        I, U32P = C.c_int, C.POINTER(C.c_uint32)
+        L.hydref_cost.argtypes = [_voidp, C.c_uint32, U32P]
+        L.hydref_cost.restype = C.c_uint32
+        L.hydref_sort.argtypes = [_u32p, I, _u32p, _u32p]
+        L.hydref_cost_table.argtypes = [_u32p, I, _voidp, I, I, _u32p, _u32p, _u32p, U32P]
+        L.hydref_dispatch.argtypes = [_u32p, _u32p, I, I, _voidp, _u8p, I, _u8p, C.POINTER(C.c_uint64)]
+        L.hydref_dispatch.restype = I
+        L.hydref_lpt.argtypes = [_u32p, _u32p, I, I, C.c_uint32, _u16p, C.POINTER(C.c_uint64)]
+        L.hydref_lpt.restype = I
+        L.hydref_pack_pipeline.argtypes = [
+            _u32p, _u32p, I, _voidp, C.POINTER(C.c_uint16), C.POINTER(C.c_uint64), _u16p, U32P,
+        ]
+        L.hydref_assign_pair.argtypes = [
+            _u32p, _u32p, I, I, _voidp, _u8p, I, _u8p, C.POINTER(C.c_uint64), _u16p, _u16p, _u64p, U32P,
+        ]
+        L.hydref_assign_pair.restype = C.c_uint64
+        L.hydref_select.argtypes = [_u64p, I, I, U32P]
+        L.hydref_select.restype = C.c_int64
+        L.hydref_assign_batch.argtypes = [
+            _u32p, I, I, _voidp, I, I, _u8p, _u8p, I, I, _u32p, _u32p, _u32p,
+            _u8p, _u64p, _u16p, _u16p, _u64p, _u64p, _i64p, U32P, I,
+        ]
+        L.hydref_assign_pairs.argtypes = [
+            _u32p, _u32p, I, I, I, _voidp, _u8p, _u8p, _i32p, _i32p, I,
+            _u8p, _u64p, _u16p, _u16p, _u64p, _u64p, U32P, I,
+        ]
+        _lib = L
+    return _lib
+
+
+def _sch_ptr(schemes):
+    assert schemes.dtype.itemsize == 48 and schemes.flags.c_contiguous
+    return schemes.ctypes.data
+
+
+def cost(scheme_row, l):
+    """T(l, P) of one scheme (structured array of length 1 or a record)."""
+    s = np.ascontiguousarray(np.atleast_1d(scheme_row))
+    st = C.c_uint32(0)
+    v = lib().hydref_cost(_sch_ptr(s), C.c_uint32(int(l)), C.byref(st))
+    return int(v), int(st.value)
+
+
+def sort(lengths):
+    x = np.ascontiguousarray(lengths, dtype=np.uint32)
+    s = np.empty_like(x)
+    p = np.empty_like(x)
+    lib().hydref_sort(x, x.size, s, p)
+    return s, p
+
+
+def cost_table(lengths_row, schemes, k_pad):
+    x = np.ascontiguousarray(lengths_row, dtype=np.uint32)
+    B = x.size
+    s, p = np.empty(B, np.uint32), np.empty(B, np.uint32)
+    cst = np.empty(B * k_pad, np.uint32)
+    st = C.c_uint32(0)
+    lib().hydref_cost_table(x, B, _sch_ptr(schemes), len(schemes), k_pad, s, p, cst, C.byref(st))
+    return s, p, cst.reshape(B, k_pad), int(st.value)
+
+
+def dispatch(sorted_len, cost_tab, schemes, cand_row):
+    B, k_pad = cost_tab.shape
+    row = np.full(32, 0xFF, np.uint8)
+    row[: len(cand_row)] = cand_row
+    pipe = np.empty(B, np.uint8)
+    lb = C.c_uint64(0)
+    ok = lib().hydref_dispatch(
+        np.ascontiguousarray(sorted_len, np.uint32), np.ascontiguousarray(cost_tab, np.uint32).ravel(),
+        B, k_pad, _sch_ptr(schemes), row, len(cand_row), pipe, C.byref(lb),
+    )
+    return bool(ok), pipe, int(lb.value)
+
+
+def lpt(ell, tau, v, max_len):
+    ell = np.ascontiguousarray(ell, np.uint32)
+    tau = np.ascontiguousarray(tau, np.uint32)
+    mb = np.zeros(max(ell.size, 1), np.uint16)
+    mx = C.c_uint64(0)
+    ok = lib().hydref_lpt(ell, tau, ell.size, int(v), int(max_len), mb, C.byref(mx))
+    return bool(ok), mb[: ell.size], int(mx.value)
+
+
+def pack_pipeline(ell, tau, scheme_row):
+    ell = np.ascontiguousarray(ell, np.uint32)
+    tau = np.ascontiguousarray(tau, np.uint32)
+    s = np.ascontiguousarray(np.atleast_1d(scheme_row))
+    mb = np.zeros(max(ell.size, 1), np.uint16)
+    v, pt, st = C.c_uint16(0), C.c_uint64(0), C.c_uint32(0)
+    lib().hydref_pack_pipeline(ell, tau, ell.size, _sch_ptr(s), C.byref(v), C.byref(pt), mb, C.byref(st))
+    return int(v.value), int(pt.value), mb[: ell.size], int(st.value)
+
+
+def select(makespan, cand_offset=0):
+    m = np.ascontiguousarray(makespan, np.uint64)
+    st = C.c_uint32(0)
+    k = lib().hydref_select(m, m.size, int(cand_offset), C.byref(st))
+    return int(k), int(st.value)
+
+
+def assign_batch(W, n_threads=0, cand_offset=0):
+    """All outputs of steps 1-7 for a ``workload.Workload``; dict of numpy arrays."""
+    It, B, Cn, kp = W.n_iter, W.batch, W.n_cand, W.k_pad
+    o = dict(
+        sorted_len=np.empty((It, B), np.uint32),
+        perm=np.empty((It, B), np.uint32),
+        cost=np.empty((It, B, kp), np.uint32),
+        pipe=np.empty((Cn, It, B), np.uint8),
+        lb=np.empty((Cn, It), np.uint64),
+        mb=np.empty((Cn, It, B), np.uint16),
+        v=np.empty((Cn, It, 32), np.uint16),
+        ptime=np.empty((Cn, It, 32), np.uint64),
+        makespan=np.empty((It, Cn), np.uint64),
+        key=np.empty(It, np.int64),
+    )
+    st = C.c_uint32(0)
+    lib().hydref_assign_batch(
+        np.ascontiguousarray(W.lengths, np.uint32), It, B, _sch_ptr(W.schemes), W.n_schemes, kp,
+        np.ascontiguousarray(W.cand), np.ascontiguousarray(W.cand_np), Cn, int(cand_offset),
+        o["sorted_len"], o["perm"], o["cost"], o["pipe"], o["lb"], o["mb"], o["v"], o["ptime"],
+        o["makespan"], o["key"], C.byref(st), int(n_threads),
+    )
+    o["status"] = int(st.value)
+    return o
+
+
+def cost_tables(W):
+    """Steps 1-2 for every iteration of ``W``: (sorted [It][B], perm, cost [It][B][k_pad], status)."""
+    It, B, kp = W.n_iter, W.batch, W.k_pad
+    s = np.empty((It, B), np.uint32)
+    p = np.empty((It, B), np.uint32)
+    cst = np.empty((It, B, kp), np.uint32)
+    status = 0
+    for t in range(It):
+        st = C.c_uint32(0)
+        lib().hydref_cost_table(
+            np.ascontiguousarray(W.lengths[t]), B, _sch_ptr(W.schemes), W.n_schemes, kp, s[t], p[t],
+            cst[t].reshape(-1), C.byref(st),
+        )
+        status |= int(st.value)
+    return s, p, cst, status
+
+
+def assign_pairs(W, pairs_c, pairs_t, tables=None, n_threads=0):
+    """Outputs for selected (c,t) pairs only; rows indexed by pair."""
+    if tables is None:
+        tables = cost_tables(W)
+    s, _, cst, status = tables
+    pc = np.ascontiguousarray(pairs_c, np.int32)
+    pt = np.ascontiguousarray(pairs_t, np.int32)
+    n, B = pc.size, W.batch
+    o = dict(
+        pipe=np.empty((n, B), np.uint8),
+        lb=np.empty(n, np.uint64),
+        mb=np.empty((n, B), np.uint16),
+        v=np.empty((n, 32), np.uint16),
+        ptime=np.empty((n, 32), np.uint64),
+        makespan=np.empty(n, np.uint64),
+    )
+    st = C.c_uint32(0)
+    lib().hydref_assign_pairs(
+        s, cst.reshape(-1), W.n_iter, B, W.k_pad, _sch_ptr(W.schemes), np.ascontiguousarray(W.cand),
+        np.ascontiguousarray(W.cand_np), pc, pt, n, o["pipe"], o["lb"], o["mb"], o["v"], o["ptime"],
+        o["makespan"], C.byref(st), int(n_threads),
+    )
+    o["status"] = status | int(st.value)
+    return o

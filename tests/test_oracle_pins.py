@@ -1,0 +1,383 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (CPU only).
+
+Each test names the passage it pins.  None of them re-calls the oracle to produce
+its own expectation: expectations come from the paper's closed forms, Python's
+exact big integers / sorted(), a literal transcription of Alg. 1, textbook LPT
+(Graham), brute-force optima (tests/bruteforce.py), SPEC.md's worked examples
+and the hand-computed example of tests/golden/worked_example.json.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import workload as w
+from tests import bruteforce as bf
+
+pytestmark = pytest.mark.usefixtures("oracle_lib")
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _oracle():
+    import oracle
+
+    return oracle
+
+
+def linear_scheme(pp=1, max_len=10**6, util_len=0, b=1, c=0, a=0):
+    return w.make_scheme(pp=pp, max_len=max_len, util_len=util_len, a_q32=a, b_q32=b << 32, c_q32=c << 32)
+
+
+# ----------------------------------------------------------------------------- step 1: cost
+def test_cost_closed_form_bigint():
+    """App. C.2: T = floor((a l^2 + b l + c)/2^32), exact, incl. 128-bit intermediates."""
+    o = _oracle()
+    rng = np.random.default_rng(1)
+    for _ in range(3000):
+        s = w.make_scheme(
+            a_q32=int(rng.integers(0, 2**40)),
+            b_q32=int(rng.integers(0, 2**50)),
+            c_q32=int(rng.integers(1, 2**62)),
+        )
+        l = int(rng.integers(1, 2**24 + 1)) if rng.random() < 0.5 else int(rng.integers(1, 5000))
+        want = bf.T(s[0], l)
+        got, st = o.cost(s, l)
+        if want == 0:
+            assert st == 2 and got == 0
+        elif want > 2**32 - 1:
+            assert st == 1 and got == 2**32 - 1
+        else:
+            assert st == 0 and got == want
+
+
+def test_cost_special_cases():
+    """a=b=0 -> c; a=0,b=1 -> l; a=1,b=c=0 -> l^2 (Q32 units); lengths outside [1,2^24] flagged."""
+    o = _oracle()
+    assert o.cost(w.make_scheme(c_q32=7 << 32), 12345) == (7, 0)
+    assert o.cost(w.make_scheme(b_q32=1 << 32), 4097) == (4097, 0)
+    assert o.cost(w.make_scheme(a_q32=1 << 32), 65535) == (65535**2, 0)
+    assert o.cost(w.make_scheme(a_q32=1 << 32), 65536) == (2**32 - 1, 1)  # 2^32 overflows u32
+    assert o.cost(w.make_scheme(b_q32=1 << 31), 1) == (0, 2)  # floor(0.5) = 0 -> ZERO_COST
+    assert o.cost(w.make_scheme(b_q32=1 << 32), 0)[1] == 4
+    assert o.cost(w.make_scheme(b_q32=1 << 32), 2**24 + 1)[1] == 4
+    # monotone in l for unsigned coefficients (P:1062 with a,b,c >= 0)
+    s = w.make_scheme(a_q32=12345, b_q32=3 << 30, c_q32=5 << 32)
+    vals = [o.cost(s, l)[0] for l in range(1, 3000)]
+    assert all(x <= y for x, y in zip(vals, vals[1:]))
+
+
+# ----------------------------------------------------------------------------- step 2: sort
+@pytest.mark.parametrize("seed", range(5))
+def test_sort_matches_python_sorted(seed):
+    o = _oracle()
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(1, 50, int(rng.integers(1, 3000))).astype(np.uint32)  # many ties
+    s, p = o.sort(lens)
+    ref = sorted(range(len(lens)), key=lambda i: (-int(lens[i]), i))
+    assert list(p) == ref
+    assert list(s) == [int(lens[i]) for i in ref]
+
+
+# ----------------------------------------------------------------------------- golden example
+def test_worked_example_golden():
+    """SURVEY §8(c) hand-computed example (T(l)=l+100, PP=2, two identical pipelines)."""
+    o = _oracle()
+    g = json.load(open(os.path.join(GOLDEN, "worked_example.json")))
+    s = w.make_scheme(**g["scheme"])
+    W = w.custom_workload(g["lengths"], s, [g["candidate"]])
+    r = o.assign_batch(W)
+    e = g["expect"]
+    assert r["status"] == 0
+    assert list(r["sorted_len"][0]) == e["sorted_len"]
+    assert list(r["perm"][0]) == e["perm"]
+    assert list(r["cost"][0][:, 0]) == e["cost"]
+    assert list(r["pipe"][0, 0]) == e["pipe"]
+    assert int(r["lb"][0, 0]) == e["lb"]
+    assert list(r["mb"][0, 0]) == e["mb"]
+    assert list(r["v"][0, 0, :2]) == e["v"] and not r["v"][0, 0, 2:].any()
+    assert list(r["ptime"][0, 0, :2]) == e["ptime"]
+    assert int(r["makespan"][0, 0]) == e["makespan"]
+    assert int(r["key"][0]) == e["key"]
+    opt, _ = bf.two_stage_opt(e["sorted_len"], s, g["candidate"])
+    assert opt == e["brute_force_opt"] and e["makespan"] >= opt
+
+
+# ----------------------------------------------------------------------------- SPEC examples
+def test_spec_packing_examples():
+    """SPEC S:313 ([10]*4, V=2 -> 2+2, obj 2 T(10)(pp+1)) and S:314 ([30,10,10], MaxLen 30)."""
+    o = _oracle()
+    ok, mb, mx = o.lpt([10, 10, 10, 10], [10, 10, 10, 10], 2, 20)
+    assert ok and sorted(np.bincount(mb)) == [2, 2] and mx == 20
+    ok, mb, mx = o.lpt([30, 10, 10], [30, 10, 10], 2, 30)
+    assert ok and mb[0] != mb[1] and mb[1] == mb[2] and mx == 30
+    # one sequence -> V=1, objective T(L) * PP
+    for pp in (1, 2, 4):
+        s = linear_scheme(pp=pp, max_len=100, c=5)
+        v, pt, mb, st = o.pack_pipeline([77], [82], s)
+        assert (v, pt, list(mb), st) == (1, 82 * pp, [0], 0)
+    # capacity forcing: V_lo = ceil(S / MaxLen) (App. D)
+    s = linear_scheme(pp=1, max_len=30)
+    v, pt, mb, st = o.pack_pipeline([30, 10, 10], [30, 10, 10], s)
+    assert v == 2 and pt == 30 * 2
+
+
+def test_spec_dispatch_examples():
+    """S:373-375 horizon (inclusive), S:382-383 lower-bound cases, S:450 homogeneous balance."""
+    o = _oracle()
+    sch = np.concatenate([linear_scheme(max_len=32768), linear_scheme(max_len=8192), linear_scheme(max_len=8192)])
+    # horizon: 10000 > 8192 -> only pipeline 0 (J=1); 8192 fits everywhere (inclusive)
+    for l, allowed in [(10000, {0}), (8192, {0, 1, 2})]:
+        lens = np.array([l], np.uint32)
+        st, _, cst, _ = o.cost_table(lens, sch, 4)
+        ok, pipe, lb = o.dispatch(st, cst, sch, [0, 1, 2])
+        assert ok and pipe[0] in allowed
+    # infeasible: longer than every MaxLen
+    st, _, cst, _ = o.cost_table(np.array([40000, 5], np.uint32), sch, 4)
+    ok, pipe, lb = o.dispatch(st, cst, sch, [0, 1, 2])
+    assert not ok and lb == 2**64 - 1 and (pipe == 0xFF).all()
+    # pp=1 -> LB = plain sum when one pipeline; single sequence, pp=4 -> 4 T(l)
+    s1 = linear_scheme(pp=1, c=3)
+    st, _, cst, _ = o.cost_table(np.array([5, 9, 2], np.uint32), s1, 4)
+    assert o.dispatch(st, cst, s1, [0])[2] == (5 + 3) + (9 + 3) + (2 + 3)
+    s4 = linear_scheme(pp=4, c=3)
+    st, _, cst, _ = o.cost_table(np.array([9], np.uint32), s4, 4)
+    assert o.dispatch(st, cst, s4, [0])[2] == 4 * 12
+    # homogeneous 4x<1,1,1>, 4 equal sequences, linear T -> makespan T(l)
+    W = w.custom_workload([100, 100, 100, 100], linear_scheme(), [[0, 0, 0, 0]])
+    r = o.assign_batch(W)
+    assert sorted(r["pipe"][0, 0]) == [0, 1, 2, 3] and int(r["makespan"][0, 0]) == 100
+
+
+# ----------------------------------------------------------------------------- dispatch = Alg. 1
+def alg1_single_trial(sorted_len, schemes, cand_row):
+    """Literal transcription of Alg. 1 for one trial with pi = sorted order.
+
+    Ties in O_max (strict '<' on line 12 leaves them open, reading 10) are broken
+    by the smaller own new load C'_j + E'_j, then the smaller j.
+    """
+    D = len(cand_row)
+    sch = [schemes[k] for k in cand_row]
+    Cj, Ej = [0] * D, [0] * D
+    assigned = [[] for _ in range(D)]
+    pipe = []
+    for l in sorted_len:
+        l = int(l)
+        J = [j for j in range(D) if int(sch[j]["max_len"]) >= l]  # j = 1..J_i
+        best = None
+        for j in J:
+            lmax = max([l] + assigned[j])  # line 8 (l_j read as l_i, reading 8)
+            Cp = Cj[j] + bf.T(sch[j], l)  # line 9
+            Ep = bf.T(sch[j], lmax) * (int(sch[j]["pp"]) - 1)  # line 10
+            Omax = max([Cp + Ep] + [Cj[k] + Ej[k] for k in range(D) if k != j])  # line 11
+            keyv = (Omax, Cp + Ep, j)
+            if best is None or keyv < best[0]:
+                best = (keyv, j, Cp, Ep)
+        _, j, Cp, Ep = best
+        Cj[j], Ej[j] = Cp, Ep
+        assigned[j].append(l)
+        pipe.append(j)
+    return pipe, max(Cj[j] + Ej[j] for j in range(D))
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_dispatch_equals_alg1_transcription(seed):
+    o = _oracle()
+    rng = np.random.default_rng(100 + seed)
+    K = int(rng.integers(1, 5))
+    sch = np.zeros(K, dtype=w.SCHEME_DTYPE)
+    for k in range(K):
+        sch[k]["pp"] = int(rng.integers(1, 5))
+        sch[k]["max_len"] = int(rng.integers(200, 2000))
+        sch[k]["a_q32"] = int(rng.integers(0, 2**28))
+        sch[k]["b_q32"] = int(rng.integers(2**30, 2**34))
+        sch[k]["c_q32"] = int(rng.integers(0, 2**40))
+    D = int(rng.integers(1, 9))
+    row = w.canonical(sch, [int(x) for x in rng.integers(0, K, D)])
+    B = int(rng.integers(1, 200))
+    lens = rng.integers(1, int(sch[row[0]]["max_len"]) + 1, B).astype(np.uint32)
+    st, _, cst, status = o.cost_table(lens, sch, w._kpad(K))
+    assert status == 0
+    ok, pipe, lb = o.dispatch(st, cst, sch, row)
+    ref_pipe, ref_lb = alg1_single_trial(st, sch, row)
+    assert ok and list(pipe) == ref_pipe and lb == ref_lb
+
+
+def test_dispatch_eq2_recomputed():
+    """LB output equals Eq. 2 recomputed from the pipe assignment, max over j (Eq. 3)."""
+    o = _oracle()
+    W = w.make_workload(3, n_cand=12, n_iter=3)
+    r = o.assign_batch(W)
+    for c in range(W.n_cand):
+        row = [int(k) for k in W.cand[c, : W.cand_np[c]]]
+        for t in range(W.n_iter):
+            if r["lb"][c, t] == 2**64 - 1:
+                continue
+            ls = r["sorted_len"][t]
+            lbs = [
+                bf.lower_bound([int(ls[i]) for i in range(W.batch) if r["pipe"][c, t, i] == j], W.schemes[row[j]])
+                for j in range(len(row))
+            ]
+            assert int(r["lb"][c, t]) == max(lbs)
+            # E.1: LB_j <= the packing objective of any feasible packing
+            for j in range(len(row)):
+                assert lbs[j] <= int(r["ptime"][c, t, j])
+
+
+def test_dispatch_graham_identical_machines():
+    """Identical pipelines, PP=1, ample capacity: dispatch is Graham's LPT list scheduling."""
+    o = _oracle()
+    s = linear_scheme(pp=1, max_len=10**6)
+    # tight case (3,3,2,2,2) on 2 machines: LPT 7 vs OPT 6 (4/3 - 1/6 = 7/6 bound)
+    st, _, cst, _ = o.cost_table(np.array([2, 3, 2, 3, 2], np.uint32), s, 4)
+    ok, pipe, lb = o.dispatch(st, cst, s, [0, 0])
+    assert lb == 7 and bf.makespan_opt_identical([3, 3, 2, 2, 2], 2) == 6
+    rng = np.random.default_rng(7)
+    worst = 1.0
+    for _ in range(150):
+        D = int(rng.integers(2, 4))
+        costs = rng.integers(1, 30, int(rng.integers(D, 9))).astype(np.uint32)
+        st, _, cst, _ = o.cost_table(costs, s, 4)
+        ok, pipe, lb = o.dispatch(st, cst, s, [0] * D)
+        # textbook LPT: least-loaded machine, lowest index on ties
+        loads = [0] * D
+        ref = []
+        for c in sorted(costs.tolist(), reverse=True):
+            j = min(range(D), key=lambda m: (loads[m], m))
+            loads[j] += c
+            ref.append(j)
+        assert list(pipe) == ref and lb == max(loads)
+        opt = bf.makespan_opt_identical(costs.tolist(), D)
+        assert lb * 3 * D <= (4 * D - 1) * opt  # Graham: LPT <= (4/3 - 1/(3D)) OPT
+        worst = max(worst, lb / opt)
+    assert worst > 1.0
+
+
+# ----------------------------------------------------------------------------- packing
+def _check_pack(o, W, r):
+    """Structural invariants of every packing (Eq. 1 constraints)."""
+    for c in range(W.n_cand):
+        row = [int(k) for k in W.cand[c, : W.cand_np[c]]]
+        for t in range(W.n_iter):
+            ms = int(r["makespan"][t, c])
+            if ms == 2**64 - 1:
+                assert (r["pipe"][c, t] == 0xFF).all() and (r["mb"][c, t] == 0xFFFF).all()
+                assert not r["v"][c, t].any() and not r["ptime"][c, t].any()
+                continue
+            ls = r["sorted_len"][t]
+            pt_max = 0
+            for j, k in enumerate(row):
+                s = W.schemes[k]
+                idx = np.nonzero(r["pipe"][c, t] == j)[0]
+                V = int(r["v"][c, t, j])
+                if idx.size == 0:
+                    assert V == 0 and int(r["ptime"][c, t, j]) == 0
+                    continue
+                lens = [int(ls[i]) for i in idx]
+                assert max(lens) <= int(s["max_len"])  # horizon J_i
+                mbs = r["mb"][c, t, idx].astype(int)
+                assert V >= 1 and mbs.min() == 0 and mbs.max() == V - 1
+                assert len(set(mbs.tolist())) == V  # no empty micro-batch
+                tok = np.bincount(mbs, weights=lens, minlength=V)
+                assert tok.max() <= int(s["max_len"])  # capacity (Eq. 1)
+                times = [sum(bf.T(s, lens[q]) for q in range(len(lens)) if mbs[q] == b) for b in range(V)]
+                obj = max(times) * (int(s["pp"]) - 1 + V)  # Eq. 1 objective
+                assert obj == int(r["ptime"][c, t, j])
+                lo, hi = bf.v_range(lens, s)
+                assert V >= lo  # App. D lower bound always holds; above hi only if extended
+                pt_max = max(pt_max, obj)
+            assert pt_max == ms
+        # step 7: key = argmin (makespan, c)
+    for t in range(W.n_iter):
+        feas = [(int(r["makespan"][t, c]), c) for c in range(W.n_cand) if r["makespan"][t, c] < 2**43]
+        want = (min(feas)[0] << 20 | min(feas)[1]) if feas else 2**63 - 1
+        assert int(r["key"][t]) == want
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_pack_invariants_configs(cfg):
+    o = _oracle()
+    W = w.make_workload(cfg, n_cand=min(6 if cfg < 5 else 2, w.CONFIGS[cfg]["C"]), n_iter=3 if cfg < 5 else 1)
+    if cfg == 5:  # keep the plain oracle fast: a 1024-sequence prefix of the stress batch
+        W.lengths = np.ascontiguousarray(W.lengths[:, :1024])
+    r = o.assign_batch(W, n_threads=4)
+    assert r["status"] == 0
+    _check_pack(o, W, r)
+
+
+def test_pack_equal_costs_closed_form():
+    """Equal costs tau, ample capacity: LPT(V) is round robin, max bin = ceil(U/V) tau, so
+    V* = argmin_V (ceil(U/V) tau (PP-1+V), V) over App. D's range (Eq. 1 closed form)."""
+    o = _oracle()
+    for U in range(1, 40):
+        for pp in (1, 2, 3, 5):
+            for ul in (0, 7, 40):
+                s = linear_scheme(pp=pp, max_len=10**6, util_len=ul, c=3)
+                lens = [10] * U
+                lo, hi = bf.v_range(lens, s)
+                want = min(((-(-U // V)) * 13 * (pp - 1 + V), V) for V in range(lo, hi + 1))
+                v, pt, mb, st = o.pack_pipeline(lens, [13] * U, s)
+                assert (pt, v) == want
+                assert list(mb) == [q % v for q in range(U)]
+
+
+def test_lpt_graham_per_v():
+    """Without binding capacity LPT(V) is Graham's LPT on V identical bins:
+    max bin <= (4/3 - 1/(3V)) * optimal max bin (brute force)."""
+    o = _oracle()
+    rng = np.random.default_rng(11)
+    for _ in range(120):
+        U = int(rng.integers(2, 7))
+        tau = sorted(rng.integers(1, 40, U).tolist(), reverse=True)
+        for V in range(1, U + 1):
+            ok, mb, mx = o.lpt([1] * U, tau, V, 10**6)
+            opt = bf.makespan_opt_identical(tau, V)
+            assert ok and mx >= opt and mx * 3 * V <= (4 * V - 1) * opt
+
+
+def test_lpt_infeasible_returns_bottom():
+    o = _oracle()
+    ok, _, _ = o.lpt([6, 6, 6], [1, 1, 1], 2, 10)  # three 6s into two bins of 10
+    assert not ok
+    # pack extends V beyond App. D's upper bound when the range is infeasible (reading 5)
+    s = linear_scheme(pp=1, max_len=10, util_len=18)  # V_hi = floor(18/18) = 1 < needed
+    v, pt, mb, st = o.pack_pipeline([6, 6, 6], [1, 1, 1], s)
+    assert v == 3 and pt == 3
+
+
+# ----------------------------------------------------------------------------- brute force
+def test_heuristic_vs_bruteforce_opt():
+    """Heuristic >= exhaustive two-stage OPT always; the Eq. 3 value it reports (LB) is >= the
+    Eq. 3 optimum; the Eq. 3 optimum <= the two-stage optimum (E.1).  The paper's statistical
+    claim (approximation error < 10%) is reported as the fraction within 1.10."""
+    o = _oracle()
+    rng = np.random.default_rng(2024)
+    within, n = 0, 0
+    for trial in range(60):
+        B = int(rng.integers(2, 7))
+        D = int(rng.integers(1, 4))
+        W = w.random_small_instance(rng, B, D)
+        r = o.assign_batch(W)
+        assert r["status"] == 0
+        row = [int(k) for k in W.cand[0, : W.cand_np[0]]]
+        opt, opt_lb = bf.two_stage_opt([int(x) for x in r["sorted_len"][0]], W.schemes, row)
+        h = int(r["makespan"][0, 0])
+        assert h >= opt
+        assert int(r["lb"][0, 0]) >= opt_lb
+        assert opt_lb <= opt
+        n += 1
+        within += h <= 1.10 * opt
+    frac = within / n
+    print(f"heuristic within 1.10 x OPT on {within}/{n} = {frac:.2%} of tiny instances")
+    assert frac >= 0.90  # S:402 acceptance: >= 90% of instances within 10%
+
+
+def test_select_rules():
+    """Step ④: argmin over (makespan, c); infeasible and key-range exclusions."""
+    o = _oracle()
+    assert o.select([5, 3, 3, 2**64 - 1])[0] == (3 << 20) | 1
+    assert o.select([5, 3, 3], cand_offset=100)[0] == (3 << 20) | 101
+    assert o.select([2**64 - 1, 2**64 - 1]) == (2**63 - 1, 0)
+    k, st = o.select([2**43, 9])
+    assert k == (9 << 20) | 1 and st == 8
