@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""Benchmark of the Hydraulis two-stage data assignment on B200.
+
+Metric (BASELINE.json): candidate-iteration assignments per second -- one c-i is one
+complete pipe + mb + ptime + makespan row for one (candidate, iteration) pair followed by
+the per-iteration selection.  A step is one pass of the whole hot path a1-a6 over the
+configuration's batch: sort + cost table, dispatch, pack, select, and (N > 1) the NCCL
+allreduce-min of the keys.  Default workload: BASELINE config 4 (512 seqs x 1024 iterations
+x 4096 candidates, LLaMA-70B-shaped cost models), strong-scaled over N GPUs by candidate.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+  N > 1: python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workload as wl  # noqa: E402
+
+METRIC = "candidate-iteration assignments/sec"
+UNIT = "c-i/s"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu/clocks)")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.p = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_gpu{gpu_index}.csv")
+
+    def start(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle leg
+def oracle_sample(W, target_s, rng_seed=0, max_cand=None):
+    """Time the oracle (as it stands) on a bounded slice of W: a1-a5 for C' candidates x It' iterations."""
+    import oracle
+
+    oracle.build()
+    rng = np.random.default_rng(rng_seed)
+    n_it = min(2, W.n_iter)
+    its = np.sort(rng.choice(W.n_iter, n_it, replace=False))
+    # calibrate on a few candidates, then size the sample to ~target_s
+    ncal = min(W.n_cand, 16)
+    sub = wl.Workload(W.cfg, W.name, W.lengths[its], W.schemes, W.cand[:ncal], W.cand_np[:ncal], W.k_pad)
+    t0 = time.perf_counter()
+    oracle.assign_batch(sub, n_threads=0)
+    per = (time.perf_counter() - t0) / (ncal * n_it)
+    nc = int(max(1, min(W.n_cand if max_cand is None else max_cand, target_s / max(per, 1e-9) / n_it)))
+    cs = np.sort(rng.choice(W.n_cand, nc, replace=False))
+    sub = wl.Workload(W.cfg, W.name, W.lengths[its], W.schemes, W.cand[cs], W.cand_np[cs], W.k_pad)
+    t0 = time.perf_counter()
+    oracle.assign_batch(sub, n_threads=0)
+    dt = time.perf_counter() - t0
+    cores = os.cpu_count() or 1
+    return {
+        "value": (nc * n_it) / dt,
+        "unit": UNIT,
+        "cores": min(cores, nc),
+        "kind": "oracle",
+        "sample": f"{nc} candidates x {n_it} iterations of cfg{W.cfg} ({nc * n_it} c-i, steps a1-a5), "
+                  f"{dt:.1f} s on {min(cores, nc)} threads",
+        "seconds": dt,
+    }
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if world > 1 and rank != 0:
+        return 0
+    W = wl.make_workload(args.config)
+    import oracle
+
+    oracle.build()
+    rng = np.random.default_rng(1)
+    per_step = 64  # candidates per step (x 2 iterations): a bounded sample of the workload
+    times = []
+    for s in range(args.warmup + args.steps):
+        its = np.sort(rng.choice(W.n_iter, 2, replace=False))
+        cs = np.sort(rng.choice(W.n_cand, per_step, replace=False))
+        sub = wl.Workload(W.cfg, W.name, W.lengths[its], W.schemes, W.cand[cs], W.cand_np[cs], W.k_pad)
+        t0 = time.perf_counter()
+        oracle.assign_batch(sub, n_threads=0)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+    ms = 1000.0 * float(np.mean(times))
+    val = (per_step * 2) / (ms / 1000.0)
+    cores = os.cpu_count() or 1
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": val,
+        "unit": UNIT,
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "int64",
+        "data": "synthetic",
+        "config": {"workload": W.name, "sample_per_step": f"{per_step} candidates x 2 iterations"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": min(cores, per_step), "kind": "oracle",
+                         "sample": f"{per_step} random candidates x 2 random iterations of cfg{W.cfg} per step"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU leg
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    from paper_2412_07894_b200 import assign, hyd
+
+    world, rank, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    W = wl.make_workload(args.config)
+    sh = assign.plan_shard(W.n_cand, W.n_iter, world, rank)
+    cand = W.cand[sh.cand_lo:sh.cand_hi]
+    cand_np = W.cand_np[sh.cand_lo:sh.cand_hi]
+    lens = W.lengths[sh.iter_lo:sh.iter_hi]
+    It_local, C_local = lens.shape[0], cand.shape[0]
+    A = assign.Assigner(W.schemes, cand, cand_np, It_local, W.batch, W.k_pad, cand_offset=sh.cand_lo, device=dev)
+    len_dev = assign.lengths_to_device(lens, dev)
+    A._lens_host = lens
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    names = ["sort_cost", "dispatch", "pack", "select", "allreduce"]
+
+    def step(evs=None):
+        It, B, K, kp, Cn = A.n_iter, A.batch, A.n_schemes, A.k_pad, A.n_cand
+        if evs:
+            evs[0].record(stream)
+        hyd.cost_table(len_dev, It, B, A.schemes, K, kp, A.sorted_len, A.perm, A.cost, A.status)
+        if evs:
+            evs[1].record(stream)
+        hyd.dispatch(A.sorted_len, A.cost, It, B, kp, A.schemes, K, A.cand, A.cand_np, Cn, A.max_np, A.pipe, A.lb,
+                     A.status)
+        if evs:
+            evs[2].record(stream)
+        hyd.pack(A.sorted_len, A.cost, It, B, kp, A.schemes, K, A.cand, A.cand_np, Cn, A.max_np, A.pipe, A.mb, A.v,
+                 A.ptime, A.makespan, A.status, A.ws)
+        if evs:
+            evs[3].record(stream)
+        hyd.select_best(A.makespan, It, Cn, A.cand_offset, A.key, A.status)
+        if evs:
+            evs[4].record(stream)
+        if sh.needs_reduce:
+            assign.reduce_keys(A.key)
+        if evs:
+            evs[5].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(dev.index) if not args.profile else None
+    if clk:
+        clk.start()
+        time.sleep(0.3)
+    per_step = []
+    per_kernel = np.zeros(len(names))
+    l0 = hyd.kernel_launches()
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush outside the timed events
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+        step(evs)
+        per_step.append(evs)
+    torch.cuda.synchronize()
+    launches = hyd.kernel_launches() - l0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = clk.stop() if clk else None
+    step_ms = []
+    for evs in per_step:
+        step_ms.append(evs[0].elapsed_time(evs[5]))
+        per_kernel += np.array([evs[i].elapsed_time(evs[i + 1]) for i in range(5)])
+    ms_local = float(np.sum(step_ms)) / args.steps
+    per_kernel /= args.steps
+    t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    total_ci = W.n_cand * W.n_iter
+    value = total_ci / (ms / 1000.0)
+    bits = A.status_bits()
+    if bits:
+        print(f"WARNING: device status {hyd.status_names(bits)}", file=sys.stderr)
+
+    # ---- roofline of the dominant kernel (largest share of the step)
+    pk, how = peaks()
+    dom = int(np.argmax(per_kernel[:4]))
+    roof = roofline(names[dom], per_kernel[dom], W, A, pk, how, local_ci=C_local * It_local)
+
+    # ---- end-to-end through the public host-buffer API (hyd_assign_host)
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        e2e = run_e2e(args, W, sh, cand, cand_np, lens, world, dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
+        cpu = oracle_sample(W, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "int64",
+            "data": "synthetic",
+            "config": {
+                "workload": W.name,
+                "batch": W.batch,
+                "pipelines": int(W.cand_np.max()),
+                "candidates": W.n_cand,
+                "iterations": W.n_iter,
+                "c_i_per_step": total_ci,
+                "shard": sh.by,
+                "parallelism": f"candidates/{world}" if sh.by == "cand" else (f"iterations/{world}" if sh.by == "iter" else "single"),
+                "l2": "flushed: 256 MiB memset between steps, outside the timed events",
+                "cost_model": W.meta.get("model"),
+            },
+            "kernel_ms": {n: float(x) for n, x in zip(names, per_kernel)},
+            "roofline": roof,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "status": hyd.status_names(bits),
+        }
+        if e2e is not None:
+            line["e2e"] = e2e
+        if cpu is not None:
+            line["cpu_baseline"] = {k: v for k, v in cpu.items() if k != "seconds"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def roofline(name, ms, W, A, pk, how, local_ci):
+    """Algorithmic work per launch / CUDA-event duration."""
+    B, D = W.batch, int(W.cand_np.max())
+    sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
+    alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e9  # int32 lane-ops/s in Gop/s
+    hbm = float(pk.get("hbm_gbs", 6650.0))
+    if name == "pack":
+        cnt = A.pack_counters()
+        ops = 6.0 * cnt["bin_evals"]  # ~6 int32 ops per (item, bin) evaluation
+        achieved = ops / (ms / 1000.0) / 1e9
+        return {"kernel": "pack (k_pack_small + k_pack_big)", "bound": "alu", "achieved": achieved,
+                "peak": alu_peak, "unit": "Gop/s", "frac": achieved / alu_peak, "traffic": None,
+                "algorithmic_ops_per_launch": ops, "bin_evals_per_launch": cnt["bin_evals"],
+                "hbm_algorithmic_GBps": local_ci * (3 * B + 10 * D + 8) / (ms / 1000.0) / 1e9,
+                "peak_source": f"148 SM x 128 INT32 lanes x {sm_mhz:.0f} MHz ({how} clock)"}
+    if name == "dispatch":
+        ev = A.dispatch_evals(A._lens_host)
+        ops = 6.0 * ev
+        achieved = ops / (ms / 1000.0) / 1e9
+        return {"kernel": "dispatch", "bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Gop/s",
+                "frac": achieved / alu_peak, "traffic": None, "algorithmic_ops_per_launch": ops,
+                "peak_source": f"148 SM x 128 INT32 lanes x {sm_mhz:.0f} MHz ({how} clock)"}
+    byts = {"sort_cost": A.n_iter * B * (4 + 8 + 4 * A.k_pad), "select": A.n_iter * A.n_cand * 8 + 8 * A.n_iter}[name]
+    achieved = byts / (ms / 1000.0) / 1e9
+    return {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": None, "peak_source": how}
+
+
+def run_e2e(args, W, sh, cand, cand_np, lens, world, dev):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2412_07894_b200 import assign
+
+    H = assign.HostAssigner(W.schemes, cand, cand_np, lens.shape[0], W.batch, W.k_pad, cand_offset=sh.cand_lo,
+                            reduce=sh.needs_reduce)
+    lh = torch.from_numpy(np.ascontiguousarray(lens).view(np.int32)).pin_memory()
+    stream = torch.cuda.current_stream()
+    for _ in range(max(1, args.warmup)):
+        H(lh)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    tot = 0.0
+    n = max(1, min(args.steps, 5))
+    for _ in range(n):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        H(lh)  # H2D copies, kernels, (allreduce), gather, D2H, stream sync
+        b.record(stream)
+        b.synchronize()
+        tot += a.elapsed_time(b)
+    ms = tot / n
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"value": W.n_cand * W.n_iter / (ms / 1000.0), "unit": UNIT,
+            "h2d_bytes_per_step": int(lh.numel() * 4 + H.h2d_bytes_fixed), "d2h_bytes_per_step": int(H.d2h_bytes),
+            "ms_per_step": ms, "api": "hyd_assign_host (pinned host buffers)"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

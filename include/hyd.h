@@ -1,0 +1,173 @@
+/* include/hyd.h -- C ABI of libhyd.so: the Hydraulis two-stage data assignment on B200.
+ *
+ * What it computes (PAPER.md = /root/reference/PAPER.md, cited P:<line>):
+ *   For every iteration t (a mini-batch of B variable-length sequences) and
+ *   every candidate heterogeneous strategy c = P_1 + ... + P_D, the two-stage
+ *   sequence assignment of §6: stage 1 dispatches the sequences across the D
+ *   pipelines (Eq. 2/3 P:634-650, Alg. 1), stage 2 packs each pipeline's
+ *   sequences into micro-batches (Eq. 1, App. D); the estimated
+ *   propagation latency of (c,t) is the max over pipelines of the Eq. 1 objective, and the
+ *   best candidate per iteration is selected (step ④).  The ILP solves are
+ *   replaced by the deterministic heuristic HYD-H1.
+ *
+ * Conventions (all entry points):
+ *   - Pointers are DEVICE pointers unless the name ends in _host.  Every call is
+ *     stream-ordered and asynchronous on `stream` (a cudaStream_t passed as void*).
+ *   - The caller owns every buffer.  The library allocates nothing and keeps no global
+ *     state; scratch memory is a caller-provided device workspace.
+ *   - Host-side argument validation returns a negative HYD_E_* code synchronously and
+ *     launches nothing.  Data-dependent faults set HYD_F_* bits in the device word
+ *     `status` (OR-ed, never cleared by the library); the caller reads it after syncing.
+ *   - Infeasibility is a result, not an error: if the longest sequence of iteration t
+ *     exceeds MaxLen of every pipeline of candidate c, then for (c,t):
+ *     pipe row = 0xFF, mb row = 0xFFFF, v = ptime = 0, lb = makespan = UINT64_MAX.
+ *   - Sequence-indexed outputs are indexed by SORTED position i (length descending,
+ *     original index ascending); perm[t][i] is the original index of position i.
+ *   - Limits: 1 <= batch <= HYD_MAX_BATCH; 1 <= n_schemes <= HYD_MAX_SCHEMES;
+ *     k_pad % 4 == 0 and k_pad >= n_schemes; 1 <= cand_np[c] <= max_np <= 32;
+ *     1 <= pp <= HYD_MAX_PP; max_len >= 1; n_cand + cand_offset <= 2^20.
+ *     Lengths must lie in [1, 2^24] (else HYD_F_BAD_LENGTH).
+ */
+#ifndef HYD_H
+#define HYD_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HYD_MAX_BATCH 16384
+#define HYD_MAX_SCHEMES 64
+#define HYD_MAX_PIPES 32
+#define HYD_MAX_PP 1024
+#define HYD_KEY_SHIFT 20 /* key = makespan << 20 | candidate (global index) */
+
+/* One parallel scheme P = <TP,PP,CP> with its profiled cost models (48 bytes).
+ *   T(l,P) = floor((a_q32 l^2 + b_q32 l + c_q32) / 2^32) ticks  (App. C.2; Q32 reading)
+ *   max_len  = MaxLen(P): token cap of one micro-batch (App. C.1; Eq. 1)
+ *   util_len = UtilLen(P) (App. D); 0 disables the upper bound on V. */
+typedef struct {
+  uint32_t tp, pp, cp; /* pp enters the arithmetic (Eq. 1/2); tp, cp informational */
+  uint32_t max_len;
+  uint32_t util_len;
+  uint32_t _pad;
+  uint64_t a_q32, b_q32, c_q32;
+} hyd_scheme;
+
+/* return codes */
+enum {
+  HYD_OK = 0,
+  HYD_E_INVALID = -1,       /* null pointer, size or limit violated */
+  HYD_E_NOT_CANONICAL = -2, /* a candidate is not (MaxLen desc, scheme index asc) ordered */
+  HYD_E_OVERFLOW = -3,
+  HYD_E_ZERO_COST = -4,
+  HYD_E_CUDA = -5,      /* a CUDA launch/copy failed (see hyd_last_cuda_error) */
+  HYD_E_WORKSPACE = -6, /* workspace null or smaller than the *_workspace() size */
+  HYD_E_REDUCE = -7     /* the caller's allreduce callback returned non-zero */
+};
+
+/* device status bits */
+enum {
+  HYD_F_OVERFLOW = 1u,      /* a cost exceeded 2^32-1 */
+  HYD_F_ZERO_COST = 2u,     /* a cost evaluated to 0 */
+  HYD_F_BAD_LENGTH = 4u,    /* a length was 0 or > 2^24 */
+  HYD_F_KEY_RANGE = 8u,     /* a feasible makespan >= 2^43 (excluded from selection) */
+  HYD_F_NOT_CANONICAL = 16u /* device-side candidate check failed (treated infeasible) */
+};
+
+/* ---- a1+a2: per-iteration stable sort + cost table ------------------------------------
+ * len [n_iter][batch] u32 -> sorted_len [n_iter][batch] (length descending, ties by
+ * original index ascending), perm [n_iter][batch] (original index of each sorted position),
+ * cost [n_iter][batch][k_pad] u32: cost[t][i][k] = T(sorted_len[t][i], schemes[k]) for
+ * k < n_schemes, 0 for padding.  An on-device LSD radix sort (one CTA per iteration).
+ * Status: HYD_F_BAD_LENGTH (cost = 0xFFFFFFFF), HYD_F_OVERFLOW (cost = 0xFFFFFFFF),
+ * HYD_F_ZERO_COST (cost = 0).  No workspace. */
+int hyd_cost_table(const uint32_t* len, int n_iter, int batch, const hyd_scheme* schemes,
+                   int n_schemes, int k_pad, uint32_t* sorted_len, uint32_t* perm, uint32_t* cost,
+                   uint32_t* status, void* stream);
+
+/* ---- a3: stage 1 dispatch (Eq. 2/3, Alg. 1) ---------------------------------------------
+ * cand [n_cand][32] u8 scheme indices (pipelines j = 0..cand_np[c]-1 in canonical order,
+ * i.e. MaxLen non-increasing, scheme index ascending on ties), cand_np [n_cand] u8.
+ * For each (c,t), sequences in sorted order go to the feasible pipeline (MaxLen_j >= l)
+ * minimising (C_j + tau + e_j, j) where tau = T(l,P_j) and e_j = tau (PP_j - 1) for an empty
+ * pipeline, else the pipeline's extra term E_j (Alg. 1 lines 8-14 with LPT order).
+ * Outputs pipe [n_cand][n_iter][batch] u8 (pipeline of each sorted position) and
+ * lb [n_cand][n_iter] u64 = max_j (C_j + E_j) (the Eq. 3 objective).
+ * max_np = max over c of cand_np[c] (host-known; selects the kernel width). */
+int hyd_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch,
+                 int k_pad, const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
+                 const uint8_t* cand_np, int n_cand, int max_np, uint8_t* pipe, uint64_t* lb,
+                 uint32_t* status, void* stream);
+
+/* ---- a4: stage 2 packing (Eq. 1 + App. D) -------------------------------------------
+ * For each (c,t,j): the pipeline's sequences Q (sorted order), U = |Q|, S = sum l:
+ * V in [max(ceil(S/MaxLen),1), min(floor(S/UtilLen),U)] (clamped up to the lower end);
+ * LPT(V): each sequence to the least-time micro-batch that stays within MaxLen (smallest
+ * index on ties); objective (max micro-batch time)(PP-1+V); V* = argmin (objective, V);
+ * if no V in range is feasible, the smallest feasible V above it.  The search over V is
+ * pruned with exact lower bounds (never changes the result).
+ * Outputs mb [n_cand][n_iter][batch] u16 (micro-batch of each sorted position),
+ * v [n_cand][n_iter][32] u16 (V* per pipeline, 0 for empty/unused),
+ * ptime [n_cand][n_iter][32] u64 (objective of V*), makespan [n_iter][n_cand] u64
+ * (max_j ptime; UINT64_MAX if infeasible).  ws: hyd_pack_workspace() bytes; after the
+ * call completes, the u64 at ws byte offset 16 holds the number of (sequence, micro-batch)
+ * evaluations the LPT runs performed (diagnostic work counter for the roofline). */
+size_t hyd_pack_workspace(int n_iter, int batch, int n_cand, int max_np);
+int hyd_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch, int k_pad,
+             const hyd_scheme* schemes, int n_schemes, const uint8_t* cand, const uint8_t* cand_np,
+             int n_cand, int max_np, const uint8_t* pipe, uint16_t* mb, uint16_t* v,
+             uint64_t* ptime, uint64_t* makespan, uint32_t* status, void* ws, size_t ws_bytes,
+             void* stream);
+
+/* ---- a5: selection ---------------------------------------------------------------------
+ * key[t] = min over c of (makespan[t][c] << 20 | (c + cand_offset)) among feasible
+ * candidates with makespan < 2^43 (others: HYD_F_KEY_RANGE); INT64_MAX if none.  The
+ * minimum key is the argmin of (makespan, c).  Across ranks, an allreduce(MIN) of key
+ * (a6, done by the caller over NCCL) yields the global winner. */
+int hyd_select_best(const uint64_t* makespan, int n_iter, int n_cand, int cand_offset,
+                    int64_t* key, uint32_t* status, void* stream);
+
+/* ---- winner extraction ---------------------------------------------------------------
+ * For every t whose winning candidate (key[t] & (2^20-1)) - cand_offset lies in
+ * [0, n_cand): win_pipe[t][perm[t][i]] = pipe[c][t][i], win_mb[t][perm[t][i]] = mb[c][t][i]
+ * (ORIGINAL sequence order), win_v[t][:] = v[c][t][:], win_ptime[t][:] = ptime[c][t][:].
+ * Rows of other iterations are left untouched.  Returns nothing per t; see key. */
+int hyd_gather_winners(const int64_t* key, const uint32_t* perm, const uint8_t* pipe,
+                       const uint16_t* mb, const uint16_t* v, const uint64_t* ptime, int n_iter,
+                       int batch, int n_cand, int cand_offset, uint8_t* win_pipe, uint16_t* win_mb,
+                       uint16_t* win_v, uint64_t* win_ptime, void* stream);
+
+/* ---- end-to-end call on HOST buffers -----------------------------------------------------
+ * Copies len_host [n_iter][batch] (and the scheme/candidate tables) to the device, runs
+ * a1-a5, calls reduce(key_dev, n_iter, user, stream) if non-null (the a6 allreduce-MIN over
+ * the caller's process group; must be stream-ordered), gathers the winners and copies
+ * key_host [n_iter], win_pipe_host [n_iter][batch], win_mb_host [n_iter][batch] (original
+ * order; rows of iterations won by another rank are unspecified), win_v_host/win_ptime_host
+ * [n_iter][32] and *status_host back, then synchronises `stream`.  Pinned host memory
+ * gives asynchronous copies.  ws: hyd_assign_workspace() bytes of device memory. */
+typedef int (*hyd_reduce_fn)(int64_t* key_dev, int n_iter, void* user, void* stream);
+size_t hyd_assign_workspace(int n_iter, int batch, int n_schemes, int k_pad, int n_cand, int max_np);
+/* byte offset of the device key buffer [n_iter] i64 inside the assign workspace */
+size_t hyd_assign_key_offset(int n_iter, int batch, int n_schemes, int k_pad, int n_cand, int max_np);
+int hyd_assign_host(const uint32_t* len_host, int n_iter, int batch, const hyd_scheme* schemes_host,
+                    int n_schemes, int k_pad, const uint8_t* cand_host, const uint8_t* cand_np_host,
+                    int n_cand, int cand_offset, int64_t* key_host, uint8_t* win_pipe_host,
+                    uint16_t* win_mb_host, uint16_t* win_v_host, uint64_t* win_ptime_host,
+                    uint32_t* status_host, hyd_reduce_fn reduce, void* reduce_user, void* ws,
+                    size_t ws_bytes, void* stream);
+
+/* ---- host utilities --------------------------------------------------------------------
+ * hyd_check_candidates: HOST tables; HYD_OK, HYD_E_INVALID or HYD_E_NOT_CANONICAL; writes
+ * max over c of cand_np to *max_np_out (if non-null). */
+int hyd_check_candidates(const uint8_t* cand_host, const uint8_t* cand_np_host, int n_cand,
+                         const hyd_scheme* schemes_host, int n_schemes, int* max_np_out);
+const char* hyd_status_string(int code); /* static string for a HYD_E_* code */
+const char* hyd_last_cuda_error(void);   /* static string of the last CUDA error seen */
+int hyd_kernel_launches(void);           /* kernel launches issued by this library so far */
+
+#ifdef __cplusplus
+}
+#endif
+#endif

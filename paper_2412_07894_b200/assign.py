@@ -1,0 +1,246 @@
+"""Host-side driver of the two-stage assignment: device buffers, the four C-ABI calls,
+the cross-GPU argmin (a6) and shard planning.  No arithmetic of the method lives here;
+every step runs in libhyd.so's sm_100a kernels (see include/hyd.h).
+
+Multi-GPU: one process per GPU.  Candidates are split into contiguous
+blocks [rank*C/G, (rank+1)*C/G); every rank sorts and costs all iterations itself
+(redundant but tiny, avoids a broadcast); the only exchange is one
+``all_reduce(key, MIN)`` of It int64 keys over NCCL -- key = makespan << 20 | c_global,
+so the minimum key is the global argmin of (makespan, c).  With fewer candidates than
+ranks, iterations are split instead and no collective is needed.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import hyd
+
+KEY_MASK = (1 << hyd.KEY_SHIFT) - 1
+
+
+@dataclass(frozen=True)
+class Shard:
+    cand_lo: int
+    cand_hi: int
+    iter_lo: int
+    iter_hi: int
+    by: str  # "cand" | "iter" | "none"
+
+    @property
+    def needs_reduce(self) -> bool:
+        return self.by == "cand"
+
+
+def plan_shard(n_cand: int, n_iter: int, world: int, rank: int) -> Shard:
+    """Contiguous candidate blocks; iterations when candidates are fewer than ranks."""
+    if world <= 1:
+        return Shard(0, n_cand, 0, n_iter, "none")
+    if n_cand >= world:
+        return Shard(rank * n_cand // world, (rank + 1) * n_cand // world, 0, n_iter, "cand")
+    return Shard(0, n_cand, rank * n_iter // world, (rank + 1) * n_iter // world, "iter")
+
+
+def decode_key(key):
+    """key -> (makespan, global candidate) ; (-1, -1) for an all-infeasible iteration."""
+    key = np.asarray(key, dtype=np.int64)
+    feas = key != hyd.INT64_MAX
+    ms = np.where(feas, key >> hyd.KEY_SHIFT, -1)
+    c = np.where(feas, key & KEY_MASK, -1)
+    return ms, c
+
+
+def reduce_keys(key, group=None):
+    """a6: the cross-GPU argmin -- one allreduce(MIN) of the per-iteration int64 keys."""
+    import torch.distributed as dist
+
+    dist.all_reduce(key, op=dist.ReduceOp.MIN, group=group)
+    return key
+
+
+def schemes_bytes(schemes) -> np.ndarray:
+    s = np.ascontiguousarray(schemes)
+    assert s.dtype.itemsize == 48
+    return s.view(np.uint8).reshape(-1)
+
+
+class Assigner:
+    """Device-resident buffers + the a1-a5 launch sequence for one (shard of a) workload.
+
+    ``schemes``: structured array (48-byte hyd_scheme records); ``cand`` [C][32] u8;
+    ``cand_np`` [C] u8 -- this rank's candidates, global index = cand_offset + local.
+    """
+
+    def __init__(self, schemes, cand, cand_np, n_iter, batch, k_pad, cand_offset=0, device=None):
+        import torch
+
+        self.torch = torch
+        self.dev = torch.device(device if device is not None else "cuda")
+        self.n_iter, self.batch, self.k_pad = int(n_iter), int(batch), int(k_pad)
+        self.n_schemes = int(len(schemes))
+        self.n_cand = int(cand.shape[0])
+        self.cand_offset = int(cand_offset)
+        self.max_np = hyd.check_candidates(cand, cand_np, schemes) if self.n_cand else 1
+        ml = np.zeros((self.n_cand, hyd.MAX_PIPES), np.int64)
+        for c in range(self.n_cand):
+            ks = cand[c, : int(cand_np[c])]
+            ml[c, : len(ks)] = schemes["max_len"][ks]
+        self._ml = ml
+        self._ml_k = schemes["max_len"].astype(np.int64)
+        mult = np.zeros((self.n_cand, self.n_schemes), np.int64)
+        for c in range(self.n_cand):
+            for k in cand[c, : int(cand_np[c])]:
+                mult[c, k] += 1
+        self._mult = mult
+        u8, dev = torch.uint8, self.dev
+        self.schemes = torch.from_numpy(schemes_bytes(schemes).copy()).to(dev)
+        self.cand = torch.from_numpy(np.ascontiguousarray(cand, dtype=np.uint8)).to(dev)
+        self.cand_np = torch.from_numpy(np.ascontiguousarray(cand_np, dtype=np.uint8)).to(dev)
+        It, B, Cn, kp = self.n_iter, self.batch, self.n_cand, self.k_pad
+        i32 = torch.int32  # u32 buffers are carried as int32 storage
+        self.sorted_len = torch.empty((It, B), dtype=i32, device=dev)
+        self.perm = torch.empty((It, B), dtype=i32, device=dev)
+        self.cost = torch.empty((It, B, kp), dtype=i32, device=dev)
+        self.pipe = torch.empty((Cn, It, B), dtype=u8, device=dev)
+        self.lb = torch.empty((Cn, It), dtype=torch.int64, device=dev)
+        self.mb = torch.empty((Cn, It, B), dtype=torch.int16, device=dev)
+        self.v = torch.empty((Cn, It, hyd.MAX_PIPES), dtype=torch.int16, device=dev)
+        self.ptime = torch.empty((Cn, It, hyd.MAX_PIPES), dtype=torch.int64, device=dev)
+        self.makespan = torch.empty((It, Cn), dtype=torch.int64, device=dev)
+        self.key = torch.empty((It,), dtype=torch.int64, device=dev)
+        self.status = torch.zeros((1,), dtype=i32, device=dev)
+        self.ws = torch.empty((max(hyd.pack_workspace(It, B, Cn, self.max_np), 1),), dtype=u8, device=dev)
+
+    # a1-a5; ``len_dev`` int32/uint32-bit tensor [It][B] on the device
+    def run(self, len_dev, stream=None):
+        It, B, K, kp, Cn = self.n_iter, self.batch, self.n_schemes, self.k_pad, self.n_cand
+        hyd.cost_table(len_dev, It, B, self.schemes, K, kp, self.sorted_len, self.perm, self.cost, self.status, stream)
+        hyd.dispatch(self.sorted_len, self.cost, It, B, kp, self.schemes, K, self.cand, self.cand_np, Cn,
+                     self.max_np, self.pipe, self.lb, self.status, stream)
+        hyd.pack(self.sorted_len, self.cost, It, B, kp, self.schemes, K, self.cand, self.cand_np, Cn, self.max_np,
+                 self.pipe, self.mb, self.v, self.ptime, self.makespan, self.status, self.ws, stream)
+        hyd.select_best(self.makespan, It, Cn, self.cand_offset, self.key, self.status, stream)
+        return self.key
+
+    KERNELS_PER_RUN = 5  # sort_cost, dispatch, pack_small, pack_big, select
+
+    def pack_counters(self) -> dict:
+        """Work counter written by the last hyd_pack (include/hyd.h: u64 at ws offset 16)."""
+        self.torch.cuda.synchronize(self.dev)
+        ev = int(self.ws[16:24].cpu().numpy().view(np.uint64)[0])
+        return {"bin_evals": ev}
+
+    def dispatch_evals(self, lengths) -> int:
+        """Sum over feasible (c,t) of sum_i J_i (feasible pipelines per sequence): the
+        dispatch's algorithmic evaluation count, from the host tables (no method arithmetic)."""
+        L = np.sort(np.asarray(lengths, dtype=np.int64), axis=1)  # ascending per t
+        ml_k = self._ml_k  # MaxLen per scheme
+        # cnt[k][t] = #{i : l_i <= MaxLen_k}
+        cnt = np.stack([np.array([np.searchsorted(L[t], m, side="right") for t in range(L.shape[0])])
+                        for m in ml_k])
+        per = self._mult @ cnt  # [C][It]
+        feas = L[:, -1][None, :] <= self._ml[:, 0][:, None]
+        return int(per[feas].sum())
+
+    def status_bits(self) -> int:
+        return int(self.status.item()) & 0xFFFFFFFF
+
+    def numpy(self) -> dict:
+        """All outputs as numpy arrays with the C ABI's unsigned dtypes."""
+        self.torch.cuda.synchronize(self.dev)
+
+        def u(t, dt):
+            return t.cpu().numpy().view(dt)
+
+        return dict(
+            sorted_len=u(self.sorted_len, np.uint32),
+            perm=u(self.perm, np.uint32),
+            cost=u(self.cost, np.uint32),
+            pipe=u(self.pipe, np.uint8),
+            lb=u(self.lb, np.uint64),
+            mb=u(self.mb, np.uint16),
+            v=u(self.v, np.uint16),
+            ptime=u(self.ptime, np.uint64),
+            makespan=u(self.makespan, np.uint64),
+            key=u(self.key, np.int64),
+            status=self.status_bits(),
+        )
+
+
+def lengths_to_device(lengths, device=None):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(lengths, dtype=np.uint32).view(np.int32)).to(
+        device if device is not None else "cuda"
+    )
+
+
+class HostAssigner:
+    """End-to-end path on HOST buffers through ``hyd_assign_host`` (the user-facing call).
+
+    Per call: H2D of the lengths (and tables), a1-a5 on the device, the optional
+    allreduce callback (a6), winner gather, D2H of keys + winners' plans in ORIGINAL
+    sequence order, one stream synchronisation.
+    """
+
+    def __init__(self, schemes, cand, cand_np, n_iter, batch, k_pad, cand_offset=0, group=None, reduce=False):
+        import torch
+
+        self.torch = torch
+        self.n_iter, self.batch, self.k_pad = int(n_iter), int(batch), int(k_pad)
+        self.schemes = np.ascontiguousarray(schemes)
+        self.cand = np.ascontiguousarray(cand, dtype=np.uint8)
+        self.cand_np = np.ascontiguousarray(cand_np, dtype=np.uint8)
+        self.n_cand = int(self.cand.shape[0])
+        self.cand_offset = int(cand_offset)
+        self.max_np = hyd.check_candidates(self.cand, self.cand_np, self.schemes) if self.n_cand else 1
+        args = (self.n_iter, self.batch, len(self.schemes), self.k_pad, self.n_cand, self.max_np)
+        self.ws = torch.empty((hyd.assign_workspace(*args),), dtype=torch.uint8, device="cuda")
+        koff = hyd.assign_key_offset(*args)
+        self.key_view = self.ws[koff : koff + 8 * self.n_iter].view(torch.int64)
+        pin = dict(pin_memory=True)
+        It, B = self.n_iter, self.batch
+        self.key = torch.empty((It,), dtype=torch.int64, **pin)
+        self.win_pipe = torch.empty((It, B), dtype=torch.uint8, **pin)
+        self.win_mb = torch.empty((It, B), dtype=torch.int16, **pin)
+        self.win_v = torch.empty((It, hyd.MAX_PIPES), dtype=torch.int16, **pin)
+        self.win_ptime = torch.empty((It, hyd.MAX_PIPES), dtype=torch.int64, **pin)
+        self.status = torch.zeros((1,), dtype=torch.int32, **pin)
+        self.group = group
+        self._cb = None
+        if reduce:
+            def _reduce(key_ptr, n, user, stream):
+                try:
+                    assert key_ptr == self.key_view.data_ptr() and n == self.n_iter
+                    reduce_keys(self.key_view, self.group)
+                    return 0
+                except Exception:  # reported as HYD_E_REDUCE
+                    return 1
+
+            self._cb = hyd.REDUCE_FN(_reduce)
+        # host copies of the (fixed) tables, pinned
+        self._sch = torch.from_numpy(schemes_bytes(self.schemes).copy()).pin_memory()
+        self._cand = torch.from_numpy(self.cand.copy()).pin_memory()
+        self._cnp = torch.from_numpy(self.cand_np.copy()).pin_memory()
+
+    @property
+    def h2d_bytes_fixed(self) -> int:
+        return self._sch.numel() + self._cand.numel() + self._cnp.numel()
+
+    @property
+    def d2h_bytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in (self.key, self.win_pipe, self.win_mb, self.win_v,
+                                                          self.win_ptime, self.status))
+
+    def __call__(self, len_host, stream=None):
+        """``len_host``: pinned int32 torch tensor [It][B] (u32 bit pattern)."""
+        It, B = self.n_iter, self.batch
+        assert len_host.is_pinned() and tuple(len_host.shape) == (It, B)
+        hyd.assign_host(
+            len_host.data_ptr(), It, B, self._sch.data_ptr(), len(self.schemes), self.k_pad, self._cand.data_ptr(),
+            self._cnp.data_ptr(), self.n_cand, self.cand_offset, self.key.data_ptr(), self.win_pipe.data_ptr(),
+            self.win_mb.data_ptr(), self.win_v.data_ptr(), self.win_ptime.data_ptr(), self.status.data_ptr(),
+            self._cb, self.ws, stream,
+        )
+        return self.key

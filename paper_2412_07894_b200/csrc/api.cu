@@ -1,0 +1,282 @@
+// api.cu -- the extern "C" boundary of libhyd.so (include/hyd.h): host-side validation,
+// launch planning, workspace layout and the end-to-end host-buffer call.
+#include <atomic>
+#include <cstring>
+
+#include "hyd_internal.cuh"
+
+namespace hyd {
+
+int launch_sort_cost(const uint32_t*, int, int, const hyd_scheme*, int, int, uint32_t*, uint32_t*,
+                     uint32_t*, uint32_t*, cudaStream_t);
+int launch_dispatch(const uint32_t*, const uint32_t*, int, int, int, const hyd_scheme*, int,
+                    const uint8_t*, const uint8_t*, int, int, uint8_t*, uint64_t*, uint32_t*,
+                    cudaStream_t);
+size_t pack_workspace(int, int, int, int);
+int launch_pack(const uint32_t*, const uint32_t*, int, int, int, const hyd_scheme*, int,
+                const uint8_t*, const uint8_t*, int, int, const uint8_t*, uint16_t*, uint16_t*,
+                uint64_t*, uint64_t*, uint32_t*, void*, size_t, cudaStream_t);
+int launch_select(const uint64_t*, int, int, int, int64_t*, uint32_t*, cudaStream_t);
+int launch_gather(const int64_t*, const uint32_t*, const uint8_t*, const uint16_t*, const uint16_t*,
+                  const uint64_t*, int, int, int, int, uint8_t*, uint16_t*, uint16_t*, uint64_t*,
+                  cudaStream_t);
+
+static std::atomic<int> g_launches{0};
+static thread_local char g_err[256] = "no CUDA error";
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int record_cuda_error(cudaError_t e) {
+  std::strncpy(g_err, cudaGetErrorString(e), sizeof(g_err) - 1);
+  g_err[sizeof(g_err) - 1] = 0;
+  return HYD_E_CUDA;
+}
+
+static bool common_ok(int n_iter, int batch, int n_schemes, int k_pad) {
+  return n_iter >= 0 && batch >= 1 && batch <= HYD_MAX_BATCH && n_schemes >= 1 &&
+         n_schemes <= HYD_MAX_SCHEMES && k_pad >= n_schemes && (k_pad % 4) == 0 &&
+         k_pad <= HYD_MAX_SCHEMES;
+}
+
+static bool cand_ok(int n_cand, int max_np) {
+  return n_cand >= 0 && n_cand <= (1 << HYD_KEY_SHIFT) && max_np >= 1 && max_np <= HYD_MAX_PIPES;
+}
+
+static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct AssignLayout {
+  size_t len, schemes, cand, cand_np, sorted, perm, cost, pipe, lb, mb, v, ptime, makespan, key,
+      status, win_pipe, win_mb, win_v, win_ptime, pack_ws, pack_bytes, total;
+};
+
+static AssignLayout assign_layout(int n_iter, int batch, int n_schemes, int k_pad, int n_cand,
+                                  int max_np) {
+  AssignLayout L;
+  const size_t It = (size_t)n_iter, B = (size_t)batch, Cn = (size_t)n_cand;
+  size_t o = 0;
+  auto put = [&](size_t bytes) {
+    const size_t at = o;
+    o += al(bytes);
+    return at;
+  };
+  L.len = put(It * B * 4);
+  L.schemes = put((size_t)n_schemes * sizeof(hyd_scheme));
+  L.cand = put(Cn * HYD_MAX_PIPES);
+  L.cand_np = put(Cn);
+  L.sorted = put(It * B * 4);
+  L.perm = put(It * B * 4);
+  L.cost = put(It * B * (size_t)k_pad * 4);
+  L.pipe = put(Cn * It * B);
+  L.lb = put(Cn * It * 8);
+  L.mb = put(Cn * It * B * 2);
+  L.v = put(Cn * It * HYD_MAX_PIPES * 2);
+  L.ptime = put(Cn * It * HYD_MAX_PIPES * 8);
+  L.makespan = put(It * Cn * 8);
+  L.key = put(It * 8);
+  L.status = put(4);
+  L.win_pipe = put(It * B);
+  L.win_mb = put(It * B * 2);
+  L.win_v = put(It * HYD_MAX_PIPES * 2);
+  L.win_ptime = put(It * HYD_MAX_PIPES * 8);
+  L.pack_bytes = pack_workspace(n_iter, batch, n_cand, max_np);
+  L.pack_ws = put(L.pack_bytes);
+  L.total = o;
+  return L;
+}
+
+}  // namespace hyd
+
+using namespace hyd;
+
+extern "C" {
+
+const char* hyd_status_string(int code) {
+  switch (code) {
+    case HYD_OK: return "ok";
+    case HYD_E_INVALID: return "invalid argument (null pointer, size or limit)";
+    case HYD_E_NOT_CANONICAL: return "candidate pipelines not in canonical (MaxLen desc, index asc) order";
+    case HYD_E_OVERFLOW: return "cost overflow";
+    case HYD_E_ZERO_COST: return "zero cost";
+    case HYD_E_CUDA: return "CUDA error";
+    case HYD_E_WORKSPACE: return "workspace missing or too small";
+    case HYD_E_REDUCE: return "allreduce callback failed";
+    default: return "unknown status";
+  }
+}
+
+const char* hyd_last_cuda_error(void) { return g_err; }
+
+int hyd_kernel_launches(void) { return g_launches.load(); }
+
+int hyd_check_candidates(const uint8_t* cand_host, const uint8_t* cand_np_host, int n_cand,
+                         const hyd_scheme* schemes_host, int n_schemes, int* max_np_out) {
+  if (!cand_host || !cand_np_host || !schemes_host || n_cand < 0 || n_schemes < 1 ||
+      n_schemes > HYD_MAX_SCHEMES)
+    return HYD_E_INVALID;
+  int mx = 0;
+  for (int c = 0; c < n_cand; ++c) {
+    const int np = cand_np_host[c];
+    if (np < 1 || np > HYD_MAX_PIPES) return HYD_E_INVALID;
+    mx = np > mx ? np : mx;
+    for (int j = 0; j < np; ++j) {
+      const int k = cand_host[(size_t)c * HYD_MAX_PIPES + j];
+      if (k >= n_schemes) return HYD_E_INVALID;
+      const hyd_scheme& s = schemes_host[k];
+      if (s.max_len < 1 || s.pp < 1 || s.pp > HYD_MAX_PP) return HYD_E_INVALID;
+      if (j > 0) {
+        const int kp = cand_host[(size_t)c * HYD_MAX_PIPES + j - 1];
+        const uint32_t mp = schemes_host[kp].max_len;
+        if (s.max_len > mp || (s.max_len == mp && k < kp)) return HYD_E_NOT_CANONICAL;
+      }
+    }
+  }
+  if (max_np_out) *max_np_out = mx;
+  return HYD_OK;
+}
+
+int hyd_cost_table(const uint32_t* len, int n_iter, int batch, const hyd_scheme* schemes,
+                   int n_schemes, int k_pad, uint32_t* sorted_len, uint32_t* perm, uint32_t* cost,
+                   uint32_t* status, void* stream) {
+  if (!len || !schemes || !sorted_len || !perm || !cost || !status ||
+      !common_ok(n_iter, batch, n_schemes, k_pad))
+    return HYD_E_INVALID;
+  return launch_sort_cost(len, n_iter, batch, schemes, n_schemes, k_pad, sorted_len, perm, cost,
+                          status, (cudaStream_t)stream);
+}
+
+int hyd_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch,
+                 int k_pad, const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
+                 const uint8_t* cand_np, int n_cand, int max_np, uint8_t* pipe, uint64_t* lb,
+                 uint32_t* status, void* stream) {
+  if (!sorted_len || !cost || !schemes || !cand || !cand_np || !pipe || !lb || !status ||
+      !common_ok(n_iter, batch, n_schemes, k_pad) || !cand_ok(n_cand, max_np))
+    return HYD_E_INVALID;
+  return launch_dispatch(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np,
+                         n_cand, max_np, pipe, lb, status, (cudaStream_t)stream);
+}
+
+size_t hyd_pack_workspace(int n_iter, int batch, int n_cand, int max_np) {
+  if (n_iter < 0 || batch < 1 || n_cand < 0 || max_np < 1) return 0;
+  return pack_workspace(n_iter, batch, n_cand, max_np);
+}
+
+int hyd_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch, int k_pad,
+             const hyd_scheme* schemes, int n_schemes, const uint8_t* cand, const uint8_t* cand_np,
+             int n_cand, int max_np, const uint8_t* pipe, uint16_t* mb, uint16_t* v,
+             uint64_t* ptime, uint64_t* makespan, uint32_t* status, void* ws, size_t ws_bytes,
+             void* stream) {
+  if (!sorted_len || !cost || !schemes || !cand || !cand_np || !pipe || !mb || !v || !ptime ||
+      !makespan || !status || !common_ok(n_iter, batch, n_schemes, k_pad) ||
+      !cand_ok(n_cand, max_np))
+    return HYD_E_INVALID;
+  if (!ws || ws_bytes < pack_workspace(n_iter, batch, n_cand, max_np)) return HYD_E_WORKSPACE;
+  return launch_pack(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np,
+                     n_cand, max_np, pipe, mb, v, ptime, makespan, status, ws, ws_bytes,
+                     (cudaStream_t)stream);
+}
+
+int hyd_select_best(const uint64_t* makespan, int n_iter, int n_cand, int cand_offset,
+                    int64_t* key, uint32_t* status, void* stream) {
+  if (!makespan || !key || !status || n_iter < 0 || n_cand < 0 || cand_offset < 0 ||
+      (long long)n_cand + cand_offset > (1ll << HYD_KEY_SHIFT))
+    return HYD_E_INVALID;
+  return launch_select(makespan, n_iter, n_cand, cand_offset, key, status, (cudaStream_t)stream);
+}
+
+int hyd_gather_winners(const int64_t* key, const uint32_t* perm, const uint8_t* pipe,
+                       const uint16_t* mb, const uint16_t* v, const uint64_t* ptime, int n_iter,
+                       int batch, int n_cand, int cand_offset, uint8_t* win_pipe, uint16_t* win_mb,
+                       uint16_t* win_v, uint64_t* win_ptime, void* stream) {
+  if (!key || !perm || !pipe || !mb || !v || !ptime || !win_pipe || !win_mb || !win_v ||
+      !win_ptime || n_iter < 0 || batch < 1 || batch > HYD_MAX_BATCH || n_cand < 0 ||
+      cand_offset < 0)
+    return HYD_E_INVALID;
+  return launch_gather(key, perm, pipe, mb, v, ptime, n_iter, batch, n_cand, cand_offset, win_pipe,
+                       win_mb, win_v, win_ptime, (cudaStream_t)stream);
+}
+
+size_t hyd_assign_workspace(int n_iter, int batch, int n_schemes, int k_pad, int n_cand, int max_np) {
+  if (!common_ok(n_iter, batch, n_schemes, k_pad) || !cand_ok(n_cand, max_np)) return 0;
+  return assign_layout(n_iter, batch, n_schemes, k_pad, n_cand, max_np).total;
+}
+
+size_t hyd_assign_key_offset(int n_iter, int batch, int n_schemes, int k_pad, int n_cand, int max_np) {
+  return assign_layout(n_iter, batch, n_schemes, k_pad, n_cand, max_np).key;
+}
+
+int hyd_assign_host(const uint32_t* len_host, int n_iter, int batch, const hyd_scheme* schemes_host,
+                    int n_schemes, int k_pad, const uint8_t* cand_host, const uint8_t* cand_np_host,
+                    int n_cand, int cand_offset, int64_t* key_host, uint8_t* win_pipe_host,
+                    uint16_t* win_mb_host, uint16_t* win_v_host, uint64_t* win_ptime_host,
+                    uint32_t* status_host, hyd_reduce_fn reduce, void* reduce_user, void* ws,
+                    size_t ws_bytes, void* stream) {
+  if (!len_host || !schemes_host || !cand_host || !cand_np_host || !key_host || !win_pipe_host ||
+      !win_mb_host || !win_v_host || !win_ptime_host || !status_host ||
+      !common_ok(n_iter, batch, n_schemes, k_pad) || cand_offset < 0 ||
+      (long long)n_cand + cand_offset > (1ll << HYD_KEY_SHIFT))
+    return HYD_E_INVALID;
+  int max_np = 0;
+  int rc = hyd_check_candidates(cand_host, cand_np_host, n_cand, schemes_host, n_schemes, &max_np);
+  if (rc != HYD_OK) return rc;
+  if (n_cand == 0) max_np = 1;
+  const AssignLayout L = assign_layout(n_iter, batch, n_schemes, k_pad, n_cand, max_np);
+  if (!ws || ws_bytes < L.total) return HYD_E_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  char* w = static_cast<char*>(ws);
+  auto D = [&](size_t off) { return static_cast<void*>(w + off); };
+  const size_t It = (size_t)n_iter, B = (size_t)batch, Cn = (size_t)n_cand;
+  cudaError_t e;
+#define HYD_CK(x)                                      \
+  do {                                                 \
+    e = (x);                                           \
+    if (e != cudaSuccess) return record_cuda_error(e); \
+  } while (0)
+  HYD_CK(cudaMemsetAsync(D(L.status), 0, 4, s));
+  HYD_CK(cudaMemcpyAsync(D(L.len), len_host, It * B * 4, cudaMemcpyHostToDevice, s));
+  HYD_CK(cudaMemcpyAsync(D(L.schemes), schemes_host, (size_t)n_schemes * sizeof(hyd_scheme),
+                         cudaMemcpyHostToDevice, s));
+  if (Cn) {
+    HYD_CK(cudaMemcpyAsync(D(L.cand), cand_host, Cn * HYD_MAX_PIPES, cudaMemcpyHostToDevice, s));
+    HYD_CK(cudaMemcpyAsync(D(L.cand_np), cand_np_host, Cn, cudaMemcpyHostToDevice, s));
+  }
+  uint32_t* st = static_cast<uint32_t*>(D(L.status));
+  auto* sorted = static_cast<uint32_t*>(D(L.sorted));
+  auto* perm = static_cast<uint32_t*>(D(L.perm));
+  auto* cost = static_cast<uint32_t*>(D(L.cost));
+  auto* sch = static_cast<const hyd_scheme*>(D(L.schemes));
+  auto* cand = static_cast<const uint8_t*>(D(L.cand));
+  auto* cnp = static_cast<const uint8_t*>(D(L.cand_np));
+  auto* pipe = static_cast<uint8_t*>(D(L.pipe));
+  auto* mb = static_cast<uint16_t*>(D(L.mb));
+  auto* vv = static_cast<uint16_t*>(D(L.v));
+  auto* pt = static_cast<uint64_t*>(D(L.ptime));
+  auto* ms = static_cast<uint64_t*>(D(L.makespan));
+  auto* key = static_cast<int64_t*>(D(L.key));
+  rc = launch_sort_cost(static_cast<const uint32_t*>(D(L.len)), n_iter, batch, sch, n_schemes, k_pad,
+                        sorted, perm, cost, st, s);
+  if (rc) return rc;
+  rc = launch_dispatch(sorted, cost, n_iter, batch, k_pad, sch, n_schemes, cand, cnp, n_cand, max_np,
+                       pipe, static_cast<uint64_t*>(D(L.lb)), st, s);
+  if (rc) return rc;
+  rc = launch_pack(sorted, cost, n_iter, batch, k_pad, sch, n_schemes, cand, cnp, n_cand, max_np,
+                   pipe, mb, vv, pt, ms, st, D(L.pack_ws), L.pack_bytes, s);
+  if (rc) return rc;
+  rc = launch_select(ms, n_iter, n_cand, cand_offset, key, st, s);
+  if (rc) return rc;
+  if (reduce && reduce(key, n_iter, reduce_user, stream) != 0) return HYD_E_REDUCE;
+  rc = launch_gather(key, perm, pipe, mb, vv, pt, n_iter, batch, n_cand, cand_offset,
+                     static_cast<uint8_t*>(D(L.win_pipe)), static_cast<uint16_t*>(D(L.win_mb)),
+                     static_cast<uint16_t*>(D(L.win_v)), static_cast<uint64_t*>(D(L.win_ptime)), s);
+  if (rc) return rc;
+  HYD_CK(cudaMemcpyAsync(key_host, key, It * 8, cudaMemcpyDeviceToHost, s));
+  HYD_CK(cudaMemcpyAsync(win_pipe_host, D(L.win_pipe), It * B, cudaMemcpyDeviceToHost, s));
+  HYD_CK(cudaMemcpyAsync(win_mb_host, D(L.win_mb), It * B * 2, cudaMemcpyDeviceToHost, s));
+  HYD_CK(cudaMemcpyAsync(win_v_host, D(L.win_v), It * HYD_MAX_PIPES * 2, cudaMemcpyDeviceToHost, s));
+  HYD_CK(cudaMemcpyAsync(win_ptime_host, D(L.win_ptime), It * HYD_MAX_PIPES * 8, cudaMemcpyDeviceToHost, s));
+  HYD_CK(cudaMemcpyAsync(status_host, st, 4, cudaMemcpyDeviceToHost, s));
+  HYD_CK(cudaStreamSynchronize(s));
+#undef HYD_CK
+  return HYD_OK;
+}
+
+}  // extern "C"

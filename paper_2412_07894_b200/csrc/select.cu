@@ -1,0 +1,94 @@
+// select.cu -- a5: per-iteration argmin of makespan over candidates (step ④),
+// and the winner gather used by the end-to-end call.
+//
+// k_select: one warp per iteration, lanes stride the makespan row (coalesced 8-byte
+// loads), key = makespan << 20 | c_global (argmin of (makespan, c) == min key), then a
+// 5-step shuffle min.  Across GPUs the caller allreduces key with MIN over NCCL.
+#include "hyd_internal.cuh"
+
+namespace hyd {
+
+__global__ void __launch_bounds__(256) k_select(const uint64_t* __restrict__ makespan, int n_iter,
+                                                int n_cand, int cand_offset,
+                                                int64_t* __restrict__ key,
+                                                uint32_t* __restrict__ status) {
+  const int w = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= n_iter) return;
+  const uint64_t* row = makespan + (size_t)w * n_cand;
+  long long best = 0x7FFFFFFFFFFFFFFFll;
+  uint32_t st = 0;
+  for (int c = lane; c < n_cand; c += 32) {
+    const uint64_t m = __ldg(reinterpret_cast<const unsigned long long*>(row) + c);
+    if (m == ~0ull) continue;  // infeasible candidate
+    if (m >= HYD_MAKESPAN_LIMIT) {
+      st |= HYD_F_KEY_RANGE;
+      continue;
+    }
+    const long long k = (long long)((m << HYD_KEY_SHIFT) | (uint64_t)(c + cand_offset));
+    best = k < best ? k : best;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long y = __shfl_xor_sync(HYD_FULL, best, o);
+    best = y < best ? y : best;
+  }
+  st = __reduce_or_sync(HYD_FULL, st);
+  if (lane == 0) {
+    key[w] = best;
+    if (st) atomicOr(status, st);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_gather(const int64_t* __restrict__ key,
+                                                const uint32_t* __restrict__ perm,
+                                                const uint8_t* __restrict__ pipe,
+                                                const uint16_t* __restrict__ mb,
+                                                const uint16_t* __restrict__ v,
+                                                const uint64_t* __restrict__ ptime, int n_iter,
+                                                int batch, int n_cand, int cand_offset,
+                                                uint8_t* __restrict__ win_pipe,
+                                                uint16_t* __restrict__ win_mb,
+                                                uint16_t* __restrict__ win_v,
+                                                uint64_t* __restrict__ win_ptime) {
+  const int t = blockIdx.x;
+  const long long k = key[t];
+  if (k == 0x7FFFFFFFFFFFFFFFll) return;
+  const int c = (int)(k & ((1ll << HYD_KEY_SHIFT) - 1)) - cand_offset;
+  if (c < 0 || c >= n_cand) return;  // another rank owns the winner
+  const size_t row = (size_t)c * n_iter + t;
+  const uint32_t* pr = perm + (size_t)t * batch;
+  for (int i = threadIdx.x; i < batch; i += blockDim.x) {
+    const uint32_t o = pr[i];
+    win_pipe[(size_t)t * batch + o] = pipe[row * batch + i];
+    win_mb[(size_t)t * batch + o] = mb[row * batch + i];
+  }
+  if (threadIdx.x < HYD_MAX_PIPES) {
+    win_v[(size_t)t * HYD_MAX_PIPES + threadIdx.x] = v[row * HYD_MAX_PIPES + threadIdx.x];
+    win_ptime[(size_t)t * HYD_MAX_PIPES + threadIdx.x] = ptime[row * HYD_MAX_PIPES + threadIdx.x];
+  }
+}
+
+int launch_select(const uint64_t* makespan, int n_iter, int n_cand, int cand_offset, int64_t* key,
+                  uint32_t* status, cudaStream_t s) {
+  if (n_iter == 0) return HYD_OK;
+  const int blocks = (n_iter * 32 + 255) / 256;
+  k_select<<<blocks, 256, 0, s>>>(makespan, n_iter, n_cand, cand_offset, key, status);
+  note_launch();
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? HYD_OK : record_cuda_error(e);
+}
+
+int launch_gather(const int64_t* key, const uint32_t* perm, const uint8_t* pipe, const uint16_t* mb,
+                  const uint16_t* v, const uint64_t* ptime, int n_iter, int batch, int n_cand,
+                  int cand_offset, uint8_t* win_pipe, uint16_t* win_mb, uint16_t* win_v,
+                  uint64_t* win_ptime, cudaStream_t s) {
+  if (n_iter == 0) return HYD_OK;
+  k_gather<<<n_iter, 256, 0, s>>>(key, perm, pipe, mb, v, ptime, n_iter, batch, n_cand, cand_offset,
+                                  win_pipe, win_mb, win_v, win_ptime);
+  note_launch();
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? HYD_OK : record_cuda_error(e);
+}
+
+}  // namespace hyd

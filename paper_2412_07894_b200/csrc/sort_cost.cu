@@ -1,0 +1,197 @@
+// sort_cost.cu -- a1 + a2: per-iteration stable radix sort of the lengths (length
+// descending, original index ascending) fused with the Q32 fixed-point cost table
+// T(l, P_k) = floor((a_k l^2 + b_k l + c_k) / 2^32)  (App. C.2).
+//
+// One CTA per iteration t.  The B lengths stay in shared memory; an LSD radix sort
+// over 4-bit digits (as many passes as the iteration's largest length needs) permutes
+// a u16 index array, blocked arrangement + digit-major block scan => stable.  The
+// cost rows are then written as 16-byte vector stores, consecutive threads writing
+// consecutive 16 B (k_pad % 4 == 0).  HBM traffic per t: 4B read + 8B + 4*B*k_pad write.
+#include "hyd_internal.cuh"
+
+namespace hyd {
+
+// T(l) with a 128-bit intermediate; status bits per include/hyd.h.
+__device__ __forceinline__ uint32_t eval_cost(uint64_t a, uint64_t b, uint64_t c, uint32_t l,
+                                              uint32_t& st) {
+  if (l == 0u || l > HYD_LEN_LIMIT) {
+    st |= HYD_F_BAD_LENGTH;
+    return 0xFFFFFFFFu;
+  }
+  const uint64_t l2 = (uint64_t)l * (uint64_t)l;  // < 2^49
+  uint64_t hi1, lo1, hi2, lo2;
+  mul128(a, l2, hi1, lo1);
+  mul128(b, (uint64_t)l, hi2, lo2);
+  uint64_t lo = lo1 + lo2;
+  uint64_t hi = hi1 + hi2 + (lo < lo1 ? 1ull : 0ull);
+  const uint64_t lo3 = lo + c;
+  hi += (lo3 < lo) ? 1ull : 0ull;
+  // T = (hi:lo3) >> 32 = hi * 2^32 + (lo3 >> 32): fits u32 iff hi == 0
+  if (hi != 0ull) {
+    st |= HYD_F_OVERFLOW;
+    return 0xFFFFFFFFu;
+  }
+  const uint32_t t = (uint32_t)(lo3 >> 32);
+  if (t == 0u) st |= HYD_F_ZERO_COST;
+  return t;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_sort_cost(const uint32_t* __restrict__ len, int batch,
+                                                  const hyd_scheme* __restrict__ schemes,
+                                                  int n_schemes, int k_pad,
+                                                  uint32_t* __restrict__ sorted_len,
+                                                  uint32_t* __restrict__ perm,
+                                                  uint32_t* __restrict__ cost,
+                                                  uint32_t* __restrict__ status) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int B = batch;
+  const int t = blockIdx.x;
+  const int tid = threadIdx.x;
+  // layout: lens[B] u32 | hist[16*NT] u32 | idxA[B] u16 | idxB[B] u16 | coef[3*K] u64
+  uint32_t* lens = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* hist = lens + B;
+  uint16_t* idxA = reinterpret_cast<uint16_t*>(hist + 16 * NT);
+  uint16_t* idxB = idxA + B;
+  uint64_t* coef = reinterpret_cast<uint64_t*>(smem_raw + (((size_t)B * 4 + 16 * NT * 4 + (size_t)B * 4 + 15) & ~(size_t)15));
+  __shared__ uint32_t s_or[NT / 32];
+  __shared__ uint32_t s_wsum[NT / 32];
+
+  const uint32_t* lrow = len + (size_t)t * B;
+  uint32_t orv = 0;
+  for (int i = tid; i < B; i += NT) {
+    const uint32_t l = __ldg(lrow + i);
+    lens[i] = l;
+    idxA[i] = (uint16_t)i;
+    orv |= l;
+  }
+  for (int k = tid; k < n_schemes; k += NT) {
+    coef[3 * k + 0] = schemes[k].a_q32;
+    coef[3 * k + 1] = schemes[k].b_q32;
+    coef[3 * k + 2] = schemes[k].c_q32;
+  }
+  orv = __reduce_or_sync(HYD_FULL, orv);
+  if ((tid & 31) == 0) s_or[tid >> 5] = orv;
+  __syncthreads();
+  if (tid < 32) {
+    uint32_t v = tid < NT / 32 ? s_or[tid] : 0u;
+    v = __reduce_or_sync(HYD_FULL, v);
+    if (tid == 0) s_or[0] = v;
+  }
+  __syncthreads();
+  const uint32_t all_or = s_or[0];
+  const int nbits = all_or ? 32 - __clz(all_or) : 1;
+  const int passes = (nbits + 3) >> 2;
+
+  const int ipt = (B + NT - 1) / NT;  // blocked arrangement: thread owns [lo, hi)
+  const int lo = min(B, tid * ipt), hi = min(B, lo + ipt);
+  uint16_t* src = idxA;
+  uint16_t* dst = idxB;
+  for (int p = 0; p < passes; ++p) {
+    const int shift = 4 * p;
+#pragma unroll
+    for (int d = 0; d < 16; ++d) hist[d * NT + tid] = 0u;
+    for (int q = lo; q < hi; ++q) {
+      const uint32_t d = 15u - ((lens[src[q]] >> shift) & 15u);  // descending digits
+      hist[d * NT + tid] += 1u;
+    }
+    __syncthreads();
+    // exclusive scan of hist (digit-major) : thread tid scans entries [16*tid, 16*tid+16)
+    uint32_t run = 0;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) run += hist[16 * tid + e];
+    uint32_t incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(HYD_FULL, incl, o);
+      if ((tid & 31) >= o) incl += y;
+    }
+    if ((tid & 31) == 31) s_wsum[tid >> 5] = incl;
+    __syncthreads();
+    if (tid < 32) {
+      uint32_t v = tid < NT / 32 ? s_wsum[tid] : 0u;
+      uint32_t inc2 = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(HYD_FULL, inc2, o);
+        if (tid >= o) inc2 += y;
+      }
+      if (tid < NT / 32) s_wsum[tid] = inc2 - v;  // exclusive warp offsets
+    }
+    __syncthreads();
+    uint32_t base = s_wsum[tid >> 5] + incl - run;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const uint32_t h = hist[16 * tid + e];
+      hist[16 * tid + e] = base;
+      base += h;
+    }
+    __syncthreads();
+    for (int q = lo; q < hi; ++q) {
+      const uint16_t ix = src[q];
+      const uint32_t d = 15u - ((lens[ix] >> shift) & 15u);
+      const uint32_t pos = hist[d * NT + tid];
+      hist[d * NT + tid] = pos + 1u;
+      dst[pos] = ix;
+    }
+    __syncthreads();
+    uint16_t* tmp = src;
+    src = dst;
+    dst = tmp;
+  }
+
+  uint32_t* srow = sorted_len + (size_t)t * B;
+  uint32_t* prow = perm + (size_t)t * B;
+  for (int i = tid; i < B; i += NT) {
+    const uint32_t ix = src[i];
+    srow[i] = lens[ix];
+    prow[i] = ix;
+  }
+  // cost rows: thread handles (i, quad) pairs, consecutive threads -> consecutive 16 B
+  uint32_t st = 0;
+  const int quads = k_pad >> 2;
+  uint4* crow = reinterpret_cast<uint4*>(cost + (size_t)t * B * k_pad);
+  for (int e = tid; e < B * quads; e += NT) {
+    const int i = e / quads, q = e - i * quads;
+    const uint32_t l = lens[src[i]];
+    uint32_t out[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int k = 4 * q + r;
+      out[r] = k < n_schemes ? eval_cost(coef[3 * k], coef[3 * k + 1], coef[3 * k + 2], l, st) : 0u;
+    }
+    crow[e] = make_uint4(out[0], out[1], out[2], out[3]);
+  }
+  st = __reduce_or_sync(HYD_FULL, st);
+  if (st && (tid & 31) == 0) atomicOr(status, st);
+}
+
+size_t sort_cost_smem(int batch, int nt, int n_schemes) {
+  return (((size_t)batch * 4 + 16 * (size_t)nt * 4 + (size_t)batch * 4 + 15) & ~(size_t)15) +
+         (size_t)n_schemes * 24;
+}
+
+int launch_sort_cost(const uint32_t* len, int n_iter, int batch, const hyd_scheme* schemes,
+                     int n_schemes, int k_pad, uint32_t* sorted_len, uint32_t* perm, uint32_t* cost,
+                     uint32_t* status, cudaStream_t s) {
+  if (n_iter == 0) return HYD_OK;
+  cudaError_t e;
+  if (batch <= 2048) {
+    const size_t sm = sort_cost_smem(batch, 256, n_schemes);
+    e = cudaFuncSetAttribute(k_sort_cost<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return record_cuda_error(e);
+    k_sort_cost<256><<<n_iter, 256, sm, s>>>(len, batch, schemes, n_schemes, k_pad, sorted_len,
+                                              perm, cost, status);
+  } else {
+    const size_t sm = sort_cost_smem(batch, 1024, n_schemes);
+    e = cudaFuncSetAttribute(k_sort_cost<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return record_cuda_error(e);
+    k_sort_cost<1024><<<n_iter, 1024, sm, s>>>(len, batch, schemes, n_schemes, k_pad, sorted_len,
+                                                perm, cost, status);
+  }
+  note_launch();
+  e = cudaGetLastError();
+  return e == cudaSuccess ? HYD_OK : record_cuda_error(e);
+}
+
+}  // namespace hyd
