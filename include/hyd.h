@@ -25,7 +25,8 @@
  *     original index ascending); perm[t][i] is the original index of position i.
  *   - Limits: 1 <= batch <= HYD_MAX_BATCH; 1 <= n_schemes <= HYD_MAX_SCHEMES;
  *     k_pad % 4 == 0 and k_pad >= n_schemes; 1 <= cand_np[c] <= max_np <= 32;
- *     1 <= pp <= HYD_MAX_PP; max_len >= 1; n_cand + cand_offset <= 2^20.
+ *     1 <= pp <= HYD_MAX_PP; max_len >= 1; n_cand + cand_offset <= 2^20 - 1 (global candidate
+ *     index <= 2^20 - 2, so no key equals the INT64_MAX "none" sentinel).
  *     Lengths must lie in [1, 2^24] (else HYD_F_BAD_LENGTH).
  */
 #ifndef HYD_H

@@ -282,13 +282,15 @@ uint64_t hydref_assign_pair(const uint32_t* sorted, const uint32_t* cost, int ba
 /* ---------------------------------------------------------------- step 7: select
  * Step ④ of the per-iteration loop ("select the optimal one" P:567):
  * winner = argmin over feasible c of (makespan, c); key = makespan * 2^20 + c_global,
- * which needs makespan < 2^43 (else KEY_RANGE, candidate excluded); INT64_MAX if none. */
+ * which needs makespan < 2^43 and c_global < 2^20 - 1 (reading 18: 2^20 - 1
+ * with makespan 2^43 - 1 would equal the INT64_MAX "none" sentinel); else KEY_RANGE and
+ * the candidate is excluded; INT64_MAX if no candidate remains. */
 int64_t hydref_select(const uint64_t* makespan, int n_cand, int cand_offset, uint32_t* status) {
   int64_t best = INT64_MAX;
   for (int c = 0; c < n_cand; ++c) {
     uint64_t m = makespan[c];
     if (m == UINT64_MAX) continue;
-    if (m >= MAKESPAN_LIMIT || (uint64_t)(c + cand_offset) >= (1ull << KEY_SHIFT)) {
+    if (m >= MAKESPAN_LIMIT || (uint64_t)(c + cand_offset) >= (1ull << KEY_SHIFT) - 1) {
       *status |= HYDREF_F_KEY_RANGE;
       continue;
     }

@@ -39,7 +39,7 @@ static bool common_ok(int n_iter, int batch, int n_schemes, int k_pad) {
 }
 
 static bool cand_ok(int n_cand, int max_np) {
-  return n_cand >= 0 && n_cand <= (1 << HYD_KEY_SHIFT) && max_np >= 1 && max_np <= HYD_MAX_PIPES;
+  return n_cand >= 0 && n_cand < (1 << HYD_KEY_SHIFT) && max_np >= 1 && max_np <= HYD_MAX_PIPES;
 }
 
 static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -178,7 +178,7 @@ int hyd_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int b
 int hyd_select_best(const uint64_t* makespan, int n_iter, int n_cand, int cand_offset,
                     int64_t* key, uint32_t* status, void* stream) {
   if (!makespan || !key || !status || n_iter < 0 || n_cand < 0 || cand_offset < 0 ||
-      (long long)n_cand + cand_offset > (1ll << HYD_KEY_SHIFT))
+      (long long)n_cand + cand_offset > (1ll << HYD_KEY_SHIFT) - 1)
     return HYD_E_INVALID;
   return launch_select(makespan, n_iter, n_cand, cand_offset, key, status, (cudaStream_t)stream);
 }
@@ -213,7 +213,7 @@ int hyd_assign_host(const uint32_t* len_host, int n_iter, int batch, const hyd_s
   if (!len_host || !schemes_host || !cand_host || !cand_np_host || !key_host || !win_pipe_host ||
       !win_mb_host || !win_v_host || !win_ptime_host || !status_host ||
       !common_ok(n_iter, batch, n_schemes, k_pad) || cand_offset < 0 ||
-      (long long)n_cand + cand_offset > (1ll << HYD_KEY_SHIFT))
+      (long long)n_cand + cand_offset > (1ll << HYD_KEY_SHIFT) - 1)
     return HYD_E_INVALID;
   int max_np = 0;
   int rc = hyd_check_candidates(cand_host, cand_np_host, n_cand, schemes_host, n_schemes, &max_np);

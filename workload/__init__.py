@@ -208,17 +208,22 @@ def canonical(schemes, ks):
     return sorted(ks, key=lambda k: (-int(schemes[k]["max_len"]), k))
 
 
-def candidate_table(rng, schemes, n_cand, n_pipes, gpu_budget, safety):
+def candidate_table(rng, schemes, n_cand, n_pipes, gpu_budget, safety, cover_len=None, p_cover=0.85):
     """Distinct multisets of ``n_pipes`` schemes with sum(GPUs) <= budget, canonical order.
 
-    Small spaces are enumerated and sampled without replacement; large ones are
-    drawn pipeline by pipeline within the remaining GPU budget, deduplicated.
+    A fraction ``p_cover`` of the candidates can hold the context length ``cover_len``
+    (their longest-MaxLen pipeline reaches it); the rest are "short-context" strategies,
+    as the strategy proposal keeps optimal strategies for every length ceiling L <= L_max
+    (§7 Problem 1).  Small spaces are enumerated and sampled without
+    replacement; large ones are drawn pipeline by pipeline within the GPU budget.
     """
     import itertools
 
     K = len(schemes)
     g = [gpus(int(s["tp"]), int(s["pp"]), int(s["cp"])) for s in schemes]
+    ml = [int(s["max_len"]) for s in schemes]
     gmin = min(g)
+    cover_len = cover_len if cover_len is not None else 0
     seen = set()
     rows = []
     if safety is not None:
@@ -226,25 +231,31 @@ def candidate_table(rng, schemes, n_cand, n_pipes, gpu_budget, safety):
         assert sum(g[k] for k in row) <= gpu_budget
         seen.add(tuple(sorted(row)))
         rows.append(row)
+    need = n_cand - len(rows)
     if math.comb(K + n_pipes - 1, n_pipes) <= 2_000_000:
         pool = [
             m
             for m in itertools.combinations_with_replacement(range(K), n_pipes)
             if sum(g[k] for k in m) <= gpu_budget and m not in seen
         ]
-        need = n_cand - len(rows)
         assert len(pool) >= need, f"only {len(pool)} distinct candidates for {need}"
-        pick = rng.permutation(len(pool))[:need]
-        rows += [tuple(canonical(schemes, list(pool[p]))) for p in pick]
+        cov = [m for m in pool if max(ml[k] for k in m) >= cover_len]
+        non = [m for m in pool if max(ml[k] for k in m) < cover_len]
+        n_cov = min(len(cov), max(need - len(non), int(round(p_cover * need))))
+        picks = [cov[i] for i in rng.permutation(len(cov))[:n_cov]]
+        picks += [non[i] for i in rng.permutation(len(non))[: need - n_cov]]
+        picks = [picks[i] for i in rng.permutation(len(picks))]
+        rows += [tuple(canonical(schemes, list(m))) for m in picks]
     else:
         tries = 0
         while len(rows) < n_cand:
             tries += 1
             assert tries < 100 * n_cand + 100000, "candidate space too small"
+            cover = rng.random() < p_cover
             ks, left = [], gpu_budget
             for r in range(n_pipes):
                 room = left - gmin * (n_pipes - r - 1)
-                ok = [k for k in range(K) if g[k] <= room]
+                ok = [k for k in range(K) if g[k] <= room and (r > 0 or not cover or ml[k] >= cover_len)]
                 k = ok[int(rng.integers(0, len(ok)))]
                 ks.append(k)
                 left -= g[k]
@@ -296,7 +307,7 @@ CONFIGS = {
     2: dict(name="cfg2-cc32k-256seq-4pipe-64cand", B=256, D=4, C=64, It=1024, budget=32, seed=202),
     3: dict(name="cfg3-gh128k-512seq-8pipe-1024cand", B=512, D=8, C=1024, It=256, budget=64, seed=303),
     4: dict(name="cfg4-70b-512seq-8pipe-4096cand", B=512, D=8, C=4096, It=1024, budget=64, seed=404),
-    5: dict(name="cfg5-stress-8192seq-16pipe-16384cand", B=8192, D=16, C=16384, It=16, budget=128, seed=505),
+    5: dict(name="cfg5-stress-8192seq-16pipe-16384cand", B=8192, D=16, C=16384, It=16, budget=256, seed=505),
 }
 
 _SHAPES = {
@@ -361,7 +372,7 @@ def make_workload(cfg: int, n_cand: int | None = None, n_iter: int | None = None
         k_long = min(longest, key=lambda k: (g[k], k))
         k_small = min(range(len(schemes)), key=lambda k: (g[k], -ml[k], k))
         safety = [k_long] + [k_small] * (D - 1)
-        cand, cand_np = candidate_table(rng_cand, schemes, C, D, p["budget"], safety=safety)
+        cand, cand_np = candidate_table(rng_cand, schemes, C, D, p["budget"], safety=safety, cover_len=maxlen_cap)
     lens = lens.reshape(full_it, B)[:It].copy()
     return Workload(
         cfg=cfg,
