@@ -232,11 +232,11 @@ def main():
         if evs:
             evs[1].record(stream)
         hyd.dispatch(A.sorted_len, A.cost, It, B, kp, A.schemes, K, A.cand, A.cand_np, Cn, A.max_np, A.pipe, A.lb,
-                     A.status)
+                     A.stats, A.status)
         if evs:
             evs[2].record(stream)
-        hyd.pack(A.sorted_len, A.cost, It, B, kp, A.schemes, K, A.cand, A.cand_np, Cn, A.max_np, A.pipe, A.mb, A.v,
-                 A.ptime, A.makespan, A.status, A.ws)
+        hyd.pack(A.sorted_len, A.cost, It, B, kp, A.schemes, K, A.cand, A.cand_np, Cn, A.max_np, A.pipe, A.stats,
+                 A.mb, A.v, A.ptime, A.makespan, A.status, A.ws)
         if evs:
             evs[3].record(stream)
         hyd.select_best(A.makespan, It, Cn, A.cand_offset, A.key, A.status)

@@ -88,21 +88,34 @@ int hyd_cost_table(const uint32_t* len, int n_iter, int batch, const hyd_scheme*
                    int n_schemes, int k_pad, uint32_t* sorted_len, uint32_t* perm, uint32_t* cost,
                    uint32_t* status, void* stream);
 
+/* Per-pipeline statistics of a dispatch, consumed by hyd_pack (24 bytes):
+ *   u = U_j (sequences dispatched to pipeline j), tau_max = T(longest of them, P_j)
+ *   (its first one in sorted order), s = S_j (their token sum), sum_t = sum of their T(l, P_j).
+ * Layout [n_cand][n_iter][max_np]; entries of infeasible (c,t) are undefined. */
+typedef struct {
+  uint32_t u;
+  uint32_t tau_max;
+  uint64_t s;
+  uint64_t sum_t;
+} hyd_pipe_stats;
+
 /* ---- a3: stage 1 dispatch (Eq. 2/3, Alg. 1) ---------------------------------------------
  * cand [n_cand][32] u8 scheme indices (pipelines j = 0..cand_np[c]-1 in canonical order,
  * i.e. MaxLen non-increasing, scheme index ascending on ties), cand_np [n_cand] u8.
  * For each (c,t), sequences in sorted order go to the feasible pipeline (MaxLen_j >= l)
  * minimising (C_j + tau + e_j, j) where tau = T(l,P_j) and e_j = tau (PP_j - 1) for an empty
  * pipeline, else the pipeline's extra term E_j (Alg. 1 lines 8-14 with LPT order).
- * Outputs pipe [n_cand][n_iter][batch] u8 (pipeline of each sorted position) and
- * lb [n_cand][n_iter] u64 = max_j (C_j + E_j) (the Eq. 3 objective).
+ * Outputs pipe [n_cand][n_iter][batch] u8 (pipeline of each sorted position),
+ * lb [n_cand][n_iter] u64 = max_j (C_j + E_j) (the Eq. 3 objective) and
+ * stats [n_cand][n_iter][max_np] (hyd_pipe_stats, for hyd_pack).
  * max_np = max over c of cand_np[c] (host-known; selects the kernel width). */
 int hyd_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch,
                  int k_pad, const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
                  const uint8_t* cand_np, int n_cand, int max_np, uint8_t* pipe, uint64_t* lb,
-                 uint32_t* status, void* stream);
+                 hyd_pipe_stats* stats, uint32_t* status, void* stream);
 
 /* ---- a4: stage 2 packing (Eq. 1 + App. D) -------------------------------------------
+ * Inputs include pipe and stats from hyd_dispatch (same n_cand/n_iter/max_np).
  * For each (c,t,j): the pipeline's sequences Q (sorted order), U = |Q|, S = sum l:
  * V in [max(ceil(S/MaxLen),1), min(floor(S/UtilLen),U)] (clamped up to the lower end);
  * LPT(V): each sequence to the least-time micro-batch that stays within MaxLen (smallest
@@ -118,7 +131,7 @@ int hyd_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, i
 size_t hyd_pack_workspace(int n_iter, int batch, int n_cand, int max_np);
 int hyd_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch, int k_pad,
              const hyd_scheme* schemes, int n_schemes, const uint8_t* cand, const uint8_t* cand_np,
-             int n_cand, int max_np, const uint8_t* pipe, uint16_t* mb, uint16_t* v,
+             int n_cand, int max_np, const uint8_t* pipe, const hyd_pipe_stats* stats, uint16_t* mb, uint16_t* v,
              uint64_t* ptime, uint64_t* makespan, uint32_t* status, void* ws, size_t ws_bytes,
              void* stream);
 

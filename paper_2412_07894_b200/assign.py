@@ -104,6 +104,7 @@ class Assigner:
         self.cost = torch.empty((It, B, kp), dtype=i32, device=dev)
         self.pipe = torch.empty((Cn, It, B), dtype=u8, device=dev)
         self.lb = torch.empty((Cn, It), dtype=torch.int64, device=dev)
+        self.stats = torch.empty((Cn, It, self.max_np, hyd.PIPE_STATS_BYTES), dtype=u8, device=dev)
         self.mb = torch.empty((Cn, It, B), dtype=torch.int16, device=dev)
         self.v = torch.empty((Cn, It, hyd.MAX_PIPES), dtype=torch.int16, device=dev)
         self.ptime = torch.empty((Cn, It, hyd.MAX_PIPES), dtype=torch.int64, device=dev)
@@ -117,13 +118,13 @@ class Assigner:
         It, B, K, kp, Cn = self.n_iter, self.batch, self.n_schemes, self.k_pad, self.n_cand
         hyd.cost_table(len_dev, It, B, self.schemes, K, kp, self.sorted_len, self.perm, self.cost, self.status, stream)
         hyd.dispatch(self.sorted_len, self.cost, It, B, kp, self.schemes, K, self.cand, self.cand_np, Cn,
-                     self.max_np, self.pipe, self.lb, self.status, stream)
+                     self.max_np, self.pipe, self.lb, self.stats, self.status, stream)
         hyd.pack(self.sorted_len, self.cost, It, B, kp, self.schemes, K, self.cand, self.cand_np, Cn, self.max_np,
-                 self.pipe, self.mb, self.v, self.ptime, self.makespan, self.status, self.ws, stream)
+                 self.pipe, self.stats, self.mb, self.v, self.ptime, self.makespan, self.status, self.ws, stream)
         hyd.select_best(self.makespan, It, Cn, self.cand_offset, self.key, self.status, stream)
         return self.key
 
-    KERNELS_PER_RUN = 5  # sort_cost, dispatch, pack_small, pack_big, select
+    KERNELS_PER_RUN = 6  # sort_cost, dispatch, pack_init, pack_lanes, pack_big, select
 
     def pack_counters(self) -> dict:
         """Work counter written by the last hyd_pack (include/hyd.h: u64 at ws offset 16)."""

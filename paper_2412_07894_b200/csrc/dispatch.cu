@@ -1,124 +1,68 @@
 // dispatch.cu -- a3: stage 1 sequence dispatching across pipelines (§6.2).
 //
 // One thread per (candidate c, iteration t).  A CTA covers `ct` candidates x `tt`
-// iterations (ct*tt <= 128), so every thread of a warp shares the iteration's sorted
+// iterations (ct*tt <= 128), so the threads of a warp share the iteration's sorted
 // lengths and cost rows; when they fit, those rows are staged in shared memory once per
-// CTA (16-byte copies) and each sequence step reads one <=64-word smem row (a single
-// wavefront: the threads' scheme indices fall in one row).  Pipeline state lives in
-// registers, unrolled over DP = next_pow2(max_np) lanes:
-//   C_j (load_j, u64), E_j (extra_j, u64), an "occupied" bit, MaxLen_j, PP_j - 1, k_j.
-// Per sequence i (longest first) and feasible j (MaxLen_j >= l_i, the horizon J_i of P:626):
-//   e_j  = occupied ? E_j : tau * (PP_j - 1)       (Eq. 2 extra term; Alg. 1 l.10)
-//   new_j = C_j + tau + e_j                          (Alg. 1 lines 9-11)
-//   j* = argmin (new_j, j)                           (SURVEY §8(c) step 4 / reading 10)
-// Decisions are packed 4 per u32 store.  Output: pipe[c][t][i], lb[c][t] = max_j C_j+E_j.
+// CTA (16-byte copies) and each sequence step reads one <= 256 B smem row.
+//
+// Per pipeline j the register state is base_j = C_j + E_j (Alg. 1's accumulators,
+// P:1136-1137) and mult_j = PP_j while the pipeline is empty, 1 afterwards.  Because the
+// sequences arrive longest first, the first one a pipeline receives fixes its extra term
+// E_j = T(l_max,P_j)(PP_j-1) (Eq. 2), so the candidate load of every feasible j is
+//   new_j = base_j + tau * mult_j      (= C_j + tau + e_j of SURVEY §8(c) step 4)
+// one IMAD; j* = argmin (new_j, j) over MaxLen_j >= l_i (J_i); base_j* = new_j*.
+// The running per-pipeline statistics U_j, S_j, tau_max,j (for the packing stage) live in
+// shared memory columns indexed by j* (one LDS/STS set per sequence, not per pipeline).
+// The sums run in u32 when a per-CTA bound proves every load < 2^32, else in u64.
+// Outputs: pipe[c][t][i] (4 decisions per u32 store), lb[c][t] = max_j base_j, stats.
 #include "hyd_internal.cuh"
 
 namespace hyd {
 
 constexpr int kDispatchThreads = 128;
 
-template <int DP, bool STAGED>
-__global__ void __launch_bounds__(kDispatchThreads)
-    k_dispatch(const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ cost,
-               int n_iter, int batch, int k_pad, const hyd_scheme* __restrict__ schemes,
-               int n_schemes, const uint8_t* __restrict__ cand, const uint8_t* __restrict__ cand_np,
-               int n_cand, int ct, int tt, uint8_t* __restrict__ pipe, uint64_t* __restrict__ lb,
-               uint32_t* __restrict__ status) {
-  extern __shared__ __align__(16) uint32_t sm[];
-  const int B = batch;
-  const int tid = threadIdx.x;
-  const int c0 = blockIdx.x * ct, t0 = blockIdx.y * tt;
-  if (STAGED) {
-    // [tt][B] lengths then [tt][B][k_pad] costs, both contiguous in global memory per t
-    const int ntt = min(tt, n_iter - t0);
-    const uint4* gl = reinterpret_cast<const uint4*>(sorted_len + (size_t)t0 * B);
-    uint4* sl4 = reinterpret_cast<uint4*>(sm);
-    const int nl = ntt * B / 4;
-    for (int e = tid; e < nl; e += kDispatchThreads) sl4[e] = __ldg(gl + e);
-    const uint4* gc = reinterpret_cast<const uint4*>(cost + (size_t)t0 * B * k_pad);
-    uint4* sc4 = reinterpret_cast<uint4*>(sm + (size_t)tt * B);
-    const int nc = ntt * B * k_pad / 4;
-    for (int e = tid; e < nc; e += kDispatchThreads) sc4[e] = __ldg(gc + e);
-    __syncthreads();
-  }
-  const int lt = tid / ct, lc = tid - lt * ct;
-  const int c = c0 + lc, t = t0 + lt;
-  if (lt >= tt || c >= n_cand || t >= n_iter) return;
-
-  const uint32_t* sl = STAGED ? sm + (size_t)lt * B : sorted_len + (size_t)t * B;
-  const uint32_t* cs = STAGED ? sm + (size_t)tt * B + (size_t)lt * B * k_pad
-                              : cost + (size_t)t * B * k_pad;
-  const size_t row = (size_t)c * n_iter + t;
-  uint8_t* prow = pipe + row * B;
-
-  // candidate: pipelines in canonical order; unused lanes get MaxLen 0 (never feasible)
-  const int np = cand_np[c];
-  uint32_t ml[DP], ppm1[DP], kk[DP];
-  bool ok = np >= 1 && np <= DP;
-  uint32_t prev_ml = 0xFFFFFFFFu, prev_k = 0;
+template <int DP, typename TT>
+__device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
+                                             const uint32_t* __restrict__ cs, bool staged, int B,
+                                             int k_pad, const uint32_t (&ml)[DP],
+                                             const uint32_t (&pp)[DP], const uint32_t (&kk)[DP],
+                                             uint8_t* __restrict__ prow, uint32_t* s_cnt,
+                                             uint32_t* s_tmax, unsigned long long* s_sum,
+                                             uint64_t& lb_out, TT (&base)[DP]) {
+  uint32_t mult[DP];
 #pragma unroll
   for (int j = 0; j < DP; ++j) {
-    ml[j] = 0u;
-    ppm1[j] = 0u;
-    kk[j] = 0u;
-    if (j < np) {
-      const uint32_t k = cand[(size_t)c * HYD_MAX_PIPES + j];
-      if (k < (uint32_t)n_schemes) {
-        const uint32_t m = schemes[k].max_len;
-        const uint32_t pp = schemes[k].pp;
-        ok = ok && (m < prev_ml || (m == prev_ml && k >= prev_k)) && pp >= 1u && pp <= HYD_MAX_PP &&
-             m >= 1u;
-        prev_ml = m;
-        prev_k = k;
-        ml[j] = m;
-        ppm1[j] = pp - 1u;
-        kk[j] = k;
-      } else {
-        ok = false;
-      }
-    }
+    base[j] = 0;
+    mult[j] = pp[j];
   }
-  if (!ok) flag(status, HYD_F_NOT_CANONICAL);
-  if (!ok || sl[0] > ml[0]) {  // infeasible candidate for this iteration (S:371, S:448)
-    for (int i = 0; i < B; ++i) prow[i] = 0xFF;
-    lb[row] = ~0ull;
-    return;
-  }
-
-  uint64_t ld[DP], ex[DP];
-#pragma unroll
-  for (int j = 0; j < DP; ++j) {
-    ld[j] = 0ull;
-    ex[j] = 0ull;
-  }
-  uint32_t occ = 0u;
   const bool words = (B & 3) == 0;
   uint32_t word = 0u;
   for (int i = 0; i < B; ++i) {
     const uint32_t l = sl[i];
     const uint32_t* crow = cs + (size_t)i * k_pad;
-    uint64_t best = ~0ull, btau = 0ull, be = 0ull;
-    uint32_t bj = 0u;
+    TT best = (TT)~(TT)0;
+    uint32_t bj = 0u, btau = 0u;
 #pragma unroll
     for (int j = 0; j < DP; ++j) {
-      const uint32_t tau = STAGED ? crow[kk[j]] : __ldg(crow + kk[j]);
-      const uint64_t e = ((occ >> j) & 1u) ? ex[j] : (uint64_t)tau * ppm1[j];
-      const uint64_t nw = ld[j] + tau + e;
+      const uint32_t tau = staged ? crow[kk[j]] : __ldg(crow + kk[j]);
+      const TT nw = base[j] + (TT)tau * (TT)mult[j];
       if (l <= ml[j] && nw < best) {
         best = nw;
         bj = (uint32_t)j;
         btau = tau;
-        be = e;
       }
     }
 #pragma unroll
     for (int j = 0; j < DP; ++j)
       if ((uint32_t)j == bj) {
-        ld[j] += btau;
-        ex[j] = be;
+        base[j] = best;
+        mult[j] = 1u;
       }
-    occ |= 1u << bj;
+    // statistics column of pipeline bj (this thread's column)
+    const uint32_t n = s_cnt[bj * kDispatchThreads];
+    if (n == 0u) s_tmax[bj * kDispatchThreads] = btau;
+    s_cnt[bj * kDispatchThreads] = n + 1u;
+    s_sum[bj * kDispatchThreads] += l;
     if (words) {
       word |= bj << (8 * (i & 3));
       if ((i & 3) == 3) {
@@ -131,27 +75,167 @@ __global__ void __launch_bounds__(kDispatchThreads)
   }
   uint64_t m = 0ull;
 #pragma unroll
-  for (int j = 0; j < DP; ++j) m = max(m, ld[j] + ex[j]);
-  lb[row] = m;
+  for (int j = 0; j < DP; ++j) m = max(m, (uint64_t)base[j]);
+  lb_out = m;
+}
+
+template <int DP, bool STAGED>
+__global__ void __launch_bounds__(kDispatchThreads)
+    k_dispatch(const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ cost,
+               int n_iter, int batch, int k_pad, const hyd_scheme* __restrict__ schemes,
+               int n_schemes, const uint8_t* __restrict__ cand, const uint8_t* __restrict__ cand_np,
+               int n_cand, int max_np, int ct, int tt, uint8_t* __restrict__ pipe,
+               uint64_t* __restrict__ lb, hyd_pipe_stats* __restrict__ stats,
+               uint32_t* __restrict__ status) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  // dynamic smem: [stage: tt*B*(1+k_pad) u32 if STAGED] [s_sum u64][s_cnt u32][s_tmax u32]
+  const size_t stage_words = STAGED ? (size_t)tt * batch * (1 + k_pad) : 0;
+  unsigned long long* s_sum = reinterpret_cast<unsigned long long*>(sm + ((stage_words + 3) & ~(size_t)3));
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_sum + DP * kDispatchThreads);
+  uint32_t* s_tmax = s_cnt + DP * kDispatchThreads;
+  __shared__ unsigned long long s_bound[kDispatchThreads / 32];
+  __shared__ uint32_t s_ppmax;
+  const int B = batch;
+  const int tid = threadIdx.x;
+  const int c0 = blockIdx.x * ct, t0 = blockIdx.y * tt;
+  const int ntt = min(tt, n_iter - t0);
+  if (STAGED) {
+    // [tt][B] lengths then [tt][B][k_pad] costs, both contiguous in global memory per t
+    const uint4* gl = reinterpret_cast<const uint4*>(sorted_len + (size_t)t0 * B);
+    uint4* sl4 = reinterpret_cast<uint4*>(sm);
+    const int nl = ntt * B / 4;
+    for (int e = tid; e < nl; e += kDispatchThreads) sl4[e] = __ldg(gl + e);
+    const uint4* gc = reinterpret_cast<const uint4*>(cost + (size_t)t0 * B * k_pad);
+    uint4* sc4 = reinterpret_cast<uint4*>(sm + (size_t)tt * B);
+    const int nc = ntt * B * k_pad / 4;
+    for (int e = tid; e < nc; e += kDispatchThreads) sc4[e] = __ldg(gc + e);
+  }
+  if (tid == 0) {
+    uint32_t m = 1u;
+    for (int k = 0; k < n_schemes; ++k) m = max(m, schemes[k].pp);
+    s_ppmax = m;
+  }
+#pragma unroll
+  for (int j = 0; j < DP; ++j) {
+    s_cnt[j * kDispatchThreads + tid] = 0u;
+    s_sum[j * kDispatchThreads + tid] = 0ull;
+  }
+  __syncthreads();
+  // u32 bound over the CTA's iterations: sum_i max_k tau_ik + max tau * (PPmax - 1) < 2^32-1
+  //  =>  every base_j and new_j of every thread fits u32 (strictly below the u32 sentinel).
+  unsigned long long bound = 0ull;
+  for (int e = tid; e < ntt * B; e += kDispatchThreads) {
+    const int lt = e / B, i = e - lt * B;
+    const uint32_t* crow = STAGED ? sm + (size_t)tt * B + ((size_t)lt * B + i) * k_pad
+                                  : cost + ((size_t)(t0 + lt) * B + i) * k_pad;
+    uint32_t mx = 0u;
+    for (int k = 0; k < n_schemes; ++k) mx = max(mx, STAGED ? crow[k] : __ldg(crow + k));
+    unsigned long long v = (unsigned long long)mx;
+    if (i == 0) v += (unsigned long long)mx * (s_ppmax - 1u);
+    bound += v;
+  }
+  for (int o = 16; o > 0; o >>= 1) bound += __shfl_xor_sync(HYD_FULL, bound, o);
+  if ((tid & 31) == 0) s_bound[tid >> 5] = bound;
+  __syncthreads();
+  bound = 0ull;
+  for (int w = 0; w < kDispatchThreads / 32; ++w) bound += s_bound[w];
+  const bool narrow = bound < 0xFFFFFFFFull;
+
+  const int lt = tid / ct, lc = tid - lt * ct;
+  const int c = c0 + lc, t = t0 + lt;
+  if (lt >= tt || c >= n_cand || t >= n_iter) return;
+
+  const uint32_t* sl = STAGED ? sm + (size_t)lt * B : sorted_len + (size_t)t * B;
+  const uint32_t* cs = STAGED ? sm + (size_t)tt * B + (size_t)lt * B * k_pad
+                              : cost + (size_t)t * B * k_pad;
+  const size_t row = (size_t)c * n_iter + t;
+  uint8_t* prow = pipe + row * B;
+
+  // candidate: pipelines in canonical order; unused lanes get MaxLen 0 (never feasible)
+  const int np = cand_np[c];
+  uint32_t ml[DP], pp[DP], kk[DP];
+  bool ok = np >= 1 && np <= DP;
+  uint32_t prev_ml = 0xFFFFFFFFu, prev_k = 0;
+#pragma unroll
+  for (int j = 0; j < DP; ++j) {
+    ml[j] = 0u;
+    pp[j] = 1u;
+    kk[j] = 0u;
+    if (j < np) {
+      const uint32_t k = cand[(size_t)c * HYD_MAX_PIPES + j];
+      if (k < (uint32_t)n_schemes) {
+        const uint32_t m = schemes[k].max_len;
+        const uint32_t p = schemes[k].pp;
+        ok = ok && (m < prev_ml || (m == prev_ml && k >= prev_k)) && p >= 1u && p <= HYD_MAX_PP &&
+             m >= 1u;
+        prev_ml = m;
+        prev_k = k;
+        ml[j] = m;
+        pp[j] = p;
+        kk[j] = k;
+      } else {
+        ok = false;
+      }
+    }
+  }
+  if (!ok) flag(status, HYD_F_NOT_CANONICAL);
+  if (!ok || sl[0] > ml[0]) {  // infeasible candidate for this iteration (S:371, S:448)
+    for (int i = 0; i < B; ++i) prow[i] = 0xFF;
+    lb[row] = ~0ull;
+    return;
+  }
+  uint32_t* cnt = s_cnt + tid;
+  uint32_t* tmx = s_tmax + tid;
+  unsigned long long* ssum = s_sum + tid;
+  uint64_t lbv = 0ull;
+  uint64_t base64[DP];
+  if (narrow) {
+    uint32_t base[DP];
+    dispatch_run<DP, uint32_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, cnt, tmx, ssum, lbv, base);
+#pragma unroll
+    for (int j = 0; j < DP; ++j) base64[j] = base[j];
+  } else {
+    dispatch_run<DP, uint64_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, cnt, tmx, ssum, lbv, base64);
+  }
+  lb[row] = lbv;
+  hyd_pipe_stats* st = stats + row * max_np;
+#pragma unroll
+  for (int j = 0; j < DP; ++j) {
+    if (j < np) {
+      const uint32_t n = cnt[j * kDispatchThreads];
+      const uint32_t tm = n ? tmx[j * kDispatchThreads] : 0u;
+      hyd_pipe_stats e;
+      e.u = n;
+      e.tau_max = tm;
+      e.s = ssum[j * kDispatchThreads];
+      e.sum_t = base64[j] - (uint64_t)tm * (pp[j] - 1u);  // base_j = C_j + E_j
+      st[j] = e;
+    }
+  }
 }
 
 template <int DP>
-static cudaError_t launch_dp(bool staged, dim3 grid, size_t smem, cudaStream_t s,
+static cudaError_t launch_dp(bool staged, dim3 grid, size_t smem_stage, cudaStream_t s,
                              const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch,
                              int k_pad, const hyd_scheme* schemes, int n_schemes,
-                             const uint8_t* cand, const uint8_t* cand_np, int n_cand, int ct,
-                             int tt, uint8_t* pipe, uint64_t* lb, uint32_t* status) {
+                             const uint8_t* cand, const uint8_t* cand_np, int n_cand, int max_np,
+                             int ct, int tt, uint8_t* pipe, uint64_t* lb, hyd_pipe_stats* stats,
+                             uint32_t* status) {
+  const size_t cols = (size_t)DP * kDispatchThreads * 16;
+  cudaError_t e;
   if (staged) {
-    cudaError_t e = cudaFuncSetAttribute(k_dispatch<DP, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = ((smem_stage + 15) & ~(size_t)15) + cols;
+    e = cudaFuncSetAttribute(k_dispatch<DP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_dispatch<DP, true><<<grid, kDispatchThreads, smem, s>>>(
-        sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, ct, tt,
-        pipe, lb, status);
+        sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np,
+        ct, tt, pipe, lb, stats, status);
   } else {
-    k_dispatch<DP, false><<<grid, kDispatchThreads, 0, s>>>(
-        sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, ct, tt,
-        pipe, lb, status);
+    e = cudaFuncSetAttribute(k_dispatch<DP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols);
+    if (e != cudaSuccess) return e;
+    k_dispatch<DP, false><<<grid, kDispatchThreads, cols, s>>>(
+        sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np,
+        ct, tt, pipe, lb, stats, status);
   }
   return cudaGetLastError();
 }
@@ -159,22 +243,23 @@ static cudaError_t launch_dp(bool staged, dim3 grid, size_t smem, cudaStream_t s
 int launch_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch,
                     int k_pad, const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
                     const uint8_t* cand_np, int n_cand, int max_np, uint8_t* pipe, uint64_t* lb,
-                    uint32_t* status, cudaStream_t s) {
+                    hyd_pipe_stats* stats, uint32_t* status, cudaStream_t s) {
   if (n_iter == 0 || n_cand == 0) return HYD_OK;
   const int ct = n_cand < kDispatchThreads ? n_cand : kDispatchThreads;
   const int tt = kDispatchThreads / ct;
   const size_t smem = (size_t)tt * batch * 4 * (1 + (size_t)k_pad);
+  const int dp = max_np <= 2 ? 2 : max_np <= 4 ? 4 : max_np <= 8 ? 8 : max_np <= 16 ? 16 : 32;
+  const size_t static_smem = (size_t)dp * kDispatchThreads * 16 + 64;
   // stage when the rows fit comfortably (leaves room for several CTAs per SM)
-  const bool staged = smem <= 96 * 1024 && (batch % 4) == 0;
+  const bool staged = smem + static_smem <= 96 * 1024 && (batch % 4) == 0;
   dim3 grid((n_cand + ct - 1) / ct, (n_iter + tt - 1) / tt);
   cudaError_t e;
-  const int dp = max_np <= 2 ? 2 : max_np <= 4 ? 4 : max_np <= 8 ? 8 : max_np <= 16 ? 16 : 32;
   switch (dp) {
-    case 2: e = launch_dp<2>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, ct, tt, pipe, lb, status); break;
-    case 4: e = launch_dp<4>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, ct, tt, pipe, lb, status); break;
-    case 8: e = launch_dp<8>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, ct, tt, pipe, lb, status); break;
-    case 16: e = launch_dp<16>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, ct, tt, pipe, lb, status); break;
-    default: e = launch_dp<32>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, ct, tt, pipe, lb, status); break;
+    case 2: e = launch_dp<2>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, status); break;
+    case 4: e = launch_dp<4>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, status); break;
+    case 8: e = launch_dp<8>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, status); break;
+    case 16: e = launch_dp<16>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, status); break;
+    default: e = launch_dp<32>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, status); break;
   }
   note_launch();
   return e == cudaSuccess ? HYD_OK : record_cuda_error(e);

@@ -18,24 +18,28 @@
 //   A completed run therefore always improves (obj, V); its bin ids (kept in shared memory)
 //   are then copied to mb.
 //
-// Two kernels:
-//   k_pack_small: one LANE per pipeline (DP = next_pow2(max_np) lanes per (c,t), 32/DP
-//     pairs per warp), member lists built in shared memory from the pipe row with SIMD byte
-//     compares, bins in registers for V <= 32 (unrolled to a warp-uniform VMAX of 4/8/16/32),
-//     u32 bin times when the pipeline's sumT < 2^32-1.  A lane whose search needs V > 32 is
-//     pushed to a work queue instead.
-//   k_pack_big: persistent warps pop (c,t,j) tasks; the WARP owns one pipeline, lanes own
-//     bins b = lane + 32 r (r < R <= 8 in registers, or global scratch beyond 256 bins);
-//     per item a redux.sync min over times, then over bin ids, picks the bin.
-//   makespan[t][c] = max_j ptime: written by k_pack_small over its lanes, completed with
-//   atomicMax by k_pack_big for queued pipelines.
+// Three kernels (all stream-ordered after hyd_dispatch, which supplies U, S, sumT, tau_max):
+//   k_pack_init: per (c,t) makespan = 0 / UINT64_MAX, v/ptime rows zeroed, infeasible mb rows.
+//   k_pack_lanes: one LANE per pipeline task, persistent inside a CTA that owns one iteration
+//     (its lengths + cost rows staged in smem) and ~2048 (c,j) tasks sorted into VMAX classes
+//     8 / 16 by V_a.  Each loop iteration advances one sequence of the lane's current LPT run
+//     (or sets up its next task), so lanes never wait for each other's runs or tasks.  Members
+//     are found in sorted order by 16-byte SIMD byte compares on the pipe row; bins are packed
+//     u32 keys time<<5|b with a sign-bit capacity mask (3 ops per bin for the argmin, 3 to
+//     place).  The first run (V_a, never aborted) writes mb directly; if a later V wins, a final
+//     run rewrites it.  Tasks needing V > 16, sumT >= 2^26 or a ragged batch are queued.
+//   k_pack_big: persistent warps pop queued (c,t,j) tasks; the WARP owns one pipeline, lanes own
+//     bins b = lane + 32 r (r < R <= 8 in registers, or global scratch beyond 256 bins); per
+//     item a redux.sync min over times, then over bin ids, picks the bin.
+//   makespan[t][c] = max_j ptime via atomicMax from the tasks.
 #include "hyd_internal.cuh"
 
 namespace hyd {
 
-constexpr int kVReg = 32;       // largest V handled by k_pack_small
-constexpr int kBigRMax = 8;     // k_pack_big: register bins per lane (V <= 256)
-constexpr int kBigWarps = 2048; // persistent warps of k_pack_big (scratch slots)
+constexpr int kLaneVMax = 16;     // largest V handled by k_pack_lanes
+constexpr int kLaneThreads = 256;
+constexpr int kBigRMax = 8;       // k_pack_big: register bins per lane (V <= 256)
+constexpr int kBigWarps = 2048;   // persistent warps of k_pack_big (scratch slots)
 
 struct PackArgs {
   const uint32_t* sorted_len;
@@ -47,6 +51,7 @@ struct PackArgs {
   const uint8_t* cand_np;
   int n_cand;
   const uint8_t* pipe;
+  const hyd_pipe_stats* stats;
   uint16_t* mb;
   uint16_t* v;
   uint64_t* ptime;
@@ -139,233 +144,262 @@ __device__ __forceinline__ void search_take(Search& s, uint32_t V, uint64_t maxb
   s.have = true;
 }
 
-// ------------------------------------------------------------------ LPT, one lane per pipeline
-template <int VMAX, typename TT>
-__device__ __forceinline__ bool lpt_lane(const uint16_t* __restrict__ lst, uint16_t* __restrict__ mbr,
-                                         uint32_t U, uint32_t V, uint32_t M,
-                                         const uint32_t* __restrict__ sl,
-                                         const uint32_t* __restrict__ cs, int kp, uint32_t k,
-                                         uint64_t thr64, uint64_t& maxbin, uint64_t& evals) {
-  const TT thr = thr64 > (uint64_t)(TT)(~TT(0)) ? (TT)(~TT(0)) : (TT)thr64;
-  TT tm[VMAX];
-  uint32_t tk[VMAX];
+// ------------------------------------------------------------------ pair-level init
+// makespan = 0 (feasible) or UINT64_MAX (infeasible); v/ptime rows zeroed; infeasible
+// pairs get mb = 0xFFFF.  Tasks then write their v/ptime slot and atomicMax the makespan.
+__global__ void __launch_bounds__(256) k_pack_init(const uint8_t* __restrict__ pipe, int n_iter,
+                                                   int batch, int n_cand, uint16_t* __restrict__ mb,
+                                                   uint16_t* __restrict__ v,
+                                                   uint64_t* __restrict__ ptime,
+                                                   uint64_t* __restrict__ makespan) {
+  const size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (e >= (size_t)n_iter * n_cand) return;
+  const int t = (int)(e / n_cand), c = (int)(e - (size_t)t * n_cand);
+  const size_t row = (size_t)c * n_iter + t;
+  const bool feasible = pipe[row * batch] != 0xFF;
+  makespan[(size_t)t * n_cand + c] = feasible ? 0ull : ~0ull;
+  uint4* v4 = reinterpret_cast<uint4*>(v + row * HYD_MAX_PIPES);
+  uint4* p4 = reinterpret_cast<uint4*>(ptime + row * HYD_MAX_PIPES);
+  const uint4 z = make_uint4(0, 0, 0, 0);
 #pragma unroll
-  for (int b = 0; b < VMAX; ++b) {
-    tm[b] = 0;
-    tk[b] = (uint32_t)b < V ? 0u : 0xFFFFFFFFu;  // sentinel: never fits
+  for (int q = 0; q < 4; ++q) v4[q] = z;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) p4[q] = z;
+  if (!feasible) {
+    uint16_t* mrow = mb + row * batch;
+    if ((batch & 7) == 0) {
+      const uint4 f = make_uint4(~0u, ~0u, ~0u, ~0u);
+      for (int q = 0; q < batch / 8; ++q) reinterpret_cast<uint4*>(mrow)[q] = f;
+    } else {
+      for (int i = 0; i < batch; ++i) mrow[i] = 0xFFFF;
+    }
   }
-  TT mx = 0;
-  for (uint32_t q = 0; q < U; ++q) {
-    const uint32_t idx = lst[q];
-    const uint32_t l = sl[idx];
-    const TT tau = (TT)cs[(size_t)idx * kp + k];
-    const uint32_t cap = M - l;
-    TT bt = ~TT(0);
-    uint32_t bb = VMAX;
-#pragma unroll
-    for (int b = 0; b < VMAX; ++b)
-      if (tk[b] <= cap && tm[b] < bt) {
-        bt = tm[b];
-        bb = (uint32_t)b;
-      }
-    evals += V;
-    if (bb == VMAX) return false;  // LPT(V) = bottom
-    const TT nt = bt + tau;
-#pragma unroll
-    for (int b = 0; b < VMAX; ++b)
-      if ((uint32_t)b == bb) {
-        tm[b] = nt;
-        tk[b] += l;
-      }
-    mx = nt > mx ? nt : mx;
-    if (mx > thr) return false;  // cannot improve (obj, V)
-    mbr[q] = (uint16_t)bb;
-  }
-  maxbin = (uint64_t)mx;
-  return true;
 }
 
-template <typename TT>
-__device__ __forceinline__ bool lpt_lane_dispatch(uint32_t vmax, const uint16_t* lst, uint16_t* mbr,
-                                                  uint32_t U, uint32_t V, uint32_t M,
-                                                  const uint32_t* sl, const uint32_t* cs, int kp,
-                                                  uint32_t k, uint64_t thr, uint64_t& maxbin,
-                                                  uint64_t& ev) {
-  if (vmax <= 4) return lpt_lane<4, TT>(lst, mbr, U, V, M, sl, cs, kp, k, thr, maxbin, ev);
-  if (vmax <= 8) return lpt_lane<8, TT>(lst, mbr, U, V, M, sl, cs, kp, k, thr, maxbin, ev);
-  if (vmax <= 16) return lpt_lane<16, TT>(lst, mbr, U, V, M, sl, cs, kp, k, thr, maxbin, ev);
-  return lpt_lane<32, TT>(lst, mbr, U, V, M, sl, cs, kp, k, thr, maxbin, ev);
+// ------------------------------------------------------------------ persistent lanes (V <= 16)
+// bins as packed u32 keys: key_b = time_b << 5 | b (needs sumT < 2^26), tokens tok_b.
+// masked_b = key_b | ((cap - tok_b) & 2^31) is >= 2^31 iff tok_b + l > MaxLen, so the
+// minimum masked key is the least-time fitting bin with the smallest index.
+template <int N>
+__device__ __forceinline__ uint32_t argmin_keys(const uint32_t (&keys)[kLaneVMax],
+                                                const uint32_t (&toks)[kLaneVMax], uint32_t cap) {
+  uint32_t m[N];
+#pragma unroll
+  for (int b = 0; b < N; ++b) m[b] = keys[b] | ((cap - toks[b]) & 0x80000000u);
+#pragma unroll
+  for (int w = N / 2; w > 0; w >>= 1)
+#pragma unroll
+    for (int b = 0; b < w; ++b) m[b] = min(m[b], m[b + w]);
+  return m[0];
 }
 
-// bytes of w equal to j (0xFF per matching byte)
-__device__ __forceinline__ uint32_t match4(uint32_t w, uint32_t jjjj) { return __vcmpeq4(w, jjjj); }
+template <int N>
+__device__ __forceinline__ void place_key(uint32_t (&keys)[kLaneVMax], uint32_t (&toks)[kLaneVMax],
+                                          uint32_t mk, uint32_t tau5, uint32_t l) {
+#pragma unroll
+  for (int b = 0; b < N; ++b) {
+    const bool hit = keys[b] == mk;
+    keys[b] += hit ? tau5 : 0u;
+    toks[b] += hit ? l : 0u;
+  }
+}
 
-template <int DP, bool STAGED>
-__global__ void __launch_bounds__(128) k_pack_small(PackArgs a, int nw, int ct, int tt) {
+struct LaneRun {
+  uint32_t V, thr, mx, wV;
+  bool writing, final_run;
+};
+
+template <bool STAGED>
+__global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int tc, int mnp) {
   extern __shared__ __align__(16) uint32_t sm[];
-  constexpr int G = 32 / DP;
+  __shared__ int s_n8, s_n16, s_next;
   const int B = a.batch, kp = a.k_pad;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int pslot = warp * G + lane / DP;
-  const int j = lane % DP;
-  const int c0 = blockIdx.x * ct, t0 = blockIdx.y * tt;
-  const int npairs = nw * G;
+  const int t = blockIdx.y, c0 = blockIdx.x * tc;
+  const int tid = threadIdx.x;
+  const int ntask_max = tc * mnp;
+  uint16_t* list = reinterpret_cast<uint16_t*>(sm + (STAGED ? (size_t)B * (1 + kp) : 0));
+  if (tid == 0) {
+    s_n8 = 0;
+    s_n16 = 0;
+    s_next = 0;
+  }
   if (STAGED) {
-    const int ntt = min(tt, a.n_iter - t0);
-    const uint4* gl = reinterpret_cast<const uint4*>(a.sorted_len + (size_t)t0 * B);
-    uint4* sl4 = reinterpret_cast<uint4*>(sm);
-    for (int e = threadIdx.x; e < ntt * B / 4; e += blockDim.x) sl4[e] = __ldg(gl + e);
-    const uint4* gc = reinterpret_cast<const uint4*>(a.cost + (size_t)t0 * B * kp);
-    uint4* sc4 = reinterpret_cast<uint4*>(sm + (size_t)tt * B);
-    for (int e = threadIdx.x; e < ntt * B * kp / 4; e += blockDim.x) sc4[e] = __ldg(gc + e);
-    __syncthreads();
+    const uint4* gl = reinterpret_cast<const uint4*>(a.sorted_len + (size_t)t * B);
+    uint4* s4 = reinterpret_cast<uint4*>(sm);
+    for (int e = tid; e < B / 4; e += kLaneThreads) s4[e] = __ldg(gl + e);
+    const uint4* gc = reinterpret_cast<const uint4*>(a.cost + (size_t)t * B * kp);
+    uint4* c4 = reinterpret_cast<uint4*>(sm + B);
+    for (int e = tid; e < B * kp / 4; e += kLaneThreads) c4[e] = __ldg(gc + e);
   }
-  uint16_t* lists = reinterpret_cast<uint16_t*>(sm + (STAGED ? (size_t)tt * B * (1 + kp) : 0));
-  uint16_t* lst = lists + (size_t)pslot * B;
-  uint16_t* mbr = lists + (size_t)npairs * B + (size_t)pslot * B;
+  __syncthreads();
+  const uint32_t* slen = STAGED ? sm : a.sorted_len + (size_t)t * B;
+  const uint32_t* cst = STAGED ? sm + B : a.cost + (size_t)t * B * kp;
+  const bool vec_ok = (B & 15) == 0;
 
-  const int lt = pslot / ct, lc = pslot - lt * ct;
-  const int c = c0 + lc, t = t0 + lt;
-  const bool pair_ok = lt < tt && c < a.n_cand && t < a.n_iter;
-  const uint32_t* sl = STAGED ? sm + (size_t)lt * B : a.sorted_len + (size_t)t * B;
-  const uint32_t* cs = STAGED ? sm + (size_t)tt * B + (size_t)lt * B * kp
-                              : a.cost + (size_t)t * B * kp;
-  const size_t row = (size_t)c * a.n_iter + t;
-  const uint8_t* prow = a.pipe + row * B;
-  uint16_t* mrow = a.mb + row * B;
-
-  const int np = pair_ok ? (int)a.cand_np[c] : 0;
-  bool infeasible = pair_ok && prow[0] == 0xFF;
-  bool on = pair_ok && !infeasible && j < np;
-  uint32_t k = on ? a.cand[(size_t)c * HYD_MAX_PIPES + j] : 0u;
-  Search s;
-  s.M = on ? a.schemes[k].max_len : 1u;
-  s.P = on ? a.schemes[k].pp : 1u;
-  s.UL = on ? a.schemes[k].util_len : 0u;
-
-  if (infeasible) {  // whole row: mb 0xFFFF, v = ptime = 0, makespan = UINT64_MAX
-    for (int i = j; i < B; i += DP) mrow[i] = 0xFFFF;
-    for (int e = j; e < HYD_MAX_PIPES; e += DP) {
-      a.v[row * HYD_MAX_PIPES + e] = 0;
-      a.ptime[row * HYD_MAX_PIPES + e] = 0ull;
-    }
-    if (j == 0) a.makespan[(size_t)t * a.n_cand + c] = ~0ull;
-  }
-
-  // ---- member list of pipeline j: count, segmented exclusive scan, fill
-  const uint32_t jjjj = 0x01010101u * (uint32_t)j;
-  const bool vec = (B & 15) == 0;
-  uint32_t cnt = 0;
-  if (on) {
-    if (vec) {
-      const uint4* p4 = reinterpret_cast<const uint4*>(prow);
-      for (int q = 0; q < B / 16; ++q) {
-        const uint4 w = __ldg(p4 + q);
-        cnt += (__popc(match4(w.x, jjjj)) + __popc(match4(w.y, jjjj)) + __popc(match4(w.z, jjjj)) +
-                __popc(match4(w.w, jjjj))) >> 3;
-      }
-    } else {
-      for (int i = 0; i < B; ++i) cnt += prow[i] == (uint8_t)j;
-    }
-  }
-  uint32_t incl = cnt;
-#pragma unroll
-  for (int o = 1; o < DP; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(HYD_FULL, incl, o, DP);
-    if (j >= o) incl += y;
-  }
-  const uint32_t off = incl - cnt;
-  lst += off;
-  mbr += off;
-  s.U = cnt;
-  s.S = 0;
-  s.sumT = 0;
-  s.tau_max = 0;
-  if (on && cnt) {
-    uint32_t n = 0;
-    auto take = [&](uint32_t idx) {
-      lst[n] = (uint16_t)idx;
-      const uint32_t tau = cs[(size_t)idx * kp + k];
-      if (n == 0) s.tau_max = tau;
-      s.S += sl[idx];
-      s.sumT += tau;
-      ++n;
-    };
-    if (vec) {
-      const uint4* p4 = reinterpret_cast<const uint4*>(prow);
-      for (int q = 0; q < B / 16 && n < cnt; ++q) {
-        const uint4 w4 = __ldg(p4 + q);
-        const uint32_t ws[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          uint32_t m = match4(ws[h], jjjj);
-          while (m) {
-            const int byte = (__ffs(m) - 1) >> 3;
-            take((uint32_t)(16 * q + 4 * h + byte));
-            m &= ~(0xFFu << (8 * byte));
-          }
-        }
-      }
-    } else {
-      for (int i = 0; i < B; ++i)
-        if (prow[i] == (uint8_t)j) take((uint32_t)i);
-    }
-  }
-
-  // ---- exact pruned V search, lanes in lock-step rounds with a warp-uniform VMAX
-  bool searching = on && s.U > 0;
-  bool deferred = false;
-  if (searching) search_init(s);
-  const bool narrow = __all_sync(HYD_FULL, !searching || s.sumT < 0xFFFFFFFFull);
-  uint64_t ev = 0;
-  while (true) {
-    uint32_t V = searching ? search_next(s) : 0u;
-    if (searching && V == 0) searching = false;
-    if (V > (uint32_t)kVReg) {
-      deferred = true;
-      searching = false;
-      V = 0;
-    }
-    const uint32_t vmax = __reduce_max_sync(HYD_FULL, V);
-    if (vmax == 0) break;
-    if (V) {
-      const uint64_t thr = search_thr(s, V);
-      uint64_t mx = 0;
-      const bool ok = narrow ? lpt_lane_dispatch<uint32_t>(vmax, lst, mbr, s.U, V, s.M, sl, cs, kp, k, thr, mx, ev)
-                             : lpt_lane_dispatch<uint64_t>(vmax, lst, mbr, s.U, V, s.M, sl, cs, kp, k, thr, mx, ev);
-      if (ok) {
-        search_take(s, V, mx);
-        for (uint32_t q = 0; q < s.U; ++q) mrow[lst[q]] = mbr[q];
-      }
-    }
-  }
-
-  // ---- outputs
-  if (pair_ok && !infeasible) {
-    if (!deferred) {
-      for (int e = j; e < HYD_MAX_PIPES; e += DP) {
-        const bool mine = e == j && on;
-        a.v[row * HYD_MAX_PIPES + e] = mine ? (uint16_t)s.vbest : (uint16_t)0;
-        a.ptime[row * HYD_MAX_PIPES + e] = mine ? s.best : 0ull;
-      }
-    } else {
-      for (int e = j + DP; e < HYD_MAX_PIPES; e += DP) {
-        a.v[row * HYD_MAX_PIPES + e] = 0;
-        a.ptime[row * HYD_MAX_PIPES + e] = 0ull;
-      }
+  // ---- task list of this CTA, split into VMAX classes 8 (front) and 16 (back)
+  for (int e = tid; e < ntask_max; e += kLaneThreads) {
+    const int c = c0 + e / mnp, j = e % mnp;
+    if (c >= a.n_cand || j >= (int)a.cand_np[c]) continue;
+    const size_t row = (size_t)c * a.n_iter + t;
+    if (a.pipe[row * B] == 0xFF) continue;  // infeasible pair: k_pack_init wrote it
+    const hyd_pipe_stats st = a.stats[row * mnp + j];
+    if (st.u == 0) continue;  // empty pipeline: V = ptime = 0 (k_pack_init)
+    const uint32_t k = a.cand[(size_t)c * HYD_MAX_PIPES + j];
+    Search s;
+    s.M = a.schemes[k].max_len;
+    s.P = a.schemes[k].pp;
+    s.UL = a.schemes[k].util_len;
+    s.U = st.u;
+    s.S = st.s;
+    s.sumT = st.sum_t;
+    s.tau_max = st.tau_max;
+    search_init(s);
+    if (!vec_ok || s.sumT >= (1ull << 26) || s.M >= 0x80000000u || s.va > (uint32_t)kLaneVMax) {
       const unsigned long long slot = atomicAdd(a.q_count, 1ull);
       if (slot < a.q_cap)
         a.queue[slot] = ((unsigned long long)c << 37) | ((unsigned long long)t << 5) | (unsigned)j;
+    } else if (s.va <= 8) {
+      list[atomicAdd(&s_n8, 1)] = (uint16_t)e;
+    } else {
+      list[ntask_max - 1 - atomicAdd(&s_n16, 1)] = (uint16_t)e;
     }
   }
-  ev = __reduce_add_sync(HYD_FULL, (uint32_t)min(ev, (uint64_t)0xFFFFFFFFull)) ;
-  if (lane == 0 && ev) atomicAdd(a.evals, (unsigned long long)ev);
-  uint64_t pm = (on && !deferred) ? s.best : 0ull;
-#pragma unroll
-  for (int o = DP / 2; o > 0; o >>= 1) pm = max(pm, __shfl_xor_sync(HYD_FULL, pm, o, DP));
-  if (pair_ok && !infeasible && j == 0) a.makespan[(size_t)t * a.n_cand + c] = pm;
-}
+  __syncthreads();
+  const int n8 = s_n8, ntask = s_n8 + s_n16;
 
+  // ---- persistent lane state machine: one sequence (or one task set-up) per iteration
+  bool have = false;
+  int c = 0, j = 0;
+  uint32_t k = 0, jjjj = 0;
+  size_t row = 0;
+  const uint8_t* prow = nullptr;
+  uint16_t* mrow = nullptr;
+  Search s;
+  LaneRun r;
+  r.V = r.thr = r.mx = r.wV = 0;
+  r.writing = r.final_run = false;
+  uint32_t keys[kLaneVMax], toks[kLaneVMax];
+  uint32_t qc = 0, m16 = 0, cbase = 0;
+  const uint32_t nchunks = (uint32_t)B / 16;
+  uint64_t ev = 0;
+
+  auto start_run = [&](uint32_t V, bool write, bool fin) {
+    r.V = V;
+    r.writing = write;
+    r.final_run = fin;
+    const uint64_t th = (write || fin) ? ~0ull : search_thr(s, V);
+    r.thr = th > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)th;
+    r.mx = 0;
+#pragma unroll
+    for (int b = 0; b < kLaneVMax; ++b) {
+      keys[b] = (uint32_t)b < V ? (uint32_t)b : 0xFFFFFFFFu;
+      toks[b] = 0u;
+    }
+    qc = 0;
+    m16 = 0;
+  };
+  auto finalize = [&]() {
+    a.v[row * HYD_MAX_PIPES + j] = (uint16_t)s.vbest;
+    a.ptime[row * HYD_MAX_PIPES + j] = s.best;
+    atomicMax(reinterpret_cast<unsigned long long*>(a.makespan + (size_t)t * a.n_cand + c),
+              (unsigned long long)s.best);
+    have = false;
+  };
+  auto defer = [&]() {
+    const unsigned long long slot = atomicAdd(a.q_count, 1ull);
+    if (slot < a.q_cap)
+      a.queue[slot] = ((unsigned long long)c << 37) | ((unsigned long long)t << 5) | (unsigned)j;
+    have = false;
+  };
+  auto run_end = [&](bool ok) {
+    if (ok) {
+      search_take(s, r.V, r.mx);
+      if (r.writing) r.wV = r.V;
+    }
+    if (r.final_run) {
+      finalize();
+      return;
+    }
+    const uint32_t nv = search_next(s);
+    if (nv == 0) {
+      if (!s.have) defer();  // cannot happen (V = U is always feasible); safety net
+      else if (s.vbest != r.wV) start_run(s.vbest, true, true);  // write the winner's mb
+      else finalize();
+    } else if (nv > (uint32_t)kLaneVMax) {
+      defer();
+    } else {
+      start_run(nv, false, false);
+    }
+  };
+
+  while (true) {
+    if (!have) {
+      const int e = atomicAdd(&s_next, 1);
+      if (e >= ntask) break;
+      const int le = e < n8 ? list[e] : list[ntask_max - (ntask - e)];
+      c = c0 + le / mnp;
+      j = le % mnp;
+      row = (size_t)c * a.n_iter + t;
+      prow = a.pipe + row * B;
+      mrow = a.mb + row * B;
+      k = a.cand[(size_t)c * HYD_MAX_PIPES + j];
+      jjjj = 0x01010101u * (uint32_t)j;
+      const hyd_pipe_stats st = a.stats[row * mnp + j];
+      s.M = a.schemes[k].max_len;
+      s.P = a.schemes[k].pp;
+      s.UL = a.schemes[k].util_len;
+      s.U = st.u;
+      s.S = st.s;
+      s.sumT = st.sum_t;
+      s.tau_max = st.tau_max;
+      search_init(s);
+      r.wV = 0;
+      start_run(s.va, true, false);  // the first run always completes or is infeasible
+      have = true;
+    }
+    // next member of pipeline j in sorted order: 16 pipe bytes -> 16-bit match mask
+    while (m16 == 0 && qc < nchunks) {
+      const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(prow) + qc);
+      const uint32_t x0 = __vcmpeq4(w4.x, jjjj) & 0x01010101u, x1 = __vcmpeq4(w4.y, jjjj) & 0x01010101u;
+      const uint32_t x2 = __vcmpeq4(w4.z, jjjj) & 0x01010101u, x3 = __vcmpeq4(w4.w, jjjj) & 0x01010101u;
+      m16 = ((x0 * 0x204081u) >> 21 & 0xFu) | (((x1 * 0x204081u) >> 21 & 0xFu) << 4) |
+            (((x2 * 0x204081u) >> 21 & 0xFu) << 8) | (((x3 * 0x204081u) >> 21 & 0xFu) << 12);
+      cbase = qc * 16u;
+      ++qc;
+    }
+    if (m16 == 0) {  // every member placed: run complete
+      run_end(true);
+      continue;
+    }
+    const uint32_t i = cbase + (uint32_t)(__ffs(m16) - 1);
+    m16 &= m16 - 1u;
+    const uint32_t l = slen[i];
+    const uint32_t tau = cst[(size_t)i * kp + k];
+    const uint32_t cap = s.M - l;
+    ev += r.V;
+    uint32_t mk;
+    if (r.V <= 8) {
+      mk = argmin_keys<8>(keys, toks, cap);
+    } else {
+      mk = argmin_keys<16>(keys, toks, cap);
+    }
+    if (mk >> 31) {  // no micro-batch can take the sequence: LPT(V) infeasible
+      run_end(false);
+      continue;
+    }
+    const uint32_t nt = (mk >> 5) + tau;
+    if (r.V <= 8) {
+      place_key<8>(keys, toks, mk, tau << 5, l);
+    } else {
+      place_key<16>(keys, toks, mk, tau << 5, l);
+    }
+    r.mx = max(r.mx, nt);
+    if (r.writing) mrow[i] = (uint16_t)(mk & 31u);
+    if (r.mx > r.thr) run_end(false);  // cannot improve (obj, V): abort this V
+  }
+  ev = __reduce_add_sync(__activemask(), (uint32_t)min(ev, (uint64_t)0xFFFFFFFFull));
+  if ((tid & 31) == 0 && ev) atomicAdd(a.evals, (unsigned long long)ev);
+}
 // ------------------------------------------------------------------ LPT, one warp per pipeline
 template <typename TT>
 __device__ __forceinline__ TT warp_min(TT x);
@@ -579,27 +613,22 @@ size_t pack_workspace(int n_iter, int batch, int n_cand, int max_np) {
          align256((size_t)kBigWarps * batch * 4);
 }
 
-template <int DP>
-static cudaError_t launch_small(bool staged, dim3 grid, int threads, size_t smem, cudaStream_t s,
-                                const PackArgs& a, int nw, int ct, int tt) {
-  cudaError_t e;
-  if (staged) {
-    e = cudaFuncSetAttribute(k_pack_small<DP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    k_pack_small<DP, true><<<grid, threads, smem, s>>>(a, nw, ct, tt);
-  } else {
-    e = cudaFuncSetAttribute(k_pack_small<DP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    k_pack_small<DP, false><<<grid, threads, smem, s>>>(a, nw, ct, tt);
-  }
+template <bool STAGED>
+static cudaError_t launch_lanes(dim3 grid, size_t smem, cudaStream_t s, const PackArgs& a, int tc,
+                                int mnp) {
+  cudaError_t e = cudaFuncSetAttribute(k_pack_lanes<STAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  k_pack_lanes<STAGED><<<grid, kLaneThreads, smem, s>>>(a, tc, mnp);
   return cudaGetLastError();
 }
 
 int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch, int k_pad,
                 const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
-                const uint8_t* cand_np, int n_cand, int max_np, const uint8_t* pipe, uint16_t* mb,
-                uint16_t* v, uint64_t* ptime, uint64_t* makespan, uint32_t* status, void* ws,
-                size_t ws_bytes, cudaStream_t s) {
+                const uint8_t* cand_np, int n_cand, int max_np, const uint8_t* pipe,
+                const hyd_pipe_stats* stats, uint16_t* mb, uint16_t* v, uint64_t* ptime,
+                uint64_t* makespan, uint32_t* status, void* ws, size_t ws_bytes, cudaStream_t s) {
+  (void)ws_bytes;
   if (n_iter == 0 || n_cand == 0) return HYD_OK;
   const int dp = dp_of(max_np);
   PackArgs a;
@@ -614,6 +643,7 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
   a.cand_np = cand_np;
   a.n_cand = n_cand;
   a.pipe = pipe;
+  a.stats = stats;
   a.mb = mb;
   a.v = v;
   a.ptime = ptime;
@@ -633,30 +663,25 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
 
   cudaError_t e = cudaMemsetAsync(a.q_count, 0, 24, s);
   if (e != cudaSuccess) return record_cuda_error(e);
+  const size_t pairs = (size_t)n_iter * n_cand;
+  k_pack_init<<<(unsigned)((pairs + 255) / 256), 256, 0, s>>>(pipe, n_iter, batch, n_cand, mb, v, ptime,
+                                                              makespan);
+  note_launch();
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return record_cuda_error(e);
 
-  // small kernel geometry: nw warps x (32/dp) pairs; shrink nw until lists fit
-  const int G = 32 / dp;
-  int nw = 4;
-  while (nw > 1 && (size_t)nw * G * batch * 4 > 96 * 1024) nw >>= 1;
-  const int npairs = nw * G;
-  const int ct = n_cand < npairs ? n_cand : npairs;
-  const int tt = npairs / ct;
-  const size_t lists = (size_t)npairs * batch * 4;
-  const size_t stage = (size_t)tt * batch * 4 * (1 + (size_t)k_pad);
-  const bool staged = (batch % 4) == 0 && stage + lists <= 112 * 1024;
-  const size_t smem = lists + (staged ? stage : 0);
-  dim3 grid((n_cand + ct - 1) / ct, (n_iter + tt - 1) / tt);
-  switch (dp) {
-    case 2: e = launch_small<2>(staged, grid, nw * 32, smem, s, a, nw, ct, tt); break;
-    case 4: e = launch_small<4>(staged, grid, nw * 32, smem, s, a, nw, ct, tt); break;
-    case 8: e = launch_small<8>(staged, grid, nw * 32, smem, s, a, nw, ct, tt); break;
-    case 16: e = launch_small<16>(staged, grid, nw * 32, smem, s, a, nw, ct, tt); break;
-    default: e = launch_small<32>(staged, grid, nw * 32, smem, s, a, nw, ct, tt); break;
-  }
+  // persistent lanes: a CTA = one iteration x tc candidates (~2048 pipeline tasks)
+  const int tc = n_cand < 2048 / max_np ? n_cand : (2048 / max_np > 0 ? 2048 / max_np : 1);
+  const size_t stage = (size_t)batch * 4 * (1 + (size_t)k_pad);
+  const size_t list = (((size_t)tc * max_np * 2) + 15) & ~(size_t)15;
+  const bool staged = (batch % 4) == 0 && stage + list <= 100 * 1024;
+  dim3 grid((n_cand + tc - 1) / tc, n_iter);
+  e = staged ? launch_lanes<true>(grid, stage + list, s, a, tc, max_np)
+             : launch_lanes<false>(grid, list, s, a, tc, max_np);
   note_launch();
   if (e != cudaSuccess) return record_cuda_error(e);
 
-  // big kernel: persistent warps over the queue
+  // warp per pipeline for the queue (V > 16, wide sums, ragged batches)
   int wpb = 8;
   while (wpb > 1 && (size_t)wpb * batch * 4 > 96 * 1024) wpb >>= 1;
   const size_t bsm = (size_t)wpb * batch * 4;

@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(HERE, "libhyd.so")
 HYD_OK = 0
 STATUS_BITS = {1: "OVERFLOW", 2: "ZERO_COST", 4: "BAD_LENGTH", 8: "KEY_RANGE", 16: "NOT_CANONICAL"}
 MAX_PIPES = 32
+PIPE_STATS_BYTES = 24  # sizeof(hyd_pipe_stats)
 KEY_SHIFT = 20
 INT64_MAX = 2**63 - 1
 
@@ -56,9 +57,9 @@ def lib():
     I, P, Z, U64 = C.c_int, C.c_void_p, C.c_size_t, C.c_uint64
     sig = {
         "hyd_cost_table": ([P, I, I, P, I, I, P, P, P, P, P], I),
-        "hyd_dispatch": ([P, P, I, I, I, P, I, P, P, I, I, P, P, P, P], I),
+        "hyd_dispatch": ([P, P, I, I, I, P, I, P, P, I, I, P, P, P, P, P], I),
         "hyd_pack_workspace": ([I, I, I, I], Z),
-        "hyd_pack": ([P, P, I, I, I, P, I, P, P, I, I, P, P, P, P, P, P, P, Z, P], I),
+        "hyd_pack": ([P, P, I, I, I, P, I, P, P, I, I, P, P, P, P, P, P, P, P, Z, P], I),
         "hyd_select_best": ([P, I, I, I, P, P, P], I),
         "hyd_gather_winners": ([P, P, P, P, P, P, I, I, I, I, P, P, P, P, P], I),
         "hyd_assign_workspace": ([I, I, I, I, I, I], Z),
@@ -130,20 +131,20 @@ def cost_table(len_, n_iter, batch, schemes, n_schemes, k_pad, sorted_len, perm,
 
 
 def dispatch(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, pipe, lb,
-             status, stream=None):
+             stats, status, stream=None):
     _check(lib().hyd_dispatch(_dev(sorted_len), _dev(cost), n_iter, batch, k_pad, _dev(schemes), n_schemes,
-                              _dev(cand), _dev(cand_np), n_cand, max_np, _dev(pipe), _dev(lb), _dev(status),
-                              _stream(stream)), "hyd_dispatch")
+                              _dev(cand), _dev(cand_np), n_cand, max_np, _dev(pipe), _dev(lb), _dev(stats),
+                              _dev(status), _stream(stream)), "hyd_dispatch")
 
 
 def pack_workspace(n_iter, batch, n_cand, max_np) -> int:
     return int(lib().hyd_pack_workspace(n_iter, batch, n_cand, max_np))
 
 
-def pack(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, pipe, mb, v,
-         ptime, makespan, status, ws, stream=None):
+def pack(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, pipe, stats,
+         mb, v, ptime, makespan, status, ws, stream=None):
     _check(lib().hyd_pack(_dev(sorted_len), _dev(cost), n_iter, batch, k_pad, _dev(schemes), n_schemes, _dev(cand),
-                          _dev(cand_np), n_cand, max_np, _dev(pipe), _dev(mb), _dev(v), _dev(ptime),
+                          _dev(cand_np), n_cand, max_np, _dev(pipe), _dev(stats), _dev(mb), _dev(v), _dev(ptime),
                           _dev(makespan), _dev(status), _dev(ws), ws.numel() * ws.element_size(),
                           _stream(stream)), "hyd_pack")
 
