@@ -232,11 +232,11 @@ def main():
         if evs:
             evs[1].record(stream)
         hyd.dispatch(A.sorted_len, A.cost, It, B, kp, A.schemes, K, A.cand, A.cand_np, Cn, A.max_np, A.pipe, A.lb,
-                     A.stats, A.status)
+                     A.stats, A.members, A.status)
         if evs:
             evs[2].record(stream)
         hyd.pack(A.sorted_len, A.cost, It, B, kp, A.schemes, K, A.cand, A.cand_np, Cn, A.max_np, A.pipe, A.stats,
-                 A.mb, A.v, A.ptime, A.makespan, A.status, A.ws)
+                 A.members, A.mb, A.v, A.ptime, A.makespan, A.status, A.ws)
         if evs:
             evs[3].record(stream)
         hyd.select_best(A.makespan, It, Cn, A.cand_offset, A.key, A.status)
@@ -354,9 +354,10 @@ def roofline(name, ms, W, A, pk, how, local_ci):
         cnt = A.pack_counters()
         ops = 6.0 * cnt["bin_evals"]  # ~6 int32 ops per (item, bin) evaluation
         achieved = ops / (ms / 1000.0) / 1e9
-        return {"kernel": "pack (k_pack_small + k_pack_big)", "bound": "alu", "achieved": achieved,
+        return {"kernel": "pack (k_pack_init + k_pack_lanes + k_pack_big)", "bound": "alu", "achieved": achieved,
                 "peak": alu_peak, "unit": "Gop/s", "frac": achieved / alu_peak, "traffic": None,
                 "algorithmic_ops_per_launch": ops, "bin_evals_per_launch": cnt["bin_evals"],
+                "queued_tasks": cnt["queued_tasks"], "handoff": cnt.get("handoff"),
                 "hbm_algorithmic_GBps": local_ci * (3 * B + 10 * D + 8) / (ms / 1000.0) / 1e9,
                 "peak_source": f"148 SM x 128 INT32 lanes x {sm_mhz:.0f} MHz ({how} clock)"}
     if name == "dispatch":

@@ -91,7 +91,8 @@ int hyd_cost_table(const uint32_t* len, int n_iter, int batch, const hyd_scheme*
 /* Per-pipeline statistics of a dispatch, consumed by hyd_pack (24 bytes):
  *   u = U_j (sequences dispatched to pipeline j), tau_max = T(longest of them, P_j)
  *   (its first one in sorted order), s = S_j (their token sum), sum_t = sum of their T(l, P_j).
- * Layout [n_cand][n_iter][max_np]; entries of infeasible (c,t) are undefined. */
+ * Layout [n_iter][n_cand][max_np] (iteration-major, so one iteration's candidates are
+ * contiguous); for an infeasible (c,t) only stats[t][c][0].u is defined, = 0xFFFFFFFF. */
 typedef struct {
   uint32_t u;
   uint32_t tau_max;
@@ -106,16 +107,19 @@ typedef struct {
  * minimising (C_j + tau + e_j, j) where tau = T(l,P_j) and e_j = tau (PP_j - 1) for an empty
  * pipeline, else the pipeline's extra term E_j (Alg. 1 lines 8-14 with LPT order).
  * Outputs pipe [n_cand][n_iter][batch] u8 (pipeline of each sorted position),
- * lb [n_cand][n_iter] u64 = max_j (C_j + E_j) (the Eq. 3 objective) and
- * stats [n_cand][n_iter][max_np] (hyd_pipe_stats, for hyd_pack).
+ * lb [n_cand][n_iter] u64 = max_j (C_j + E_j) (the Eq. 3 objective),
+ * stats [n_iter][n_cand][max_np] (hyd_pipe_stats, for hyd_pack) and
+ * members [n_iter][n_cand][max_np][ceil(batch/32)] u32: bit (i mod 32) of word i/32 of
+ * pipeline j is set iff sorted position i was dispatched to j (the m_ij matrix of Eq. 3,
+ * P:643-648, as bitmaps; for hyd_pack).  Rows of infeasible (c,t) are undefined.
  * max_np = max over c of cand_np[c] (host-known; selects the kernel width). */
 int hyd_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch,
                  int k_pad, const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
                  const uint8_t* cand_np, int n_cand, int max_np, uint8_t* pipe, uint64_t* lb,
-                 hyd_pipe_stats* stats, uint32_t* status, void* stream);
+                 hyd_pipe_stats* stats, uint32_t* members, uint32_t* status, void* stream);
 
 /* ---- a4: stage 2 packing (Eq. 1 + App. D) -------------------------------------------
- * Inputs include pipe and stats from hyd_dispatch (same n_cand/n_iter/max_np).
+ * Inputs include pipe, stats and members from hyd_dispatch (same n_cand/n_iter/max_np).
  * For each (c,t,j): the pipeline's sequences Q (sorted order), U = |Q|, S = sum l:
  * V in [max(ceil(S/MaxLen),1), min(floor(S/UtilLen),U)] (clamped up to the lower end);
  * LPT(V): each sequence to the least-time micro-batch that stays within MaxLen (smallest
@@ -127,11 +131,13 @@ int hyd_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, i
  * ptime [n_cand][n_iter][32] u64 (objective of V*), makespan [n_iter][n_cand] u64
  * (max_j ptime; UINT64_MAX if infeasible).  ws: hyd_pack_workspace() bytes; after the
  * call completes, the u64 at ws byte offset 16 holds the number of (sequence, micro-batch)
- * evaluations the LPT runs performed (diagnostic work counter for the roofline). */
+ * evaluations the LPT runs performed (diagnostic work counter for the roofline) and bytes
+ * [24, 88) eight u64 counters of pipelines handed between the kernel's internal passes. */
 size_t hyd_pack_workspace(int n_iter, int batch, int n_cand, int max_np);
 int hyd_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch, int k_pad,
              const hyd_scheme* schemes, int n_schemes, const uint8_t* cand, const uint8_t* cand_np,
-             int n_cand, int max_np, const uint8_t* pipe, const hyd_pipe_stats* stats, uint16_t* mb, uint16_t* v,
+             int n_cand, int max_np, const uint8_t* pipe, const hyd_pipe_stats* stats,
+             const uint32_t* members, uint16_t* mb, uint16_t* v,
              uint64_t* ptime, uint64_t* makespan, uint32_t* status, void* ws, size_t ws_bytes,
              void* stream);
 

@@ -105,6 +105,7 @@ class Assigner:
         self.pipe = torch.empty((Cn, It, B), dtype=u8, device=dev)
         self.lb = torch.empty((Cn, It), dtype=torch.int64, device=dev)
         self.stats = torch.empty((Cn, It, self.max_np, hyd.PIPE_STATS_BYTES), dtype=u8, device=dev)
+        self.members = torch.empty((Cn, It, self.max_np, (B + 31) // 32), dtype=i32, device=dev)
         self.mb = torch.empty((Cn, It, B), dtype=torch.int16, device=dev)
         self.v = torch.empty((Cn, It, hyd.MAX_PIPES), dtype=torch.int16, device=dev)
         self.ptime = torch.empty((Cn, It, hyd.MAX_PIPES), dtype=torch.int64, device=dev)
@@ -118,9 +119,10 @@ class Assigner:
         It, B, K, kp, Cn = self.n_iter, self.batch, self.n_schemes, self.k_pad, self.n_cand
         hyd.cost_table(len_dev, It, B, self.schemes, K, kp, self.sorted_len, self.perm, self.cost, self.status, stream)
         hyd.dispatch(self.sorted_len, self.cost, It, B, kp, self.schemes, K, self.cand, self.cand_np, Cn,
-                     self.max_np, self.pipe, self.lb, self.stats, self.status, stream)
+                     self.max_np, self.pipe, self.lb, self.stats, self.members, self.status, stream)
         hyd.pack(self.sorted_len, self.cost, It, B, kp, self.schemes, K, self.cand, self.cand_np, Cn, self.max_np,
-                 self.pipe, self.stats, self.mb, self.v, self.ptime, self.makespan, self.status, self.ws, stream)
+                 self.pipe, self.stats, self.members, self.mb, self.v, self.ptime, self.makespan, self.status, self.ws,
+                 stream)
         hyd.select_best(self.makespan, It, Cn, self.cand_offset, self.key, self.status, stream)
         return self.key
 
@@ -129,8 +131,11 @@ class Assigner:
     def pack_counters(self) -> dict:
         """Work counter written by the last hyd_pack (include/hyd.h: u64 at ws offset 16)."""
         self.torch.cuda.synchronize(self.dev)
-        ev = int(self.ws[16:24].cpu().numpy().view(np.uint64)[0])
-        return {"bin_evals": ev}
+        w = self.ws[0:112].cpu().numpy().view(np.uint64)
+        names = ["sumt16", "va16", "bottom16", "cand16", "sumt32", "bottom32", "cand32", "overflow",
+                 "cand_total16", "tasks_total16", "cand_max_cta16"]
+        return {"bin_evals": int(w[2]), "queued_tasks": int(w[0]),
+                "handoff": {n: int(x) for n, x in zip(names, w[3:14])}}
 
     def dispatch_evals(self, lengths) -> int:
         """Sum over feasible (c,t) of sum_i J_i (feasible pipelines per sequence): the

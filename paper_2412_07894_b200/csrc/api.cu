@@ -11,11 +11,12 @@ int launch_sort_cost(const uint32_t*, int, int, const hyd_scheme*, int, int, uin
                      uint32_t*, uint32_t*, cudaStream_t);
 int launch_dispatch(const uint32_t*, const uint32_t*, int, int, int, const hyd_scheme*, int,
                     const uint8_t*, const uint8_t*, int, int, uint8_t*, uint64_t*, hyd_pipe_stats*,
-                    uint32_t*, cudaStream_t);
+                    uint32_t*, uint32_t*, cudaStream_t);
 size_t pack_workspace(int, int, int, int);
 int launch_pack(const uint32_t*, const uint32_t*, int, int, int, const hyd_scheme*, int,
                 const uint8_t*, const uint8_t*, int, int, const uint8_t*, const hyd_pipe_stats*,
-                uint16_t*, uint16_t*, uint64_t*, uint64_t*, uint32_t*, void*, size_t, cudaStream_t);
+                const uint32_t*, uint16_t*, uint16_t*, uint64_t*, uint64_t*, uint32_t*, void*, size_t,
+                cudaStream_t);
 int launch_select(const uint64_t*, int, int, int, int64_t*, uint32_t*, cudaStream_t);
 int launch_gather(const int64_t*, const uint32_t*, const uint8_t*, const uint16_t*, const uint16_t*,
                   const uint64_t*, int, int, int, int, uint8_t*, uint16_t*, uint16_t*, uint64_t*,
@@ -45,7 +46,7 @@ static bool cand_ok(int n_cand, int max_np) {
 static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct AssignLayout {
-  size_t len, schemes, cand, cand_np, sorted, perm, cost, pipe, lb, stats, mb, v, ptime, makespan, key,
+  size_t len, schemes, cand, cand_np, sorted, perm, cost, pipe, lb, stats, members, mb, v, ptime, makespan, key,
       status, win_pipe, win_mb, win_v, win_ptime, pack_ws, pack_bytes, total;
 };
 
@@ -69,6 +70,7 @@ static AssignLayout assign_layout(int n_iter, int batch, int n_schemes, int k_pa
   L.pipe = put(Cn * It * B);
   L.lb = put(Cn * It * 8);
   L.stats = put(Cn * It * (size_t)max_np * sizeof(hyd_pipe_stats));
+  L.members = put(Cn * It * (size_t)max_np * ((B + 31) / 32) * 4);
   L.mb = put(Cn * It * B * 2);
   L.v = put(Cn * It * HYD_MAX_PIPES * 2);
   L.ptime = put(Cn * It * HYD_MAX_PIPES * 8);
@@ -148,12 +150,12 @@ int hyd_cost_table(const uint32_t* len, int n_iter, int batch, const hyd_scheme*
 int hyd_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch,
                  int k_pad, const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
                  const uint8_t* cand_np, int n_cand, int max_np, uint8_t* pipe, uint64_t* lb,
-                 hyd_pipe_stats* stats, uint32_t* status, void* stream) {
-  if (!sorted_len || !cost || !schemes || !cand || !cand_np || !pipe || !lb || !stats || !status ||
+                 hyd_pipe_stats* stats, uint32_t* members, uint32_t* status, void* stream) {
+  if (!sorted_len || !cost || !schemes || !cand || !cand_np || !pipe || !lb || !stats || !members || !status ||
       !common_ok(n_iter, batch, n_schemes, k_pad) || !cand_ok(n_cand, max_np))
     return HYD_E_INVALID;
   return launch_dispatch(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np,
-                         n_cand, max_np, pipe, lb, stats, status, (cudaStream_t)stream);
+                         n_cand, max_np, pipe, lb, stats, members, status, (cudaStream_t)stream);
 }
 
 size_t hyd_pack_workspace(int n_iter, int batch, int n_cand, int max_np) {
@@ -163,16 +165,16 @@ size_t hyd_pack_workspace(int n_iter, int batch, int n_cand, int max_np) {
 
 int hyd_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch, int k_pad,
              const hyd_scheme* schemes, int n_schemes, const uint8_t* cand, const uint8_t* cand_np,
-             int n_cand, int max_np, const uint8_t* pipe, const hyd_pipe_stats* stats, uint16_t* mb,
-             uint16_t* v, uint64_t* ptime, uint64_t* makespan, uint32_t* status, void* ws,
-             size_t ws_bytes, void* stream) {
-  if (!sorted_len || !cost || !schemes || !cand || !cand_np || !pipe || !stats || !mb || !v || !ptime ||
+             int n_cand, int max_np, const uint8_t* pipe, const hyd_pipe_stats* stats,
+             const uint32_t* members, uint16_t* mb, uint16_t* v, uint64_t* ptime, uint64_t* makespan,
+             uint32_t* status, void* ws, size_t ws_bytes, void* stream) {
+  if (!sorted_len || !cost || !schemes || !cand || !cand_np || !pipe || !stats || !members || !mb || !v || !ptime ||
       !makespan || !status || !common_ok(n_iter, batch, n_schemes, k_pad) ||
       !cand_ok(n_cand, max_np))
     return HYD_E_INVALID;
   if (!ws || ws_bytes < pack_workspace(n_iter, batch, n_cand, max_np)) return HYD_E_WORKSPACE;
   return launch_pack(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np,
-                     n_cand, max_np, pipe, stats, mb, v, ptime, makespan, status, ws, ws_bytes,
+                     n_cand, max_np, pipe, stats, members, mb, v, ptime, makespan, status, ws, ws_bytes,
                      (cudaStream_t)stream);
 }
 
@@ -257,11 +259,12 @@ int hyd_assign_host(const uint32_t* len_host, int n_iter, int batch, const hyd_s
                         sorted, perm, cost, st, s);
   if (rc) return rc;
   auto* pst = static_cast<hyd_pipe_stats*>(D(L.stats));
+  auto* mem = static_cast<uint32_t*>(D(L.members));
   rc = launch_dispatch(sorted, cost, n_iter, batch, k_pad, sch, n_schemes, cand, cnp, n_cand, max_np,
-                       pipe, static_cast<uint64_t*>(D(L.lb)), pst, st, s);
+                       pipe, static_cast<uint64_t*>(D(L.lb)), pst, mem, st, s);
   if (rc) return rc;
   rc = launch_pack(sorted, cost, n_iter, batch, k_pad, sch, n_schemes, cand, cnp, n_cand, max_np,
-                   pipe, pst, mb, vv, pt, ms, st, D(L.pack_ws), L.pack_bytes, s);
+                   pipe, pst, mem, mb, vv, pt, ms, st, D(L.pack_ws), L.pack_bytes, s);
   if (rc) return rc;
   rc = launch_select(ms, n_iter, n_cand, cand_offset, key, st, s);
   if (rc) return rc;

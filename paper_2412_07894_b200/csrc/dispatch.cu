@@ -28,12 +28,14 @@ __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
                                              const uint32_t (&pp)[DP], const uint32_t (&kk)[DP],
                                              uint8_t* __restrict__ prow, uint32_t* s_cnt,
                                              uint32_t* s_tmax, unsigned long long* s_sum,
+                                             uint32_t* __restrict__ mbits, int np, int nwords,
                                              uint64_t& lb_out, TT (&base)[DP]) {
-  uint32_t mult[DP];
+  uint32_t mult[DP], bits[DP];
 #pragma unroll
   for (int j = 0; j < DP; ++j) {
     base[j] = 0;
     mult[j] = pp[j];
+    bits[j] = 0u;
   }
   const bool words = (B & 3) == 0;
   uint32_t word = 0u;
@@ -52,12 +54,23 @@ __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
         btau = tau;
       }
     }
+    // branch-free update of pipeline bj (a switch here compiles to a divergent jump table)
+    const uint32_t bit = 1u << (i & 31);
 #pragma unroll
-    for (int j = 0; j < DP; ++j)
-      if ((uint32_t)j == bj) {
-        base[j] = best;
-        mult[j] = 1u;
+    for (int j = 0; j < DP; ++j) {
+      const uint32_t hit = 0u - (uint32_t)((uint32_t)j == bj);
+      const TT hitw = (TT)0 - (TT)((uint32_t)j == bj);
+      base[j] = (base[j] & ~hitw) | (best & hitw);
+      mult[j] = (mult[j] & ~hit) | (1u & hit);
+      bits[j] |= bit & hit;
+    }
+    if ((i & 31) == 31 || i == B - 1) {  // flush one membership word per pipeline
+#pragma unroll
+      for (int j = 0; j < DP; ++j) {
+        if (j < np) mbits[(size_t)j * nwords + (i >> 5)] = bits[j];
+        bits[j] = 0u;
       }
+    }
     // statistics column of pipeline bj (this thread's column)
     const uint32_t n = s_cnt[bj * kDispatchThreads];
     if (n == 0u) s_tmax[bj * kDispatchThreads] = btau;
@@ -86,7 +99,7 @@ __global__ void __launch_bounds__(kDispatchThreads)
                int n_schemes, const uint8_t* __restrict__ cand, const uint8_t* __restrict__ cand_np,
                int n_cand, int max_np, int ct, int tt, uint8_t* __restrict__ pipe,
                uint64_t* __restrict__ lb, hyd_pipe_stats* __restrict__ stats,
-               uint32_t* __restrict__ status) {
+               uint32_t* __restrict__ members, uint32_t* __restrict__ status) {
   extern __shared__ __align__(16) uint32_t sm[];
   // dynamic smem: [stage: tt*B*(1+k_pad) u32 if STAGED] [s_sum u64][s_cnt u32][s_tmax u32]
   const size_t stage_words = STAGED ? (size_t)tt * batch * (1 + k_pad) : 0;
@@ -179,11 +192,15 @@ __global__ void __launch_bounds__(kDispatchThreads)
     }
   }
   if (!ok) flag(status, HYD_F_NOT_CANONICAL);
+  const size_t srow = (size_t)t * n_cand + c;  // iteration-major stats / members row
   if (!ok || sl[0] > ml[0]) {  // infeasible candidate for this iteration
     for (int i = 0; i < B; ++i) prow[i] = 0xFF;
     lb[row] = ~0ull;
+    stats[srow * max_np].u = 0xFFFFFFFFu;
     return;
   }
+  const int nwords = (B + 31) >> 5;
+  uint32_t* mbits = members + srow * max_np * nwords;
   uint32_t* cnt = s_cnt + tid;
   uint32_t* tmx = s_tmax + tid;
   unsigned long long* ssum = s_sum + tid;
@@ -191,14 +208,16 @@ __global__ void __launch_bounds__(kDispatchThreads)
   uint64_t base64[DP];
   if (narrow) {
     uint32_t base[DP];
-    dispatch_run<DP, uint32_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, cnt, tmx, ssum, lbv, base);
+    dispatch_run<DP, uint32_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, cnt, tmx, ssum, mbits, np,
+                               nwords, lbv, base);
 #pragma unroll
     for (int j = 0; j < DP; ++j) base64[j] = base[j];
   } else {
-    dispatch_run<DP, uint64_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, cnt, tmx, ssum, lbv, base64);
+    dispatch_run<DP, uint64_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, cnt, tmx, ssum, mbits, np,
+                               nwords, lbv, base64);
   }
   lb[row] = lbv;
-  hyd_pipe_stats* st = stats + row * max_np;
+  hyd_pipe_stats* st = stats + srow * max_np;
 #pragma unroll
   for (int j = 0; j < DP; ++j) {
     if (j < np) {
@@ -220,7 +239,7 @@ static cudaError_t launch_dp(bool staged, dim3 grid, size_t smem_stage, cudaStre
                              int k_pad, const hyd_scheme* schemes, int n_schemes,
                              const uint8_t* cand, const uint8_t* cand_np, int n_cand, int max_np,
                              int ct, int tt, uint8_t* pipe, uint64_t* lb, hyd_pipe_stats* stats,
-                             uint32_t* status) {
+                             uint32_t* members, uint32_t* status) {
   const size_t cols = (size_t)DP * kDispatchThreads * 16;
   cudaError_t e;
   if (staged) {
@@ -229,13 +248,13 @@ static cudaError_t launch_dp(bool staged, dim3 grid, size_t smem_stage, cudaStre
     if (e != cudaSuccess) return e;
     k_dispatch<DP, true><<<grid, kDispatchThreads, smem, s>>>(
         sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np,
-        ct, tt, pipe, lb, stats, status);
+        ct, tt, pipe, lb, stats, members, status);
   } else {
     e = cudaFuncSetAttribute(k_dispatch<DP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols);
     if (e != cudaSuccess) return e;
     k_dispatch<DP, false><<<grid, kDispatchThreads, cols, s>>>(
         sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np,
-        ct, tt, pipe, lb, stats, status);
+        ct, tt, pipe, lb, stats, members, status);
   }
   return cudaGetLastError();
 }
@@ -243,7 +262,7 @@ static cudaError_t launch_dp(bool staged, dim3 grid, size_t smem_stage, cudaStre
 int launch_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch,
                     int k_pad, const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
                     const uint8_t* cand_np, int n_cand, int max_np, uint8_t* pipe, uint64_t* lb,
-                    hyd_pipe_stats* stats, uint32_t* status, cudaStream_t s) {
+                    hyd_pipe_stats* stats, uint32_t* members, uint32_t* status, cudaStream_t s) {
   if (n_iter == 0 || n_cand == 0) return HYD_OK;
   const int ct = n_cand < kDispatchThreads ? n_cand : kDispatchThreads;
   const int tt = kDispatchThreads / ct;
@@ -255,11 +274,11 @@ int launch_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter
   dim3 grid((n_cand + ct - 1) / ct, (n_iter + tt - 1) / tt);
   cudaError_t e;
   switch (dp) {
-    case 2: e = launch_dp<2>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, status); break;
-    case 4: e = launch_dp<4>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, status); break;
-    case 8: e = launch_dp<8>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, status); break;
-    case 16: e = launch_dp<16>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, status); break;
-    default: e = launch_dp<32>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, status); break;
+    case 2: e = launch_dp<2>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status); break;
+    case 4: e = launch_dp<4>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status); break;
+    case 8: e = launch_dp<8>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status); break;
+    case 16: e = launch_dp<16>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status); break;
+    default: e = launch_dp<32>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status); break;
   }
   note_launch();
   return e == cudaSuccess ? HYD_OK : record_cuda_error(e);

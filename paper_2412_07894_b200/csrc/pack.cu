@@ -36,8 +36,8 @@
 
 namespace hyd {
 
-constexpr int kLaneVMax = 16;     // largest V handled by k_pack_lanes
 constexpr int kLaneThreads = 256;
+constexpr int kLaneEpoch = 8;     // sequences per lane between bookkeeping phases
 constexpr int kBigRMax = 8;       // k_pack_big: register bins per lane (V <= 256)
 constexpr int kBigWarps = 2048;   // persistent warps of k_pack_big (scratch slots)
 
@@ -52,6 +52,8 @@ struct PackArgs {
   int n_cand;
   const uint8_t* pipe;
   const hyd_pipe_stats* stats;
+  const uint32_t* members;  // [C][It][mnp][nwords] membership bitmaps from hyd_dispatch
+  int mnp, nwords;
   uint16_t* mb;
   uint16_t* v;
   uint64_t* ptime;
@@ -60,8 +62,10 @@ struct PackArgs {
   unsigned long long* q_count;
   unsigned long long* q_head;
   unsigned long long* evals;  // (item, bin) evaluations performed (ws bytes [16, 24))
+  unsigned long long* why;    // hand-off reason counters (ws bytes [24, 88)), diagnostic
   unsigned long long* queue;
   unsigned long long q_cap;
+  uint32_t* flags;  // [It*C*mnp bits] tasks handed from the VMAX-16 to the VMAX-32 lane pass
   uint64_t* scr_time;  // [kBigWarps][B]
   uint32_t* scr_tok;   // [kBigWarps][B]
 };
@@ -74,12 +78,21 @@ struct Search {
   bool have;
 };
 
+__device__ __forceinline__ uint32_t ceil_div_small(uint64_t n, uint32_t d) {
+  // n / d rounded up, with a 32-bit division when n fits
+  return n < 0xFFFFFFFFull - d ? ((uint32_t)n + d - 1u) / d : (uint32_t)((n + d - 1) / d);
+}
+
 __device__ __forceinline__ void search_init(Search& s) {
-  const uint64_t vlo = max((s.S + s.M - 1) / s.M, (uint64_t)1);
-  uint64_t vhi = s.UL ? min(s.S / s.UL, (uint64_t)s.U) : (uint64_t)s.U;
+  const uint32_t vlo = max(ceil_div_small(s.S, s.M), 1u);
+  uint32_t vhi = s.U;
+  if (s.UL) {
+    const uint64_t q = s.S < 0xFFFFFFFFull ? (uint64_t)((uint32_t)s.S / s.UL) : s.S / s.UL;
+    vhi = q < (uint64_t)s.U ? (uint32_t)q : s.U;
+  }
   if (vhi < vlo) vhi = vlo;
-  s.vlo = (uint32_t)vlo;
-  s.vhi = (uint32_t)vhi;
+  s.vlo = vlo;
+  s.vhi = vhi;
   uint32_t va = s.vlo;
   if (s.P > 1 && s.tau_max > 0) {
     const float vc = (float)s.sumT / (float)s.tau_max;
@@ -130,25 +143,44 @@ __device__ __forceinline__ uint32_t search_next(Search& s) {
   return 0;
 }
 
-// largest max-bin time that can still improve (obj, V)
-__device__ __forceinline__ uint64_t search_thr(const Search& s, uint32_t V) {
+// A bin-time ceiling for early abort that is never below the exact one (the exact test
+// is repeated when a run completes): floor(best/(PP-1+V)) estimated in fp32 with slack.
+__device__ __forceinline__ uint64_t search_thr_approx(const Search& s, uint32_t V) {
   if (!s.have) return ~0ull;
-  const uint64_t m = (uint64_t)(s.P - 1 + V);
-  if (V < s.vbest) return s.best / m;
-  return s.best == 0 ? 0ull : (s.best - 1) / m;
+  const float q = (float)s.best / (float)(s.P - 1 + V);
+  return (uint64_t)(q * 1.0001f) + 2ull;
+}
+
+// exact: does LPT(V) with this max bin time improve (best, V_best)?
+__device__ __forceinline__ bool search_improves(const Search& s, uint32_t V, uint64_t maxbin) {
+  if (!s.have) return true;
+  const uint64_t obj = maxbin * (uint64_t)(s.P - 1 + V);
+  return obj < s.best || (obj == s.best && V < s.vbest);
 }
 
 __device__ __forceinline__ void search_take(Search& s, uint32_t V, uint64_t maxbin) {
   s.best = maxbin * (uint64_t)(s.P - 1 + V);
   s.vbest = V;
   s.have = true;
+  // every V < ceil(sumT (PP-1) / (best - sumT)) has sumT (PP-1+V) > best V: jump past them
+  // (fp32 estimate minus a margin of 2; the exact per-V tests in search_next stay in force)
+  if (s.phase == 1 && s.P > 1) {
+    if (s.best <= s.sumT) {
+      s.cursor = s.vhi + 1;
+    } else {
+      const float est = (float)s.sumT * (float)(s.P - 1) / (float)(s.best - s.sumT);
+      const float lo = est - 2.0f;
+      if (lo > (float)s.cursor) s.cursor = lo >= (float)s.vhi ? s.vhi + 1 : (uint32_t)lo;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ pair-level init
 // makespan = 0 (feasible) or UINT64_MAX (infeasible); v/ptime rows zeroed; infeasible
 // pairs get mb = 0xFFFF.  Tasks then write their v/ptime slot and atomicMax the makespan.
-__global__ void __launch_bounds__(256) k_pack_init(const uint8_t* __restrict__ pipe, int n_iter,
-                                                   int batch, int n_cand, uint16_t* __restrict__ mb,
+__global__ void __launch_bounds__(256) k_pack_init(const hyd_pipe_stats* __restrict__ stats,
+                                                   int mnp, int n_iter, int batch, int n_cand,
+                                                   uint16_t* __restrict__ mb,
                                                    uint16_t* __restrict__ v,
                                                    uint64_t* __restrict__ ptime,
                                                    uint64_t* __restrict__ makespan) {
@@ -156,7 +188,7 @@ __global__ void __launch_bounds__(256) k_pack_init(const uint8_t* __restrict__ p
   if (e >= (size_t)n_iter * n_cand) return;
   const int t = (int)(e / n_cand), c = (int)(e - (size_t)t * n_cand);
   const size_t row = (size_t)c * n_iter + t;
-  const bool feasible = pipe[row * batch] != 0xFF;
+  const bool feasible = stats[e * mnp].u != 0xFFFFFFFFu;  // e = t * n_cand + c
   makespan[(size_t)t * n_cand + c] = feasible ? 0ull : ~0ull;
   uint4* v4 = reinterpret_cast<uint4*>(v + row * HYD_MAX_PIPES);
   uint4* p4 = reinterpret_cast<uint4*>(ptime + row * HYD_MAX_PIPES);
@@ -176,13 +208,20 @@ __global__ void __launch_bounds__(256) k_pack_init(const uint8_t* __restrict__ p
   }
 }
 
-// ------------------------------------------------------------------ persistent lanes (V <= 16)
-// bins as packed u32 keys: key_b = time_b << 5 | b (needs sumT < 2^26), tokens tok_b.
-// masked_b = key_b | ((cap - tok_b) & 2^31) is >= 2^31 iff tok_b + l > MaxLen, so the
-// minimum masked key is the least-time fitting bin with the smallest index.
-template <int N>
-__device__ __forceinline__ uint32_t argmin_keys(const uint32_t (&keys)[kLaneVMax],
-                                                const uint32_t (&toks)[kLaneVMax], uint32_t cap) {
+// ------------------------------------------------------------------ persistent lanes (V <= 32)
+// bins as packed u32 keys: key_b = time_b << SH | b, tokens tok_b.  SH = 4 for VMAX 16
+// (sumT < 2^27), 5 for VMAX 32 (sumT < 2^26).  masked_b = key_b | ((cap - tok_b) & 2^31) is
+// >= 2^31 iff tok_b + l > MaxLen, so the minimum masked key is the least-time fitting bin with
+// the smallest index.
+template <int VM>
+struct LaneCfg {
+  static constexpr int SH = VM <= 16 ? 4 : 5;
+  static constexpr uint64_t SUMT_LIMIT = 1ull << (31 - SH);
+};
+
+template <int N, int VM>
+__device__ __forceinline__ uint32_t argmin_keys(const uint32_t (&keys)[VM],
+                                                const uint32_t (&toks)[VM], uint32_t cap) {
   uint32_t m[N];
 #pragma unroll
   for (int b = 0; b < N; ++b) m[b] = keys[b] | ((cap - toks[b]) & 0x80000000u);
@@ -193,35 +232,242 @@ __device__ __forceinline__ uint32_t argmin_keys(const uint32_t (&keys)[kLaneVMax
   return m[0];
 }
 
-template <int N>
-__device__ __forceinline__ void place_key(uint32_t (&keys)[kLaneVMax], uint32_t (&toks)[kLaneVMax],
-                                          uint32_t mk, uint32_t tau5, uint32_t l) {
+template <int N, int VM>
+__device__ __forceinline__ void place_key(uint32_t (&keys)[VM], uint32_t (&toks)[VM], uint32_t mk,
+                                          uint32_t tau_sh, uint32_t l) {
 #pragma unroll
   for (int b = 0; b < N; ++b) {
     const bool hit = keys[b] == mk;
-    keys[b] += hit ? tau5 : 0u;
+    keys[b] += hit ? tau_sh : 0u;
     toks[b] += hit ? l : 0u;
   }
 }
 
-struct LaneRun {
-  uint32_t V, thr, mx, wV;
-  bool writing, final_run;
+// per-CTA task records (compacted slots), built in parallel before the lane phases
+struct TaskRecs {
+  unsigned long long* key;  // best (obj << 16 | V) found so far
+  uint32_t* sum_t;
+  uint32_t* tau_max;
+  uint32_t* eid;    // tile-local task id: (candidate - c0) * mnp + j
+  uint32_t* list2;  // phase-2 units: slot << 16 | V (class 16 from the front, class 8 from the middle)
+  uint16_t* u;
+  uint16_t* vlo;
+  uint16_t* vhi;
+  uint16_t* va;
+  uint16_t* perm;   // phase-1 order of slots (longest-processing-time first)
+  uint8_t* k;
+  uint8_t* state;   // 0 active, 1 handed to another pass, 2 no phase-2 candidates
 };
 
-template <bool STAGED>
-__global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int tc, int mnp) {
+// one bulk L2 prefetch of a contiguous block (TMA engine), clipped to 16-byte granules
+__device__ __forceinline__ void prefetch_l2_block(const void* base, size_t off, size_t bytes, size_t total) {
+  size_t lo = off & ~(size_t)15, hi = (off + bytes + 15) & ~(size_t)15;
+  if (hi > (total & ~(size_t)15)) hi = total & ~(size_t)15;
+  if (hi <= lo) return;
+  const char* p = static_cast<const char*>(base) + lo;
+  size_t n = hi - lo;
+  while (n) {
+    const uint32_t chunk = n > (1u << 20) ? (1u << 20) : (uint32_t)n;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(chunk) : "memory");
+    p += chunk;
+    n -= chunk;
+  }
+}
+
+// One LPT run as a lane's unit of work (state carried across loop iterations).
+template <int VM>
+struct LaneUnit {
+  uint32_t keys[VM], toks[VM];
+  const uint32_t* mw;
+  uint16_t* mrow;
+  uint32_t qw, cur, wbase, nxtw;
+  uint32_t V, thr, mx, k, M;
+  int e;
+  bool write;
+};
+
+template <int VM>
+__device__ __forceinline__ void unit_start(LaneUnit<VM>& u, uint32_t V, uint32_t thr) {
+  u.V = V;
+  u.thr = thr;
+  u.mx = 0;
+#pragma unroll
+  for (int b = 0; b < VM; ++b) {
+    u.keys[b] = (uint32_t)b < V ? (uint32_t)b : 0xFFFFFFFFu;
+    u.toks[b] = 0u;
+  }
+  u.qw = 0;
+  u.cur = 0;
+  u.nxtw = __ldg(u.mw);
+}
+
+// Advance the unit by one sequence.  Returns 0 while running, 1 when the run completed,
+// 2 when it failed (no micro-batch fits: LPT(V) infeasible, or it cannot beat u.thr).
+template <int N, int VM>
+__device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords,
+                                         const uint32_t* __restrict__ slen,
+                                         const uint32_t* __restrict__ cst, int kp, uint64_t& ev) {
+  constexpr int SH = LaneCfg<VM>::SH;
+  while (u.cur == 0) {  // next membership word (prefetched one ahead)
+    if (u.qw >= nwords) return 1;
+    u.cur = u.nxtw;
+    u.wbase = u.qw * 32u;
+    ++u.qw;
+    u.nxtw = u.qw < nwords ? __ldg(u.mw + u.qw) : 0u;
+  }
+  const uint32_t i = u.wbase + (uint32_t)(__ffs(u.cur) - 1);
+  u.cur &= u.cur - 1u;
+  const uint32_t l = slen[i];
+  const uint32_t tau = cst[(size_t)i * kp + u.k];
+  ev += u.V;
+  const uint32_t mk = argmin_keys<N, VM>(u.keys, u.toks, u.M - l);
+  if (mk >> 31) return 2;
+  place_key<N, VM>(u.keys, u.toks, mk, tau << SH, l);
+  u.mx = max(u.mx, (mk >> SH) + tau);
+  if (u.write) u.mrow[i] = (uint16_t)(mk & ((1u << SH) - 1u));
+  return u.mx > u.thr ? 2 : 0;
+}
+
+// VM = 16: every (c,t,j) of the tile, classes 8 / 16; a task needing some V > 16 is flagged
+//          for the VM = 32 pass.  VM = 32: flagged tasks only (whole-iteration tiles, records
+//          compacted).  Tasks the lanes cannot hold (V > VM in the last pass, sumT over the key
+//          limit, an infeasible V_a and V_a + 1) go to the warp queue, which runs the sequential
+//          exact search.
+template <bool STAGED, int VM>
+__global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int tc, int mnp, int ncap) {
+  constexpr int NB = 64;  // LPT-order buckets: (class, U) descending
+  constexpr unsigned long long kBottom = ~0ull;
   extern __shared__ __align__(16) uint32_t sm[];
-  __shared__ int s_n8, s_n16, s_next;
+  __shared__ int s_next, s_nrec, s_n2a, s_n2b;
+  __shared__ int s_hist[NB];
+  __shared__ uint32_t s_ml[HYD_MAX_SCHEMES], s_pp[HYD_MAX_SCHEMES], s_ul[HYD_MAX_SCHEMES];
   const int B = a.batch, kp = a.k_pad;
   const int t = blockIdx.y, c0 = blockIdx.x * tc;
-  const int tid = threadIdx.x;
-  const int ntask_max = tc * mnp;
-  uint16_t* list = reinterpret_cast<uint16_t*>(sm + (STAGED ? (size_t)B * (1 + kp) : 0));
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int ncl = min(tc, a.n_cand - c0);
+  const int ntile = ncl * mnp;  // task ids of the tile
+  const uint32_t nwords = (uint32_t)a.nwords;
+  const size_t fbase = ((size_t)t * a.n_cand + c0) * mnp;  // first task bit / stats row of the tile
+  if (tid == 0 && VM == 16) {  // this CTA's stats and membership rows are contiguous: pull them into L2
+    const size_t total_rows = (size_t)a.n_iter * a.n_cand * mnp;
+    prefetch_l2_block(a.members, fbase * nwords * 4, (size_t)ntile * nwords * 4, total_rows * nwords * 4);
+    prefetch_l2_block(a.stats, fbase * sizeof(hyd_pipe_stats), (size_t)ntile * sizeof(hyd_pipe_stats),
+                      total_rows * sizeof(hyd_pipe_stats));
+  }
+  // dynamic smem: [stage B*(1+kp) u32] [key u64] [sum_t, tau_max, eid, list2 u32]
+  //               [u, vlo, vhi, va, perm u16] [k, state u8]   (ncap slots each)
+  uint32_t* recbase = sm + (STAGED ? (size_t)B * (1 + kp) : 0);
+  TaskRecs R;
+  R.key = reinterpret_cast<unsigned long long*>(recbase);
+  R.sum_t = reinterpret_cast<uint32_t*>(R.key + ncap);
+  R.tau_max = R.sum_t + ncap;
+  R.eid = R.tau_max + ncap;
+  R.list2 = R.eid + ncap;
+  R.u = reinterpret_cast<uint16_t*>(R.list2 + ncap);
+  R.vlo = R.u + ncap;
+  R.vhi = R.vlo + ncap;
+  R.va = R.vhi + ncap;
+  R.perm = R.va + ncap;
+  R.k = reinterpret_cast<uint8_t*>(R.perm + ncap);
+  R.state = R.k + ncap;
   if (tid == 0) {
-    s_n8 = 0;
-    s_n16 = 0;
     s_next = 0;
+    s_nrec = 0;
+    s_n2a = 0;
+    s_n2b = 0;
+  }
+  for (int b = tid; b < NB; b += kLaneThreads) s_hist[b] = 0;
+  for (int k = tid; k < a.n_schemes; k += kLaneThreads) {
+    s_ml[k] = a.schemes[k].max_len;
+    s_pp[k] = a.schemes[k].pp;
+    s_ul[k] = a.schemes[k].util_len;
+  }
+  __syncthreads();
+
+  auto to_queue = [&](int c, int j) {
+    const unsigned long long slot = atomicAdd(a.q_count, 1ull);
+    if (slot < a.q_cap)
+      a.queue[slot] = ((unsigned long long)c << 37) | ((unsigned long long)t << 5) | (unsigned)j;
+  };
+  auto hand_off_e = [&](int e) {  // the task leaves this pass
+    const int c = c0 + e / mnp, j = e % mnp;
+    if (VM == 16) {
+      const size_t bit = fbase + e;
+      atomicOr(a.flags + (bit >> 5), 1u << (bit & 31));
+    } else {
+      to_queue(c, j);
+    }
+  };
+
+  // ---- task records (parallel, compacted), bucketed by (class, U) for LPT-order processing
+  for (int e = tid; e < ntile; e += kLaneThreads) {
+    const int c = c0 + e / mnp, j = e % mnp;
+    if (j >= (int)a.cand_np[c]) continue;
+    if (VM == 32) {
+      const size_t bit = fbase + e;
+      if (!((a.flags[bit >> 5] >> (bit & 31)) & 1u)) continue;
+    }
+    const hyd_pipe_stats* sp = a.stats + (fbase + e - j);
+    if (VM == 16 && sp[0].u == 0xFFFFFFFFu) continue;  // infeasible pair: k_pack_init wrote it
+    const hyd_pipe_stats st = sp[j];
+    if (st.u == 0) continue;  // empty pipeline: V = ptime = 0 (k_pack_init)
+    const uint32_t k = a.cand[(size_t)c * HYD_MAX_PIPES + j];
+    Search s;
+    s.M = s_ml[k];
+    s.P = s_pp[k];
+    s.UL = s_ul[k];
+    s.U = st.u;
+    s.S = st.s;
+    s.sumT = st.sum_t;
+    s.tau_max = st.tau_max;
+    search_init(s);
+    if (s.sumT >= LaneCfg<VM>::SUMT_LIMIT || s.M >= 0x80000000u || (VM == 32 && s.va > 32u)) {
+      atomicAdd(a.why + (VM == 16 ? 0 : 4), 1ull);
+      to_queue(c, j);
+      continue;
+    }
+    if (VM == 16 && s.va > 16u) {
+      atomicAdd(a.why + 1, 1ull);
+      hand_off_e(e);
+      continue;
+    }
+    const int r = atomicAdd(&s_nrec, 1);
+    if (r >= ncap) {  // record space full (whole-iteration tiles of the VM = 32 pass)
+      atomicAdd(a.why + 7, 1ull);
+      to_queue(c, j);
+      continue;
+    }
+    R.eid[r] = (uint32_t)e;
+    R.sum_t[r] = (uint32_t)s.sumT;
+    R.tau_max[r] = s.tau_max;
+    R.u[r] = (uint16_t)s.U;
+    R.vlo[r] = (uint16_t)s.vlo;
+    R.vhi[r] = (uint16_t)s.vhi;
+    R.va[r] = (uint16_t)s.va;
+    R.k[r] = (uint8_t)k;
+    R.state[r] = 0;
+    const int ub = min(31, (int)(s.U >> 3));
+    const int bk = (VM == 16 && s.va <= 8) ? ub : 32 + ub;  // heavier class first, then larger U
+    R.perm[r] = (uint16_t)bk;  // bucket, replaced by the order below
+    atomicAdd(&s_hist[bk], 1);
+  }
+  __syncthreads();
+  const int nrec = min(s_nrec, ncap);
+  if (nrec == 0) return;
+  if (tid == 0) {  // exclusive scan over the 64 buckets in descending order
+    int run = 0;
+    for (int b = NB - 1; b >= 0; --b) {
+      const int h = s_hist[b];
+      s_hist[b] = run;
+      run += h;
+    }
+  }
+  __syncthreads();
+  {
+    // bucket -> position (list2 is free until phase 1.5: used as scratch for the order)
+    for (int r = tid; r < nrec; r += kLaneThreads) R.list2[atomicAdd(&s_hist[R.perm[r]], 1)] = (uint32_t)r;
+    __syncthreads();
+    for (int q = tid; q < nrec; q += kLaneThreads) R.perm[q] = (uint16_t)R.list2[q];
   }
   if (STAGED) {
     const uint4* gl = reinterpret_cast<const uint4*>(a.sorted_len + (size_t)t * B);
@@ -234,172 +480,193 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
   __syncthreads();
   const uint32_t* slen = STAGED ? sm : a.sorted_len + (size_t)t * B;
   const uint32_t* cst = STAGED ? sm + B : a.cost + (size_t)t * B * kp;
-  const bool vec_ok = (B & 15) == 0;
 
-  // ---- task list of this CTA, split into VMAX classes 8 (front) and 16 (back)
-  for (int e = tid; e < ntask_max; e += kLaneThreads) {
-    const int c = c0 + e / mnp, j = e % mnp;
-    if (c >= a.n_cand || j >= (int)a.cand_np[c]) continue;
+  LaneUnit<VM> u;
+  uint64_t ev = 0;
+  auto load_unit = [&](int r, uint32_t V, uint32_t thr, bool write) {
+    const int e = (int)R.eid[r];
+    const int c = c0 + e / mnp;
     const size_t row = (size_t)c * a.n_iter + t;
-    if (a.pipe[row * B] == 0xFF) continue;  // infeasible pair: k_pack_init wrote it
-    const hyd_pipe_stats st = a.stats[row * mnp + j];
-    if (st.u == 0) continue;  // empty pipeline: V = ptime = 0 (k_pack_init)
-    const uint32_t k = a.cand[(size_t)c * HYD_MAX_PIPES + j];
-    Search s;
-    s.M = a.schemes[k].max_len;
-    s.P = a.schemes[k].pp;
-    s.UL = a.schemes[k].util_len;
-    s.U = st.u;
-    s.S = st.s;
-    s.sumT = st.sum_t;
-    s.tau_max = st.tau_max;
-    search_init(s);
-    if (!vec_ok || s.sumT >= (1ull << 26) || s.M >= 0x80000000u || s.va > (uint32_t)kLaneVMax) {
-      const unsigned long long slot = atomicAdd(a.q_count, 1ull);
-      if (slot < a.q_cap)
-        a.queue[slot] = ((unsigned long long)c << 37) | ((unsigned long long)t << 5) | (unsigned)j;
-    } else if (s.va <= 8) {
-      list[atomicAdd(&s_n8, 1)] = (uint16_t)e;
-    } else {
-      list[ntask_max - 1 - atomicAdd(&s_n16, 1)] = (uint16_t)e;
+    u.e = r;
+    u.k = R.k[r];
+    u.M = s_ml[u.k];
+    u.mw = a.members + (fbase + e) * nwords;
+    u.mrow = a.mb + row * B;
+    u.write = write;
+    unit_start<VM>(u, V, thr);
+  };
+  // Lanes run epochs of kLaneEpoch sequences of their current unit; between epochs all lanes
+  // that finished a unit record its result and pull the next one together (converged), so the
+  // per-unit work never runs one lane at a time.  pull(q) returns false for units to skip.
+  auto run_units = [&](int n_units, auto&& pull, auto&& finish) {
+    if (tid == 0) s_next = 0;
+    __syncthreads();
+    bool have = false, done = false;
+    while (true) {
+      while (!have && !done) {
+        const int q = atomicAdd(&s_next, 1);
+        if (q >= n_units) done = true;
+        else have = pull(q);
+      }
+      if (__all_sync(HYD_FULL, done && !have)) break;
+      if (have) {
+        int st = 0;
+#pragma unroll 1
+        for (int e = 0; e < kLaneEpoch && st == 0; ++e) {
+          if (VM == 16 && u.V <= 8) st = unit_step<8, VM>(u, nwords, slen, cst, kp, ev);
+          else st = unit_step<VM, VM>(u, nwords, slen, cst, kp, ev);
+        }
+        if (st) {
+          finish(st);
+          have = false;
+        }
+      }
     }
+    __syncthreads();
+  };
+  auto obj_key = [&](const LaneUnit<VM>& w) {
+    return (((uint64_t)w.mx * (uint64_t)(s_pp[w.k] - 1 + w.V)) << 16) | w.V;
+  };
+
+  // ---- phase 1: the V_a run of every task (writes mb)
+  run_units(
+      nrec,
+      [&](int q) {
+        const int r = R.perm[q];
+        load_unit(r, R.va[r], 0xFFFFFFFFu, true);
+        return true;
+      },
+      [&](int st) { R.key[u.e] = st == 1 ? obj_key(u) : kBottom; });
+
+  // ---- phase 1b: where LPT(V_a) is infeasible (capacity), V_a + 1 is tried; it then takes
+  //      V_a's place as the reference run of the exact tests below
+  run_units(
+      nrec,
+      [&](int q) {
+        const int r = R.perm[q];
+        if (R.key[r] != kBottom) return false;
+        const uint32_t V = (uint32_t)R.va[r] + 1u;
+        if (V > (uint32_t)R.vhi[r] || V > (uint32_t)VM) return false;
+        R.va[r] = (uint16_t)V;
+        load_unit(r, V, 0xFFFFFFFFu, true);
+        return true;
+      },
+      [&](int st) {
+        if (st == 1) R.key[u.e] = obj_key(u);
+      });
+
+  // ---- phase 1.5 (thread per task): every V of App. D's range that survives the exact tests
+  //      against the reference run, reserved contiguously per task in list2 (class 16 from the
+  //      front half, class 8 from the back half); a task that does not fit is handed off
+  auto walk = [&](int r, Search& s) {
+    s.P = s_pp[R.k[r]];
+    s.U = R.u[r];
+    s.sumT = R.sum_t[r];
+    s.tau_max = R.tau_max[r];
+    s.vlo = R.vlo[r];
+    s.vhi = R.vhi[r];
+    s.va = R.va[r];
+    s.cursor = s.vlo;
+    s.phase = 1;
+    s.have = false;
+    search_take(s, s.va, (R.key[r] >> 16) / (uint64_t)(s.P - 1 + s.va));  // reference, cursor jump
+  };
+  const int half = ncap / 2;
+  for (int r = tid; r < nrec; r += kLaneThreads) {
+    if (R.key[r] == kBottom) {  // the sequential search (with extension) runs elsewhere
+      atomicAdd(a.why + (VM == 16 ? 2 : 5), 1ull);
+      const int e = (int)R.eid[r];
+      to_queue(c0 + e / mnp, e % mnp);
+      R.state[r] = 1;
+      continue;
+    }
+    Search s;
+    walk(r, s);
+    int cnt = 0;
+    uint32_t vmax = 0, V;
+    while ((V = search_next(s)) != 0) {
+      vmax = max(vmax, V);
+      ++cnt;
+    }
+    if (vmax > (uint32_t)VM) {
+      atomicAdd(a.why + (VM == 16 ? 3 : 6), 1ull);
+      hand_off_e((int)R.eid[r]);
+      R.state[r] = 1;
+      continue;
+    }
+    if (cnt == 0) {
+      R.state[r] = 2;
+      continue;
+    }
+    const bool small = VM == 16 && vmax <= 8;
+    const int base = atomicAdd(small ? &s_n2b : &s_n2a, cnt);
+    if (base + cnt > half) {  // does not fit: void the reserved slots inside the half
+      uint32_t* dst = R.list2 + (small ? half : 0);
+      for (int q = base; q < min(base + cnt, half); ++q) dst[q] = 0xFFFFFFFFu;
+      atomicAdd(a.why + 7, 1ull);
+      hand_off_e((int)R.eid[r]);
+      R.state[r] = 1;
+      continue;
+    }
+    walk(r, s);
+    int n = 0;
+    uint32_t* dst = R.list2 + (small ? half : 0) + base;
+    while ((V = search_next(s)) != 0 && n < cnt) dst[n++] = ((uint32_t)r << 16) | V;
   }
   __syncthreads();
-  const int n8 = s_n8, ntask = s_n8 + s_n16;
+  const int n2a = min(s_n2a, half), n2b = min(s_n2b, half);
 
-  // ---- persistent lane state machine: one sequence (or one task set-up) per iteration
-  bool have = false;
-  int c = 0, j = 0;
-  uint32_t k = 0, jjjj = 0;
-  size_t row = 0;
-  const uint8_t* prow = nullptr;
-  uint16_t* mrow = nullptr;
-  Search s;
-  LaneRun r;
-  r.V = r.thr = r.mx = r.wV = 0;
-  r.writing = r.final_run = false;
-  uint32_t keys[kLaneVMax], toks[kLaneVMax];
-  uint32_t qc = 0, m16 = 0, cbase = 0;
-  const uint32_t nchunks = (uint32_t)B / 16;
-  uint64_t ev = 0;
+  // ---- phase 2: the surviving V, each an independent run against the reference; argmin by
+  //      atomicMin on (obj << 16 | V)
+  run_units(
+      n2a + n2b,
+      [&](int q) {
+        const uint32_t w = R.list2[q < n2a ? q : half + (q - n2a)];
+        if (w == 0xFFFFFFFFu) return false;
+        const int r = (int)(w >> 16);
+        if (r >= nrec || R.state[r] == 1) return false;
+        const uint32_t V = w & 0xFFFFu;
+        Search s;
+        s.P = s_pp[R.k[r]];
+        s.have = true;
+        s.best = R.key[r] >> 16;
+        const uint64_t th = search_thr_approx(s, V);
+        load_unit(r, V, th > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)th, false);
+        return true;
+      },
+      [&](int st) {
+        if (st == 1) atomicMin(&R.key[u.e], obj_key(u));
+      });
 
-  auto start_run = [&](uint32_t V, bool write, bool fin) {
-    r.V = V;
-    r.writing = write;
-    r.final_run = fin;
-    const uint64_t th = (write || fin) ? ~0ull : search_thr(s, V);
-    r.thr = th > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)th;
-    r.mx = 0;
-#pragma unroll
-    for (int b = 0; b < kLaneVMax; ++b) {
-      keys[b] = (uint32_t)b < V ? (uint32_t)b : 0xFFFFFFFFu;
-      toks[b] = 0u;
-    }
-    qc = 0;
-    m16 = 0;
-  };
-  auto finalize = [&]() {
-    a.v[row * HYD_MAX_PIPES + j] = (uint16_t)s.vbest;
-    a.ptime[row * HYD_MAX_PIPES + j] = s.best;
-    atomicMax(reinterpret_cast<unsigned long long*>(a.makespan + (size_t)t * a.n_cand + c),
-              (unsigned long long)s.best);
-    have = false;
-  };
-  auto defer = [&]() {
-    const unsigned long long slot = atomicAdd(a.q_count, 1ull);
-    if (slot < a.q_cap)
-      a.queue[slot] = ((unsigned long long)c << 37) | ((unsigned long long)t << 5) | (unsigned)j;
-    have = false;
-  };
-  auto run_end = [&](bool ok) {
-    if (ok) {
-      search_take(s, r.V, r.mx);
-      if (r.writing) r.wV = r.V;
-    }
-    if (r.final_run) {
-      finalize();
-      return;
-    }
-    const uint32_t nv = search_next(s);
-    if (nv == 0) {
-      if (!s.have) defer();  // cannot happen (V = U is always feasible); safety net
-      else if (s.vbest != r.wV) start_run(s.vbest, true, true);  // write the winner's mb
-      else finalize();
-    } else if (nv > (uint32_t)kLaneVMax) {
-      defer();
-    } else {
-      start_run(nv, false, false);
-    }
-  };
+  // ---- phase 3: tasks whose winner is not the reference run write their mb with one more run
+  run_units(
+      nrec,
+      [&](int q) {
+        const int r = R.perm[q];
+        if (R.state[r] == 1) return false;
+        const uint32_t V = (uint32_t)(R.key[r] & 0xFFFFu);
+        if (V == R.va[r]) return false;
+        load_unit(r, V, 0xFFFFFFFFu, true);
+        return true;
+      },
+      [&](int) {});
 
-  while (true) {
-    if (!have) {
-      const int e = atomicAdd(&s_next, 1);
-      if (e >= ntask) break;
-      const int le = e < n8 ? list[e] : list[ntask_max - (ntask - e)];
-      c = c0 + le / mnp;
-      j = le % mnp;
-      row = (size_t)c * a.n_iter + t;
-      prow = a.pipe + row * B;
-      mrow = a.mb + row * B;
-      k = a.cand[(size_t)c * HYD_MAX_PIPES + j];
-      jjjj = 0x01010101u * (uint32_t)j;
-      const hyd_pipe_stats st = a.stats[row * mnp + j];
-      s.M = a.schemes[k].max_len;
-      s.P = a.schemes[k].pp;
-      s.UL = a.schemes[k].util_len;
-      s.U = st.u;
-      s.S = st.s;
-      s.sumT = st.sum_t;
-      s.tau_max = st.tau_max;
-      search_init(s);
-      r.wV = 0;
-      start_run(s.va, true, false);  // the first run always completes or is infeasible
-      have = true;
-    }
-    // next member of pipeline j in sorted order: 16 pipe bytes -> 16-bit match mask
-    while (m16 == 0 && qc < nchunks) {
-      const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(prow) + qc);
-      const uint32_t x0 = __vcmpeq4(w4.x, jjjj) & 0x01010101u, x1 = __vcmpeq4(w4.y, jjjj) & 0x01010101u;
-      const uint32_t x2 = __vcmpeq4(w4.z, jjjj) & 0x01010101u, x3 = __vcmpeq4(w4.w, jjjj) & 0x01010101u;
-      m16 = ((x0 * 0x204081u) >> 21 & 0xFu) | (((x1 * 0x204081u) >> 21 & 0xFu) << 4) |
-            (((x2 * 0x204081u) >> 21 & 0xFu) << 8) | (((x3 * 0x204081u) >> 21 & 0xFu) << 12);
-      cbase = qc * 16u;
-      ++qc;
-    }
-    if (m16 == 0) {  // every member placed: run complete
-      run_end(true);
-      continue;
-    }
-    const uint32_t i = cbase + (uint32_t)(__ffs(m16) - 1);
-    m16 &= m16 - 1u;
-    const uint32_t l = slen[i];
-    const uint32_t tau = cst[(size_t)i * kp + k];
-    const uint32_t cap = s.M - l;
-    ev += r.V;
-    uint32_t mk;
-    if (r.V <= 8) {
-      mk = argmin_keys<8>(keys, toks, cap);
-    } else {
-      mk = argmin_keys<16>(keys, toks, cap);
-    }
-    if (mk >> 31) {  // no micro-batch can take the sequence: LPT(V) infeasible
-      run_end(false);
-      continue;
-    }
-    const uint32_t nt = (mk >> 5) + tau;
-    if (r.V <= 8) {
-      place_key<8>(keys, toks, mk, tau << 5, l);
-    } else {
-      place_key<16>(keys, toks, mk, tau << 5, l);
-    }
-    r.mx = max(r.mx, nt);
-    if (r.writing) mrow[i] = (uint16_t)(mk & 31u);
-    if (r.mx > r.thr) run_end(false);  // cannot improve (obj, V): abort this V
+  // ---- outputs (parallel over tasks)
+  for (int r = tid; r < nrec; r += kLaneThreads) {
+    if (R.state[r] == 1) continue;
+    const int e = (int)R.eid[r];
+    const int c = c0 + e / mnp, j = e % mnp;
+    const size_t row = (size_t)c * a.n_iter + t;
+    const unsigned long long key = R.key[r];
+    a.v[row * HYD_MAX_PIPES + j] = (uint16_t)(key & 0xFFFFu);
+    a.ptime[row * HYD_MAX_PIPES + j] = key >> 16;
+    atomicMax(reinterpret_cast<unsigned long long*>(a.makespan + (size_t)t * a.n_cand + c), key >> 16);
   }
-  ev = __reduce_add_sync(__activemask(), (uint32_t)min(ev, (uint64_t)0xFFFFFFFFull));
-  if ((tid & 31) == 0 && ev) atomicAdd(a.evals, (unsigned long long)ev);
+  __syncwarp();
+  ev = __reduce_add_sync(HYD_FULL, (uint32_t)min(ev, (uint64_t)0xFFFFFFFFull));
+  if (lane == 0 && ev) atomicAdd(a.evals, (unsigned long long)ev);
 }
+
 // ------------------------------------------------------------------ LPT, one warp per pipeline
 template <typename TT>
 __device__ __forceinline__ TT warp_min(TT x);
@@ -420,8 +687,10 @@ __device__ __forceinline__ bool lpt_warp(const uint16_t* __restrict__ lst, uint1
                                          uint32_t U, uint32_t V, uint32_t M,
                                          const uint32_t* __restrict__ sl,
                                          const uint32_t* __restrict__ cs, int kp, uint32_t k,
-                                         uint64_t thr64, uint64_t& maxbin, uint64_t* scr_t,
-                                         uint32_t* scr_k, uint64_t& evals) {
+                                         const uint32_t* __restrict__ el,
+                                         const uint32_t* __restrict__ ta, uint64_t thr64,
+                                         uint64_t& maxbin, uint64_t* scr_t, uint32_t* scr_k,
+                                         uint64_t& evals) {
   const int lane = threadIdx.x & 31;
   const TT thr = thr64 > (uint64_t)(TT)(~TT(0)) ? (TT)(~TT(0)) : (TT)thr64;
   constexpr int RR = R > 0 ? R : 1;
@@ -442,9 +711,16 @@ __device__ __forceinline__ bool lpt_warp(const uint16_t* __restrict__ lst, uint1
   }
   TT mx = 0;
   for (uint32_t q = 0; q < U; ++q) {
-    const uint32_t idx = lst[q];
-    const uint32_t l = __ldg(sl + idx);
-    const TT tau = (TT)__ldg(cs + (size_t)idx * kp + k);
+    uint32_t l;
+    TT tau;
+    if (el) {  // member (length, cost) staged in shared memory by the list build
+      l = el[q];
+      tau = (TT)ta[q];
+    } else {
+      const uint32_t idx = lst[q];
+      l = __ldg(sl + idx);
+      tau = (TT)__ldg(cs + (size_t)idx * kp + k);
+    }
     const uint32_t cap = M - l;
     TT lt = ~TT(0);
     uint32_t lr = 0xFFFFu;
@@ -473,11 +749,11 @@ __device__ __forceinline__ bool lpt_warp(const uint16_t* __restrict__ lst, uint1
       const uint32_t rs = bstar >> 5;
       if (R > 0) {
 #pragma unroll
-        for (int r = 0; r < RR; ++r)
-          if ((uint32_t)r == rs) {
-            tm[r] += tau;
-            tk[r] += l;
-          }
+        for (int r = 0; r < RR; ++r) {  // branch-free (a switch compiles to a jump table)
+          const bool h = (uint32_t)r == rs;
+          tm[r] += h ? tau : (TT)0;
+          tk[r] += h ? l : 0u;
+        }
       } else {
         scr_t[bstar] += (uint64_t)tau;
         scr_k[bstar] += l;
@@ -496,21 +772,26 @@ template <typename TT>
 __device__ __forceinline__ bool lpt_warp_dispatch(const uint16_t* lst, uint16_t* mbr, uint32_t U,
                                                   uint32_t V, uint32_t M, const uint32_t* sl,
                                                   const uint32_t* cs, int kp, uint32_t k,
+                                                  const uint32_t* el, const uint32_t* ta,
                                                   uint64_t thr, uint64_t& maxbin, uint64_t* st,
                                                   uint32_t* sk, uint64_t& ev) {
-  if (V <= 32) return lpt_warp<1, TT>(lst, mbr, U, V, M, sl, cs, kp, k, thr, maxbin, st, sk, ev);
-  if (V <= 64) return lpt_warp<2, TT>(lst, mbr, U, V, M, sl, cs, kp, k, thr, maxbin, st, sk, ev);
-  if (V <= 128) return lpt_warp<4, TT>(lst, mbr, U, V, M, sl, cs, kp, k, thr, maxbin, st, sk, ev);
-  if (V <= 32 * kBigRMax) return lpt_warp<kBigRMax, TT>(lst, mbr, U, V, M, sl, cs, kp, k, thr, maxbin, st, sk, ev);
-  return lpt_warp<0, TT>(lst, mbr, U, V, M, sl, cs, kp, k, thr, maxbin, st, sk, ev);
+  if (V <= 32) return lpt_warp<1, TT>(lst, mbr, U, V, M, sl, cs, kp, k, el, ta, thr, maxbin, st, sk, ev);
+  if (V <= 64) return lpt_warp<2, TT>(lst, mbr, U, V, M, sl, cs, kp, k, el, ta, thr, maxbin, st, sk, ev);
+  if (V <= 128) return lpt_warp<4, TT>(lst, mbr, U, V, M, sl, cs, kp, k, el, ta, thr, maxbin, st, sk, ev);
+  if (V <= 32 * kBigRMax) return lpt_warp<kBigRMax, TT>(lst, mbr, U, V, M, sl, cs, kp, k, el, ta, thr, maxbin, st, sk, ev);
+  return lpt_warp<0, TT>(lst, mbr, U, V, M, sl, cs, kp, k, el, ta, thr, maxbin, st, sk, ev);
 }
 
-__global__ void __launch_bounds__(256) k_pack_big(PackArgs a) {
+__global__ void __launch_bounds__(256) k_pack_big(PackArgs a, int stage_items) {
   extern __shared__ __align__(16) uint32_t sm[];
   const int B = a.batch, kp = a.k_pad;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw = blockIdx.x * (blockDim.x >> 5) + warp;  // scratch slot
-  uint16_t* lst = reinterpret_cast<uint16_t*>(sm) + (size_t)warp * 2 * B;
+  // per warp: [el B u32][ta B u32] (if stage_items) [lst B u16][mbr B u16]
+  uint32_t* wbase = sm + (size_t)warp * (stage_items ? 3 : 1) * B;
+  uint32_t* el = stage_items ? wbase : nullptr;
+  uint32_t* ta = stage_items ? wbase + B : nullptr;
+  uint16_t* lst = reinterpret_cast<uint16_t*>(stage_items ? wbase + 2 * B : wbase);
   uint16_t* mbr = lst + B;
   uint64_t* scr_t = a.scr_time + (size_t)gw * B;
   uint32_t* scr_k = a.scr_tok + (size_t)gw * B;
@@ -524,7 +805,6 @@ __global__ void __launch_bounds__(256) k_pack_big(PackArgs a) {
     const unsigned long long e = a.queue[task];
     const int c = (int)(e >> 37), t = (int)((e >> 5) & 0xFFFFFFFFull), j = (int)(e & 31);
     const size_t row = (size_t)c * a.n_iter + t;
-    const uint8_t* prow = a.pipe + row * B;
     const uint32_t* sl = a.sorted_len + (size_t)t * B;
     const uint32_t* cs = a.cost + (size_t)t * B * kp;
     const uint32_t k = a.cand[(size_t)c * HYD_MAX_PIPES + j];
@@ -532,15 +812,14 @@ __global__ void __launch_bounds__(256) k_pack_big(PackArgs a) {
     s.M = a.schemes[k].max_len;
     s.P = a.schemes[k].pp;
     s.UL = a.schemes[k].util_len;
-    // member list: 16 pipe bytes per lane per round, warp-wide exclusive scan of counts
+    // member list from the membership bitmap: one word per lane per round, warp scan of counts
+    const uint32_t* mw = a.members + (((size_t)t * a.n_cand + c) * a.mnp + j) * a.nwords;
     uint32_t n = 0;
     uint64_t S = 0, sumT = 0;
-    for (int base = 0; base < B; base += 512) {
-      const int i0 = base + 16 * lane;
-      uint32_t m16 = 0;
-      for (int b = 0; b < 16; ++b)
-        if (i0 + b < B && prow[i0 + b] == (uint8_t)j) m16 |= 1u << b;
-      const uint32_t cnt = __popc(m16);
+    for (int base = 0; base < a.nwords; base += 32) {
+      const int w = base + lane;
+      uint32_t bits = w < a.nwords ? __ldg(mw + w) : 0u;
+      const uint32_t cnt = __popc(bits);
       uint32_t incl = cnt;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -548,13 +827,18 @@ __global__ void __launch_bounds__(256) k_pack_big(PackArgs a) {
         if (lane >= o) incl += y;
       }
       uint32_t pos = n + incl - cnt;
-      while (m16) {
-        const int b = __ffs(m16) - 1;
-        m16 &= m16 - 1;
-        const uint32_t idx = (uint32_t)(i0 + b);
+      while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const uint32_t idx = (uint32_t)(32 * w + b);
+        const uint32_t l = __ldg(sl + idx), tau = __ldg(cs + (size_t)idx * kp + k);
+        if (stage_items) {
+          el[pos] = l;
+          ta[pos] = tau;
+        }
         lst[pos++] = (uint16_t)idx;
-        S += __ldg(sl + idx);
-        sumT += __ldg(cs + (size_t)idx * kp + k);
+        S += l;
+        sumT += tau;
       }
       n += __shfl_sync(HYD_FULL, incl, 31);
     }
@@ -574,12 +858,12 @@ __global__ void __launch_bounds__(256) k_pack_big(PackArgs a) {
       const bool narrow = s.sumT < 0xFFFFFFFFull;
       uint32_t V;
       while ((V = search_next(s)) != 0) {
-        const uint64_t thr = search_thr(s, V);
+        const uint64_t thr = search_thr_approx(s, V);
         uint64_t mx = 0;
-        const bool ok = narrow ? lpt_warp_dispatch<uint32_t>(lst, mbr, s.U, V, s.M, sl, cs, kp, k, thr, mx, scr_t, scr_k, ev)
-                               : lpt_warp_dispatch<uint64_t>(lst, mbr, s.U, V, s.M, sl, cs, kp, k, thr, mx, scr_t, scr_k, ev);
+        const bool ok = narrow ? lpt_warp_dispatch<uint32_t>(lst, mbr, s.U, V, s.M, sl, cs, kp, k, el, ta, thr, mx, scr_t, scr_k, ev)
+                               : lpt_warp_dispatch<uint64_t>(lst, mbr, s.U, V, s.M, sl, cs, kp, k, el, ta, thr, mx, scr_t, scr_k, ev);
         __syncwarp();
-        if (ok) {
+        if (ok && search_improves(s, V, mx)) {
           search_take(s, V, mx);
           for (uint32_t q = lane; q < s.U; q += 32) mrow[lst[q]] = mbr[q];
         }
@@ -607,26 +891,31 @@ static int dp_of(int max_np) {
   return max_np <= 2 ? 2 : max_np <= 4 ? 4 : max_np <= 8 ? 8 : max_np <= 16 ? 16 : 32;
 }
 
-size_t pack_workspace(int n_iter, int batch, int n_cand, int max_np) {
-  const size_t cap = (size_t)n_iter * n_cand * dp_of(max_np);
-  return align256(32) + align256(cap * 8) + align256((size_t)kBigWarps * batch * 8) +
-         align256((size_t)kBigWarps * batch * 4);
+static size_t flag_bytes(int n_iter, int n_cand, int max_np) {
+  return ((size_t)n_iter * n_cand * max_np + 31) / 32 * 4;
 }
 
-template <bool STAGED>
+size_t pack_workspace(int n_iter, int batch, int n_cand, int max_np) {
+  const size_t cap = (size_t)n_iter * n_cand * dp_of(max_np);
+  return align256(256) + align256(cap * 8) + align256((size_t)kBigWarps * batch * 8) +
+         align256((size_t)kBigWarps * batch * 4) + align256(flag_bytes(n_iter, n_cand, max_np));
+}
+
+template <bool STAGED, int VM>
 static cudaError_t launch_lanes(dim3 grid, size_t smem, cudaStream_t s, const PackArgs& a, int tc,
-                                int mnp) {
-  cudaError_t e = cudaFuncSetAttribute(k_pack_lanes<STAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+                                int mnp, int ncap) {
+  cudaError_t e = cudaFuncSetAttribute(k_pack_lanes<STAGED, VM>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_pack_lanes<STAGED><<<grid, kLaneThreads, smem, s>>>(a, tc, mnp);
+  k_pack_lanes<STAGED, VM><<<grid, kLaneThreads, smem, s>>>(a, tc, mnp, ncap);
   return cudaGetLastError();
 }
 
 int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch, int k_pad,
                 const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
                 const uint8_t* cand_np, int n_cand, int max_np, const uint8_t* pipe,
-                const hyd_pipe_stats* stats, uint16_t* mb, uint16_t* v, uint64_t* ptime,
+                const hyd_pipe_stats* stats, const uint32_t* members, uint16_t* mb, uint16_t* v,
+                uint64_t* ptime,
                 uint64_t* makespan, uint32_t* status, void* ws, size_t ws_bytes, cudaStream_t s) {
   (void)ws_bytes;
   if (n_iter == 0 || n_cand == 0) return HYD_OK;
@@ -644,6 +933,9 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
   a.n_cand = n_cand;
   a.pipe = pipe;
   a.stats = stats;
+  a.members = members;
+  a.mnp = max_np;
+  a.nwords = (batch + 31) / 32;
   a.mb = mb;
   a.v = v;
   a.ptime = ptime;
@@ -653,41 +945,58 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
   a.q_count = reinterpret_cast<unsigned long long*>(w);
   a.q_head = a.q_count + 1;
   a.evals = a.q_count + 2;
-  w += align256(32);
+  a.why = a.q_count + 3;
+  w += align256(256);
   a.q_cap = (unsigned long long)n_iter * n_cand * dp;
   a.queue = reinterpret_cast<unsigned long long*>(w);
   w += align256(a.q_cap * 8);
   a.scr_time = reinterpret_cast<uint64_t*>(w);
   w += align256((size_t)kBigWarps * batch * 8);
   a.scr_tok = reinterpret_cast<uint32_t*>(w);
+  w += align256((size_t)kBigWarps * batch * 4);
+  a.flags = reinterpret_cast<uint32_t*>(w);
 
-  cudaError_t e = cudaMemsetAsync(a.q_count, 0, 24, s);
+  cudaError_t e = cudaMemsetAsync(a.q_count, 0, 112, s);
+  if (e != cudaSuccess) return record_cuda_error(e);
+  e = cudaMemsetAsync(a.flags, 0, flag_bytes(n_iter, n_cand, max_np), s);
   if (e != cudaSuccess) return record_cuda_error(e);
   const size_t pairs = (size_t)n_iter * n_cand;
-  k_pack_init<<<(unsigned)((pairs + 255) / 256), 256, 0, s>>>(pipe, n_iter, batch, n_cand, mb, v, ptime,
-                                                              makespan);
+  k_pack_init<<<(unsigned)((pairs + 255) / 256), 256, 0, s>>>(stats, max_np, n_iter, batch, n_cand,
+                                                              mb, v, ptime, makespan);
   note_launch();
   e = cudaGetLastError();
   if (e != cudaSuccess) return record_cuda_error(e);
 
-  // persistent lanes: a CTA = one iteration x tc candidates (~2048 pipeline tasks)
-  const int tc = n_cand < 2048 / max_np ? n_cand : (2048 / max_np > 0 ? 2048 / max_np : 1);
+  // persistent lanes: pass 1 (VMAX 16) CTA = one iteration x tc candidates (~2048 tasks);
+  // pass 2 (VMAX 32, flagged tasks, compacted records) CTA = one whole iteration
   const size_t stage = (size_t)batch * 4 * (1 + (size_t)k_pad);
-  const size_t list = (((size_t)tc * max_np * 2) + 15) & ~(size_t)15;
-  const bool staged = (batch % 4) == 0 && stage + list <= 100 * 1024;
-  dim3 grid((n_cand + tc - 1) / tc, n_iter);
-  e = staged ? launch_lanes<true>(grid, stage + list, s, a, tc, max_np)
-             : launch_lanes<false>(grid, list, s, a, tc, max_np);
+  const int ncap = 2048;
+  const size_t recs = (size_t)ncap * 36;  // bytes of task records per CTA
+  const bool staged = (batch % 4) == 0 && stage + recs <= 110 * 1024;
+  const size_t smem = recs + (staged ? stage : 0);
+  const int tc1 = max(1, min(n_cand, ncap / max_np));
+  dim3 grid1((n_cand + tc1 - 1) / tc1, n_iter);
+  e = staged ? launch_lanes<true, 16>(grid1, smem, s, a, tc1, max_np, ncap)
+             : launch_lanes<false, 16>(grid1, smem, s, a, tc1, max_np, ncap);
+  note_launch();
+  if (e != cudaSuccess) return record_cuda_error(e);
+  const int tc2 = max(1, min(n_cand, 65535 / max_np));
+  dim3 grid2((n_cand + tc2 - 1) / tc2, n_iter);
+  e = staged ? launch_lanes<true, 32>(grid2, smem, s, a, tc2, max_np, ncap)
+             : launch_lanes<false, 32>(grid2, smem, s, a, tc2, max_np, ncap);
   note_launch();
   if (e != cudaSuccess) return record_cuda_error(e);
 
-  // warp per pipeline for the queue (V > 16, wide sums, ragged batches)
+  // warp per pipeline for the queue (V > 16, wide sums, ragged batches); members' (l, tau)
+  // staged in smem next to the list when they fit
+  const int stage_items = batch <= 1024 ? 1 : 0;
+  const size_t per_warp = (size_t)batch * 4 * (stage_items ? 3 : 1);
   int wpb = 8;
-  while (wpb > 1 && (size_t)wpb * batch * 4 > 96 * 1024) wpb >>= 1;
-  const size_t bsm = (size_t)wpb * batch * 4;
+  while (wpb > 1 && (size_t)wpb * per_warp > 96 * 1024) wpb >>= 1;
+  const size_t bsm = (size_t)wpb * per_warp;
   e = cudaFuncSetAttribute(k_pack_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
   if (e != cudaSuccess) return record_cuda_error(e);
-  k_pack_big<<<kBigWarps / wpb, wpb * 32, bsm, s>>>(a);
+  k_pack_big<<<kBigWarps / wpb, wpb * 32, bsm, s>>>(a, stage_items);
   note_launch();
   e = cudaGetLastError();
   return e == cudaSuccess ? HYD_OK : record_cuda_error(e);

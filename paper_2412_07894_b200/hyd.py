@@ -57,9 +57,9 @@ def lib():
     I, P, Z, U64 = C.c_int, C.c_void_p, C.c_size_t, C.c_uint64
     sig = {
         "hyd_cost_table": ([P, I, I, P, I, I, P, P, P, P, P], I),
-        "hyd_dispatch": ([P, P, I, I, I, P, I, P, P, I, I, P, P, P, P, P], I),
+        "hyd_dispatch": ([P, P, I, I, I, P, I, P, P, I, I, P, P, P, P, P, P], I),
         "hyd_pack_workspace": ([I, I, I, I], Z),
-        "hyd_pack": ([P, P, I, I, I, P, I, P, P, I, I, P, P, P, P, P, P, P, P, Z, P], I),
+        "hyd_pack": ([P, P, I, I, I, P, I, P, P, I, I, P, P, P, P, P, P, P, P, P, Z, P], I),
         "hyd_select_best": ([P, I, I, I, P, P, P], I),
         "hyd_gather_winners": ([P, P, P, P, P, P, I, I, I, I, P, P, P, P, P], I),
         "hyd_assign_workspace": ([I, I, I, I, I, I], Z),
@@ -131,10 +131,10 @@ def cost_table(len_, n_iter, batch, schemes, n_schemes, k_pad, sorted_len, perm,
 
 
 def dispatch(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, pipe, lb,
-             stats, status, stream=None):
+             stats, members, status, stream=None):
     _check(lib().hyd_dispatch(_dev(sorted_len), _dev(cost), n_iter, batch, k_pad, _dev(schemes), n_schemes,
                               _dev(cand), _dev(cand_np), n_cand, max_np, _dev(pipe), _dev(lb), _dev(stats),
-                              _dev(status), _stream(stream)), "hyd_dispatch")
+                              _dev(members), _dev(status), _stream(stream)), "hyd_dispatch")
 
 
 def pack_workspace(n_iter, batch, n_cand, max_np) -> int:
@@ -142,9 +142,10 @@ def pack_workspace(n_iter, batch, n_cand, max_np) -> int:
 
 
 def pack(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, pipe, stats,
-         mb, v, ptime, makespan, status, ws, stream=None):
+         members, mb, v, ptime, makespan, status, ws, stream=None):
     _check(lib().hyd_pack(_dev(sorted_len), _dev(cost), n_iter, batch, k_pad, _dev(schemes), n_schemes, _dev(cand),
-                          _dev(cand_np), n_cand, max_np, _dev(pipe), _dev(stats), _dev(mb), _dev(v), _dev(ptime),
+                          _dev(cand_np), n_cand, max_np, _dev(pipe), _dev(stats), _dev(members), _dev(mb), _dev(v),
+                          _dev(ptime),
                           _dev(makespan), _dev(status), _dev(ws), ws.numel() * ws.element_size(),
                           _stream(stream)), "hyd_pack")
 
