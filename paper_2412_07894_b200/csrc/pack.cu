@@ -255,8 +255,10 @@ struct TaskRecs {
   uint16_t* vhi;
   uint16_t* va;
   uint16_t* perm;   // phase-1 order of slots (longest-processing-time first)
+  uint16_t* ncand;  // phase-2 candidate count
   uint8_t* k;
-  uint8_t* state;   // 0 active, 1 handed to another pass, 2 no phase-2 candidates
+  uint8_t* state;   // 0 active, 1 handed to another pass
+  uint8_t* cbucket; // phase-2 bucket
 };
 
 // one bulk L2 prefetch of a contiguous block (TMA engine), clipped to 16-byte granules
@@ -355,7 +357,7 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
                       total_rows * sizeof(hyd_pipe_stats));
   }
   // dynamic smem: [stage B*(1+kp) u32] [key u64] [sum_t, tau_max, eid, list2 u32]
-  //               [u, vlo, vhi, va, perm u16] [k, state u8]   (ncap slots each)
+  //               [u, vlo, vhi, va, perm, ncand u16] [k, state, cbucket u8]   (ncap slots each)
   uint32_t* recbase = sm + (STAGED ? (size_t)B * (1 + kp) : 0);
   TaskRecs R;
   R.key = reinterpret_cast<unsigned long long*>(recbase);
@@ -368,8 +370,10 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
   R.vhi = R.vlo + ncap;
   R.va = R.vhi + ncap;
   R.perm = R.va + ncap;
-  R.k = reinterpret_cast<uint8_t*>(R.perm + ncap);
+  R.ncand = R.perm + ncap;
+  R.k = reinterpret_cast<uint8_t*>(R.ncand + ncap);
   R.state = R.k + ncap;
+  R.cbucket = R.state + ncap;
   if (tid == 0) {
     s_next = 0;
     s_nrec = 0;
@@ -465,7 +469,16 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
   __syncthreads();
   {
     // bucket -> position (list2 is free until phase 1.5: used as scratch for the order)
-    for (int r = tid; r < nrec; r += kLaneThreads) R.list2[atomicAdd(&s_hist[R.perm[r]], 1)] = (uint32_t)r;
+    for (int r0 = 0; r0 < nrec; r0 += kLaneThreads) {  // warp-aggregated bucket cursors
+      const int r = r0 + tid;
+      const int bk = r < nrec ? (int)R.perm[r] : -1 - lane;  // distinct dummies for idle lanes
+      const unsigned peers = __match_any_sync(HYD_FULL, bk);
+      const int leader = __ffs(peers) - 1;
+      int pos = 0;
+      if (lane == leader && bk >= 0) pos = atomicAdd(&s_hist[bk], __popc(peers));
+      pos = __shfl_sync(HYD_FULL, pos, leader) + __popc(peers & ((1u << lane) - 1u));
+      if (bk >= 0) R.list2[pos] = (uint32_t)r;
+    }
     __syncthreads();
     for (int q = tid; q < nrec; q += kLaneThreads) R.perm[q] = (uint16_t)R.list2[q];
   }
@@ -495,30 +508,34 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
     u.write = write;
     unit_start<VM>(u, V, thr);
   };
-  // Lanes run epochs of kLaneEpoch sequences of their current unit; between epochs all lanes
-  // that finished a unit record its result and pull the next one together (converged), so the
-  // per-unit work never runs one lane at a time.  pull(q) returns false for units to skip.
+  // Warp-batch scheduling: a warp takes 32 consecutive units of a list sorted by (class, U), so
+  // its lanes run the same code path over nearly the same number of sequences and finish
+  // together; it takes the next batch when all 32 are done.  Inside a batch, lanes step in
+  // epochs of kLaneEpoch sequences.  pull(q) prepares unit q (false: nothing to run).
   auto run_units = [&](int n_units, auto&& pull, auto&& finish) {
     if (tid == 0) s_next = 0;
     __syncthreads();
-    bool have = false, done = false;
     while (true) {
-      while (!have && !done) {
-        const int q = atomicAdd(&s_next, 1);
-        if (q >= n_units) done = true;
-        else have = pull(q);
-      }
-      if (__all_sync(HYD_FULL, done && !have)) break;
-      if (have) {
-        int st = 0;
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&s_next, 32);
+      base = __shfl_sync(HYD_FULL, base, 0);
+      if (base >= n_units) break;
+      const int q = base + lane;
+      bool have = q < n_units && pull(q);
+      // one code path per batch: the widest unit decides (narrower units run with sentinel bins)
+      const bool narrow = __all_sync(HYD_FULL, !have || u.V <= 8u);
+      while (__any_sync(HYD_FULL, have)) {
+        if (have) {
+          int st = 0;
 #pragma unroll 1
-        for (int e = 0; e < kLaneEpoch && st == 0; ++e) {
-          if (VM == 16 && u.V <= 8) st = unit_step<8, VM>(u, nwords, slen, cst, kp, ev);
-          else st = unit_step<VM, VM>(u, nwords, slen, cst, kp, ev);
-        }
-        if (st) {
-          finish(st);
-          have = false;
+          for (int e = 0; e < kLaneEpoch && st == 0; ++e) {
+            if (VM == 16 && narrow) st = unit_step<8, VM>(u, nwords, slen, cst, kp, ev);
+            else st = unit_step<VM, VM>(u, nwords, slen, cst, kp, ev);
+          }
+          if (st) {
+            finish(st);
+            have = false;
+          }
         }
       }
     }
@@ -526,6 +543,24 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
   };
   auto obj_key = [&](const LaneUnit<VM>& w) {
     return (((uint64_t)w.mx * (uint64_t)(s_pp[w.k] - 1 + w.V)) << 16) | w.V;
+  };
+  // order-preserving compaction of perm[0..nrec) into list2 by one warp (ballot prefix)
+  auto compact = [&](auto&& keep) -> int {
+    __syncthreads();
+    if (tid < 32) {
+      int n = 0;
+      for (int q0 = 0; q0 < nrec; q0 += 32) {
+        const int q = q0 + lane;
+        const int r = q < nrec ? (int)R.perm[q] : 0;
+        const bool k = q < nrec && keep(r);
+        const unsigned m = __ballot_sync(HYD_FULL, k);
+        if (k) R.list2[n + __popc(m & ((1u << lane) - 1u))] = (uint32_t)r;
+        n += __popc(m);
+      }
+      if (lane == 0) s_n2a = n;
+    }
+    __syncthreads();
+    return s_n2a;
   };
 
   // ---- phase 1: the V_a run of every task (writes mb)
@@ -540,24 +575,28 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
 
   // ---- phase 1b: where LPT(V_a) is infeasible (capacity), V_a + 1 is tried; it then takes
   //      V_a's place as the reference run of the exact tests below
-  run_units(
-      nrec,
-      [&](int q) {
-        const int r = R.perm[q];
-        if (R.key[r] != kBottom) return false;
-        const uint32_t V = (uint32_t)R.va[r] + 1u;
-        if (V > (uint32_t)R.vhi[r] || V > (uint32_t)VM) return false;
-        R.va[r] = (uint16_t)V;
-        load_unit(r, V, 0xFFFFFFFFu, true);
-        return true;
-      },
-      [&](int st) {
-        if (st == 1) R.key[u.e] = obj_key(u);
-      });
+  {
+    const int n1b = compact([&](int r) {
+      const uint32_t V = (uint32_t)R.va[r] + 1u;
+      return R.key[r] == kBottom && V <= (uint32_t)R.vhi[r] && V <= (uint32_t)VM;
+    });
+    run_units(
+        n1b,
+        [&](int q) {
+          const int r = (int)R.list2[q];
+          const uint32_t V = (uint32_t)R.va[r] + 1u;
+          R.va[r] = (uint16_t)V;
+          load_unit(r, V, 0xFFFFFFFFu, true);
+          return true;
+        },
+        [&](int st) {
+          if (st == 1) R.key[u.e] = obj_key(u);
+        });
+  }
 
   // ---- phase 1.5 (thread per task): every V of App. D's range that survives the exact tests
-  //      against the reference run, reserved contiguously per task in list2 (class 16 from the
-  //      front half, class 8 from the back half); a task that does not fit is handed off
+  //      against the reference run, bucket-sorted by (class, U) into list2; tasks that do not
+  //      fit are handed off
   auto walk = [&](int r, Search& s) {
     s.P = s_pp[R.k[r]];
     s.U = R.u[r];
@@ -569,10 +608,24 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
     s.cursor = s.vlo;
     s.phase = 1;
     s.have = false;
-    search_take(s, s.va, (R.key[r] >> 16) / (uint64_t)(s.P - 1 + s.va));  // reference, cursor jump
+    // reference run: best = its objective (search_take's bookkeeping without the division)
+    s.best = R.key[r] >> 16;
+    s.vbest = s.va;
+    s.have = true;
+    if (s.P > 1) {
+      if (s.best <= s.sumT) {
+        s.cursor = s.vhi + 1;
+      } else {
+        const float est = (float)s.sumT * (float)(s.P - 1) / (float)(s.best - s.sumT);
+        const float lo = est - 2.0f;
+        if (lo > (float)s.cursor) s.cursor = lo >= (float)s.vhi ? s.vhi + 1 : (uint32_t)lo;
+      }
+    }
   };
-  const int half = ncap / 2;
+  for (int b = tid; b < NB; b += kLaneThreads) s_hist[b] = 0;
+  __syncthreads();
   for (int r = tid; r < nrec; r += kLaneThreads) {
+    R.ncand[r] = 0;
     if (R.key[r] == kBottom) {  // the sequential search (with extension) runs elsewhere
       atomicAdd(a.why + (VM == 16 ? 2 : 5), 1ull);
       const int e = (int)R.eid[r];
@@ -582,11 +635,12 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
     }
     Search s;
     walk(r, s);
-    int cnt = 0;
+    int n_lo = 0, n_hi = 0;  // candidates with V <= 8 / V > 8 (VM = 32: all counted high)
     uint32_t vmax = 0, V;
     while ((V = search_next(s)) != 0) {
       vmax = max(vmax, V);
-      ++cnt;
+      if (VM == 16 && V <= 8) ++n_lo;
+      else ++n_hi;
     }
     if (vmax > (uint32_t)VM) {
       atomicAdd(a.why + (VM == 16 ? 3 : 6), 1ull);
@@ -594,37 +648,64 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
       R.state[r] = 1;
       continue;
     }
-    if (cnt == 0) {
-      R.state[r] = 2;
-      continue;
+    if (n_lo + n_hi == 0) continue;
+    const int ub = min(31, (int)(R.u[r] >> 3));
+    R.ncand[r] = (uint16_t)(n_lo | (n_hi << 8));
+    R.cbucket[r] = (uint8_t)ub;
+    if (n_lo) atomicAdd(&s_hist[ub], n_lo);
+    if (n_hi) atomicAdd(&s_hist[32 + ub], n_hi);
+  }
+  __syncthreads();
+  if (tid == 0) {  // exclusive scan, descending buckets
+    int run = 0;
+    for (int b = NB - 1; b >= 0; --b) {
+      const int h = s_hist[b];
+      s_hist[b] = run;
+      run += h;
     }
-    const bool small = VM == 16 && vmax <= 8;
-    const int base = atomicAdd(small ? &s_n2b : &s_n2a, cnt);
-    if (base + cnt > half) {  // does not fit: void the reserved slots inside the half
-      uint32_t* dst = R.list2 + (small ? half : 0);
-      for (int q = base; q < min(base + cnt, half); ++q) dst[q] = 0xFFFFFFFFu;
+    s_n2b = min(run, ncap);
+  }
+  __syncthreads();
+  for (int r = tid; r < nrec; r += kLaneThreads) {
+    const int packed = R.ncand[r];
+    if (packed == 0) continue;
+    const int n_lo = packed & 0xFF, n_hi = packed >> 8;
+    const int ub = R.cbucket[r];
+    const int p_lo = n_lo ? atomicAdd(&s_hist[ub], n_lo) : 0;
+    const int p_hi = n_hi ? atomicAdd(&s_hist[32 + ub], n_hi) : 0;
+    if ((n_lo && p_lo + n_lo > ncap) || (n_hi && p_hi + n_hi > ncap)) {
+      // does not fit: void its slots below ncap, hand it off
+      if (n_lo) for (int q = p_lo; q < min(p_lo + n_lo, ncap); ++q) R.list2[q] = 0xFFFFFFFFu;
+      if (n_hi) for (int q = p_hi; q < min(p_hi + n_hi, ncap); ++q) R.list2[q] = 0xFFFFFFFFu;
       atomicAdd(a.why + 7, 1ull);
       hand_off_e((int)R.eid[r]);
       R.state[r] = 1;
       continue;
     }
+    Search s;
     walk(r, s);
-    int n = 0;
-    uint32_t* dst = R.list2 + (small ? half : 0) + base;
-    while ((V = search_next(s)) != 0 && n < cnt) dst[n++] = ((uint32_t)r << 16) | V;
+    uint32_t V;
+    int i_lo = 0, i_hi = 0;
+    while ((V = search_next(s)) != 0) {
+      const uint32_t w = ((uint32_t)r << 16) | V;
+      if (VM == 16 && V <= 8) {
+        if (i_lo < n_lo) R.list2[p_lo + i_lo++] = w;
+      } else {
+        if (i_hi < n_hi) R.list2[p_hi + i_hi++] = w;
+      }
+    }
   }
   __syncthreads();
-  const int n2a = min(s_n2a, half), n2b = min(s_n2b, half);
 
   // ---- phase 2: the surviving V, each an independent run against the reference; argmin by
   //      atomicMin on (obj << 16 | V)
   run_units(
-      n2a + n2b,
+      s_n2b,
       [&](int q) {
-        const uint32_t w = R.list2[q < n2a ? q : half + (q - n2a)];
+        const uint32_t w = R.list2[q];
         if (w == 0xFFFFFFFFu) return false;
         const int r = (int)(w >> 16);
-        if (r >= nrec || R.state[r] == 1) return false;
+        if (R.state[r] == 1) return false;
         const uint32_t V = w & 0xFFFFu;
         Search s;
         s.P = s_pp[R.k[r]];
@@ -639,17 +720,19 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
       });
 
   // ---- phase 3: tasks whose winner is not the reference run write their mb with one more run
-  run_units(
-      nrec,
-      [&](int q) {
-        const int r = R.perm[q];
-        if (R.state[r] == 1) return false;
-        const uint32_t V = (uint32_t)(R.key[r] & 0xFFFFu);
-        if (V == R.va[r]) return false;
-        load_unit(r, V, 0xFFFFFFFFu, true);
-        return true;
-      },
-      [&](int) {});
+  {
+    const int n3 = compact([&](int r) {
+      return R.state[r] != 1 && (uint32_t)(R.key[r] & 0xFFFFu) != (uint32_t)R.va[r];
+    });
+    run_units(
+        n3,
+        [&](int q) {
+          const int r = (int)R.list2[q];
+          load_unit(r, (uint32_t)(R.key[r] & 0xFFFFu), 0xFFFFFFFFu, true);
+          return true;
+        },
+        [&](int) {});
+  }
 
   // ---- outputs (parallel over tasks)
   for (int r = tid; r < nrec; r += kLaneThreads) {
@@ -969,10 +1052,13 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
 
   // persistent lanes: pass 1 (VMAX 16) CTA = one iteration x tc candidates (~2048 tasks);
   // pass 2 (VMAX 32, flagged tasks, compacted records) CTA = one whole iteration
+  // two CTAs per SM: ~110 KB of dynamic smem each for the staged iteration + task records
   const size_t stage = (size_t)batch * 4 * (1 + (size_t)k_pad);
-  const int ncap = 2048;
-  const size_t recs = (size_t)ncap * 36;  // bytes of task records per CTA
-  const bool staged = (batch % 4) == 0 && stage + recs <= 110 * 1024;
+  const size_t budget = 110 * 1024;
+  const bool staged = (batch % 4) == 0 && stage + 512 * 39 <= budget;
+  int ncap = (int)(((staged ? budget - stage : budget) / 39) & ~(size_t)31);
+  ncap = ncap > 2048 ? 2048 : ncap;
+  const size_t recs = (size_t)ncap * 39;  // bytes of task records per CTA
   const size_t smem = recs + (staged ? stage : 0);
   const int tc1 = max(1, min(n_cand, ncap / max_np));
   dim3 grid1((n_cand + tc1 - 1) / tc1, n_iter);
