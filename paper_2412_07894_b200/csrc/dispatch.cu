@@ -11,8 +11,9 @@
 // E_j = T(l_max,P_j)(PP_j-1) (Eq. 2), so the candidate load of every feasible j is
 //   new_j = base_j + tau * mult_j      (= C_j + tau + e_j of SURVEY §8(c) step 4)
 // one IMAD; j* = argmin (new_j, j) over MaxLen_j >= l_i (J_i); base_j* = new_j*.
-// The running per-pipeline statistics U_j, S_j, tau_max,j (for the packing stage) live in
-// shared memory columns indexed by j* (one LDS/STS set per sequence, not per pipeline).
+// Per-pipeline statistics for the packing stage: S_j in a shared-memory column indexed by j*
+// (one LDS/STS per sequence); U_j and tau_max,j from the membership bitmap words, which are
+// flushed every 32 sequences.
 // The sums run in u32 when a per-CTA bound proves every load < 2^32, else in u64.
 // Outputs: pipe[c][t][i] (4 decisions per u32 store), lb[c][t] = max_j base_j, stats.
 #include "hyd_internal.cuh"
@@ -21,61 +22,82 @@ namespace hyd {
 
 constexpr int kDispatchThreads = 128;
 
+// One sequence step: candidate loads, argmin (new_j, j), branch-free update of pipeline j*.
+// FEAS: test MaxLen_j >= l (only needed while l exceeds the smallest MaxLen of the candidate;
+// lengths are sorted descending, so the tail of the batch skips the test).
+template <int DP, typename TT, bool FEAS>
+__device__ __forceinline__ uint32_t dispatch_step(uint32_t l, const uint32_t* __restrict__ crow,
+                                                  bool staged, const uint32_t (&ml)[DP],
+                                                  const uint32_t (&kk)[DP], TT (&base)[DP],
+                                                  uint32_t (&mult)[DP], uint32_t (&bits)[DP],
+                                                  uint32_t bit) {
+  TT best = (TT)~(TT)0;
+  uint32_t bj = 0u;
+#pragma unroll
+  for (int j = 0; j < DP; ++j) {
+    const uint32_t tau = staged ? crow[kk[j]] : __ldg(crow + kk[j]);
+    const TT nw = base[j] + (TT)tau * (TT)mult[j];
+    if ((!FEAS || l <= ml[j]) && nw < best) {
+      best = nw;
+      bj = (uint32_t)j;
+    }
+  }
+  // branch-free update of pipeline bj (a switch here compiles to a divergent jump table)
+#pragma unroll
+  for (int j = 0; j < DP; ++j) {
+    const uint32_t hit = 0u - (uint32_t)((uint32_t)j == bj);
+    const TT hitw = (TT)0 - (TT)((uint32_t)j == bj);
+    base[j] = (base[j] & ~hitw) | (best & hitw);
+    mult[j] = (mult[j] & ~hit) | (1u & hit);
+    bits[j] |= bit & hit;
+  }
+  return bj;
+}
+
 template <int DP, typename TT>
 __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
                                              const uint32_t* __restrict__ cs, bool staged, int B,
                                              int k_pad, const uint32_t (&ml)[DP],
                                              const uint32_t (&pp)[DP], const uint32_t (&kk)[DP],
-                                             uint8_t* __restrict__ prow, uint32_t* s_cnt,
-                                             uint32_t* s_tmax, unsigned long long* s_sum,
+                                             uint8_t* __restrict__ prow, unsigned long long* s_sum,
                                              uint32_t* __restrict__ mbits, int np, int nwords,
-                                             uint64_t& lb_out, TT (&base)[DP]) {
+                                             uint64_t& lb_out, TT (&base)[DP], uint32_t (&cnt)[DP],
+                                             uint32_t (&tmax)[DP]) {
   uint32_t mult[DP], bits[DP];
+  uint32_t ml_min = 0xFFFFFFFFu;
 #pragma unroll
-  for (int j = 0; j < DP; ++j) {
-    base[j] = 0;
-    mult[j] = pp[j];
+  for (int j = 0; j < DP; ++j) {  // unused slots: base = max, mult = 0 -> never strictly best
+    base[j] = j < np ? (TT)0 : (TT)~(TT)0;
+    mult[j] = j < np ? pp[j] : 0u;
     bits[j] = 0u;
+    cnt[j] = 0u;
+    tmax[j] = 0u;
+    if (j < np) ml_min = min(ml_min, ml[j]);
   }
   const bool words = (B & 3) == 0;
   uint32_t word = 0u;
   for (int i = 0; i < B; ++i) {
     const uint32_t l = sl[i];
     const uint32_t* crow = cs + (size_t)i * k_pad;
-    TT best = (TT)~(TT)0;
-    uint32_t bj = 0u, btau = 0u;
-#pragma unroll
-    for (int j = 0; j < DP; ++j) {
-      const uint32_t tau = staged ? crow[kk[j]] : __ldg(crow + kk[j]);
-      const TT nw = base[j] + (TT)tau * (TT)mult[j];
-      if (l <= ml[j] && nw < best) {
-        best = nw;
-        bj = (uint32_t)j;
-        btau = tau;
-      }
-    }
-    // branch-free update of pipeline bj (a switch here compiles to a divergent jump table)
     const uint32_t bit = 1u << (i & 31);
-#pragma unroll
-    for (int j = 0; j < DP; ++j) {
-      const uint32_t hit = 0u - (uint32_t)((uint32_t)j == bj);
-      const TT hitw = (TT)0 - (TT)((uint32_t)j == bj);
-      base[j] = (base[j] & ~hitw) | (best & hitw);
-      mult[j] = (mult[j] & ~hit) | (1u & hit);
-      bits[j] |= bit & hit;
-    }
-    if ((i & 31) == 31 || i == B - 1) {  // flush one membership word per pipeline
+    const uint32_t bj = l > ml_min ? dispatch_step<DP, TT, true>(l, crow, staged, ml, kk, base, mult, bits, bit)
+                                   : dispatch_step<DP, TT, false>(l, crow, staged, ml, kk, base, mult, bits, bit);
+    s_sum[bj * kDispatchThreads] += l;  // S_j column of this thread
+    if ((i & 31) == 31 || i == B - 1) {  // flush one membership word per pipeline; U_j, tau_max_j
+      const int w0 = i & ~31;
 #pragma unroll
       for (int j = 0; j < DP; ++j) {
-        if (j < np) mbits[(size_t)j * nwords + (i >> 5)] = bits[j];
+        if (j < np) {
+          mbits[(size_t)j * nwords + (i >> 5)] = bits[j];
+          if (cnt[j] == 0u && bits[j] != 0u) {  // first (= longest) member of pipeline j
+            const uint32_t* frow = cs + (size_t)(w0 + __ffs(bits[j]) - 1) * k_pad;
+            tmax[j] = staged ? frow[kk[j]] : __ldg(frow + kk[j]);
+          }
+          cnt[j] += __popc(bits[j]);
+        }
         bits[j] = 0u;
       }
     }
-    // statistics column of pipeline bj (this thread's column)
-    const uint32_t n = s_cnt[bj * kDispatchThreads];
-    if (n == 0u) s_tmax[bj * kDispatchThreads] = btau;
-    s_cnt[bj * kDispatchThreads] = n + 1u;
-    s_sum[bj * kDispatchThreads] += l;
     if (words) {
       word |= bj << (8 * (i & 3));
       if ((i & 3) == 3) {
@@ -88,7 +110,8 @@ __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
   }
   uint64_t m = 0ull;
 #pragma unroll
-  for (int j = 0; j < DP; ++j) m = max(m, (uint64_t)base[j]);
+  for (int j = 0; j < DP; ++j)
+    if (j < np) m = max(m, (uint64_t)base[j]);
   lb_out = m;
 }
 
@@ -101,11 +124,9 @@ __global__ void __launch_bounds__(kDispatchThreads)
                uint64_t* __restrict__ lb, hyd_pipe_stats* __restrict__ stats,
                uint32_t* __restrict__ members, uint32_t* __restrict__ status) {
   extern __shared__ __align__(16) uint32_t sm[];
-  // dynamic smem: [stage: tt*B*(1+k_pad) u32 if STAGED] [s_sum u64][s_cnt u32][s_tmax u32]
+  // dynamic smem: [stage: tt*B*(1+k_pad) u32 if STAGED] [s_sum u64 columns]
   const size_t stage_words = STAGED ? (size_t)tt * batch * (1 + k_pad) : 0;
   unsigned long long* s_sum = reinterpret_cast<unsigned long long*>(sm + ((stage_words + 3) & ~(size_t)3));
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_sum + DP * kDispatchThreads);
-  uint32_t* s_tmax = s_cnt + DP * kDispatchThreads;
   __shared__ unsigned long long s_bound[kDispatchThreads / 32];
   __shared__ uint32_t s_ppmax;
   const int B = batch;
@@ -129,10 +150,7 @@ __global__ void __launch_bounds__(kDispatchThreads)
     s_ppmax = m;
   }
 #pragma unroll
-  for (int j = 0; j < DP; ++j) {
-    s_cnt[j * kDispatchThreads + tid] = 0u;
-    s_sum[j * kDispatchThreads + tid] = 0ull;
-  }
+  for (int j = 0; j < DP; ++j) s_sum[j * kDispatchThreads + tid] = 0ull;
   __syncthreads();
   // u32 bound over the CTA's iterations: sum_i max_k tau_ik + max tau * (PPmax - 1) < 2^32-1
   //  =>  every base_j and new_j of every thread fits u32 (strictly below the u32 sentinel).
@@ -201,33 +219,30 @@ __global__ void __launch_bounds__(kDispatchThreads)
   }
   const int nwords = (B + 31) >> 5;
   uint32_t* mbits = members + srow * max_np * nwords;
-  uint32_t* cnt = s_cnt + tid;
-  uint32_t* tmx = s_tmax + tid;
   unsigned long long* ssum = s_sum + tid;
   uint64_t lbv = 0ull;
   uint64_t base64[DP];
+  uint32_t cnt[DP], tmx[DP];
   if (narrow) {
     uint32_t base[DP];
-    dispatch_run<DP, uint32_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, cnt, tmx, ssum, mbits, np,
-                               nwords, lbv, base);
+    dispatch_run<DP, uint32_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, ssum, mbits, np, nwords,
+                               lbv, base, cnt, tmx);
 #pragma unroll
     for (int j = 0; j < DP; ++j) base64[j] = base[j];
   } else {
-    dispatch_run<DP, uint64_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, cnt, tmx, ssum, mbits, np,
-                               nwords, lbv, base64);
+    dispatch_run<DP, uint64_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, ssum, mbits, np, nwords,
+                               lbv, base64, cnt, tmx);
   }
   lb[row] = lbv;
   hyd_pipe_stats* st = stats + srow * max_np;
 #pragma unroll
   for (int j = 0; j < DP; ++j) {
     if (j < np) {
-      const uint32_t n = cnt[j * kDispatchThreads];
-      const uint32_t tm = n ? tmx[j * kDispatchThreads] : 0u;
       hyd_pipe_stats e;
-      e.u = n;
-      e.tau_max = tm;
+      e.u = cnt[j];
+      e.tau_max = tmx[j];
       e.s = ssum[j * kDispatchThreads];
-      e.sum_t = base64[j] - (uint64_t)tm * (pp[j] - 1u);  // base_j = C_j + E_j
+      e.sum_t = base64[j] - (uint64_t)tmx[j] * (pp[j] - 1u);  // base_j = C_j + E_j
       st[j] = e;
     }
   }
@@ -240,7 +255,7 @@ static cudaError_t launch_dp(bool staged, dim3 grid, size_t smem_stage, cudaStre
                              const uint8_t* cand, const uint8_t* cand_np, int n_cand, int max_np,
                              int ct, int tt, uint8_t* pipe, uint64_t* lb, hyd_pipe_stats* stats,
                              uint32_t* members, uint32_t* status) {
-  const size_t cols = (size_t)DP * kDispatchThreads * 16;
+  const size_t cols = (size_t)DP * kDispatchThreads * 8;
   cudaError_t e;
   if (staged) {
     const size_t smem = ((smem_stage + 15) & ~(size_t)15) + cols;
@@ -268,7 +283,7 @@ int launch_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter
   const int tt = kDispatchThreads / ct;
   const size_t smem = (size_t)tt * batch * 4 * (1 + (size_t)k_pad);
   const int dp = max_np <= 2 ? 2 : max_np <= 4 ? 4 : max_np <= 8 ? 8 : max_np <= 16 ? 16 : 32;
-  const size_t static_smem = (size_t)dp * kDispatchThreads * 16 + 64;
+  const size_t static_smem = (size_t)dp * kDispatchThreads * 8 + 64;
   // stage when the rows fit comfortably (leaves room for several CTAs per SM)
   const bool staged = smem + static_smem <= 96 * 1024 && (batch % 4) == 0;
   dim3 grid((n_cand + ct - 1) / ct, (n_iter + tt - 1) / tt);

@@ -39,7 +39,7 @@ namespace hyd {
 constexpr int kLaneThreads = 256;
 constexpr int kLaneEpoch = 8;     // sequences per lane between bookkeeping phases
 constexpr int kBigRMax = 8;       // k_pack_big: register bins per lane (V <= 256)
-constexpr int kBigWarps = 2048;   // persistent warps of k_pack_big (scratch slots)
+constexpr int kBigWarps = 3584;   // persistent warps of k_pack_big (scratch slots): 148 SMs x 24
 
 struct PackArgs {
   const uint32_t* sorted_len;
@@ -765,13 +765,82 @@ __device__ __forceinline__ uint64_t warp_min<uint64_t>(uint64_t x) {
 }
 
 // bins b = lane + 32 r; R register slots per lane (R*32 >= V), or scratch when R == 0
+// Warp-cooperative member stream of one pipeline: the membership bitmap is decoded 32
+// members at a time (word popcounts, warp prefix scan, per-lane rank search), each lane
+// gathering its member's (l, tau) so the sequential LPT loop reads them by shuffle.
+struct MemberStream {
+  const uint32_t* mw;
+  uint32_t nwords, wpos;  // next word window start
+  uint32_t wbits;         // this lane's word of the current window (already consumed bits cleared)
+  uint32_t incl;          // inclusive prefix of remaining popcounts in the window
+  uint32_t left;          // members left in the window
+};
+
+__device__ __forceinline__ void ms_open(MemberStream& m, const uint32_t* mw, uint32_t nwords) {
+  m.mw = mw;
+  m.nwords = nwords;
+  m.wpos = 0;
+  m.left = 0;
+  m.wbits = 0;
+  m.incl = 0;
+}
+
+// Fill (idx, l, tau) for up to 32 next members; returns how many (0 at the end).
+__device__ __forceinline__ uint32_t ms_next32(MemberStream& m, const uint32_t* __restrict__ sl,
+                                              const uint32_t* __restrict__ cs, int kp, uint32_t k,
+                                              uint32_t& idx, uint32_t& l, uint32_t& tau) {
+  const int lane = threadIdx.x & 31;
+  while (m.left == 0) {
+    if (m.wpos >= m.nwords) return 0;
+    const uint32_t w = m.wpos + lane;
+    m.wbits = w < m.nwords ? __ldg(m.mw + w) : 0u;
+    uint32_t c = __popc(m.wbits);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(HYD_FULL, c, o);
+      if (lane >= o) c += y;
+    }
+    m.incl = c;
+    m.left = __shfl_sync(HYD_FULL, c, 31);
+    m.wpos += 32;
+  }
+  const uint32_t n = min(m.left, 32u);
+  // lane r takes the r-th remaining member: the word w with incl[w-1] <= r < incl[w]
+  const uint32_t r = (uint32_t)lane;
+  uint32_t lo = 0;
+#pragma unroll
+  for (int step = 16; step > 0; step >>= 1) {
+    const uint32_t probe = __shfl_sync(HYD_FULL, m.incl, lo + step - 1);
+    if (probe <= r) lo += step;
+  }
+  // lo = word index holding rank r (valid when r < n)
+  const uint32_t before_raw = __shfl_sync(HYD_FULL, m.incl, lo ? lo - 1 : 0);  // all lanes shuffle
+  const uint32_t before = lo ? before_raw : 0u;
+  const uint32_t bits = __shfl_sync(HYD_FULL, m.wbits, lo & 31u);
+  if (r < n) {
+    const uint32_t bit = __fns(bits, 0, (int)(r - before) + 1);
+    idx = (m.wpos - 32u + lo) * 32u + bit;
+    l = __ldg(sl + idx);
+    tau = __ldg(cs + (size_t)idx * kp + k);
+  }
+  // consume n members: clear the n lowest set bits across the window
+  const uint32_t up = __shfl_up_sync(HYD_FULL, m.incl, 1);  // all lanes shuffle
+  const uint32_t mine_before = lane ? up : 0u;
+  const uint32_t take0 = n > mine_before ? n - mine_before : 0u;
+  uint32_t take = min(take0, (uint32_t)__popc(m.wbits));
+  while (take--) m.wbits &= m.wbits - 1u;
+  m.incl = m.incl > n ? m.incl - n : 0u;
+  m.left -= n;
+  return n;
+}
+
+// LPT(V) over the member stream, bins b = lane + 32 r (R register slots, or scratch when R == 0).
+// Writes mb when `write`; returns false if infeasible or the running max exceeds thr.
 template <int R, typename TT>
-__device__ __forceinline__ bool lpt_warp(const uint16_t* __restrict__ lst, uint16_t* __restrict__ mbr,
-                                         uint32_t U, uint32_t V, uint32_t M,
-                                         const uint32_t* __restrict__ sl,
+__device__ __forceinline__ bool lpt_warp(const uint32_t* __restrict__ mw, uint32_t nwords,
+                                         uint32_t V, uint32_t M, const uint32_t* __restrict__ sl,
                                          const uint32_t* __restrict__ cs, int kp, uint32_t k,
-                                         const uint32_t* __restrict__ el,
-                                         const uint32_t* __restrict__ ta, uint64_t thr64,
+                                         uint64_t thr64, bool write, uint16_t* __restrict__ mrow,
                                          uint64_t& maxbin, uint64_t* scr_t, uint32_t* scr_k,
                                          uint64_t& evals) {
   const int lane = threadIdx.x & 31;
@@ -792,90 +861,82 @@ __device__ __forceinline__ bool lpt_warp(const uint16_t* __restrict__ lst, uint1
       scr_k[32 * r + lane] = (32 * r + lane) < V ? 0u : 0xFFFFFFFFu;
     }
   }
+  MemberStream ms;
+  ms_open(ms, mw, nwords);
   TT mx = 0;
-  for (uint32_t q = 0; q < U; ++q) {
-    uint32_t l;
-    TT tau;
-    if (el) {  // member (length, cost) staged in shared memory by the list build
-      l = el[q];
-      tau = (TT)ta[q];
-    } else {
-      const uint32_t idx = lst[q];
-      l = __ldg(sl + idx);
-      tau = (TT)__ldg(cs + (size_t)idx * kp + k);
-    }
-    const uint32_t cap = M - l;
-    TT lt = ~TT(0);
-    uint32_t lr = 0xFFFFu;
-    if (R > 0) {
-#pragma unroll
-      for (int r = 0; r < RR; ++r)
-        if (tk[r] <= cap && tm[r] < lt) {
-          lt = tm[r];
-          lr = (uint32_t)r;
-        }
-    } else {
-      for (uint32_t r = 0; r < rn; ++r) {
-        const uint32_t tkr = scr_k[32 * r + lane];
-        const TT tmr = (TT)scr_t[32 * r + lane];
-        if (tkr <= cap && tmr < lt) {
-          lt = tmr;
-          lr = r;
-        }
-      }
-    }
-    const TT m = warp_min<TT>(lt);
-    evals += V;
-    if (m == ~TT(0)) return false;  // no bin fits: LPT(V) = bottom (warp-uniform)
-    const uint32_t bstar = __reduce_min_sync(HYD_FULL, lt == m ? (uint32_t)lane + 32u * lr : 0xFFFFFFFFu);
-    if ((bstar & 31u) == (uint32_t)lane) {
-      const uint32_t rs = bstar >> 5;
+  uint32_t cidx = 0, cl = 0, ctau = 0, n;
+  while ((n = ms_next32(ms, sl, cs, kp, k, cidx, cl, ctau)) != 0) {
+    for (uint32_t q = 0; q < n; ++q) {
+      const uint32_t l = __shfl_sync(HYD_FULL, cl, q);
+      const TT tau = (TT)__shfl_sync(HYD_FULL, ctau, q);
+      const uint32_t iq = __shfl_sync(HYD_FULL, cidx, q);
+      const uint32_t cap = M - l;
+      TT lt = ~TT(0);
+      uint32_t lr = 0xFFFFu;
       if (R > 0) {
 #pragma unroll
-        for (int r = 0; r < RR; ++r) {  // branch-free (a switch compiles to a jump table)
-          const bool h = (uint32_t)r == rs;
-          tm[r] += h ? tau : (TT)0;
-          tk[r] += h ? l : 0u;
-        }
+        for (int r = 0; r < RR; ++r)
+          if (tk[r] <= cap && tm[r] < lt) {
+            lt = tm[r];
+            lr = (uint32_t)r;
+          }
       } else {
-        scr_t[bstar] += (uint64_t)tau;
-        scr_k[bstar] += l;
+        for (uint32_t r = 0; r < rn; ++r) {
+          const uint32_t tkr = scr_k[32 * r + lane];
+          const TT tmr = (TT)scr_t[32 * r + lane];
+          if (tkr <= cap && tmr < lt) {
+            lt = tmr;
+            lr = r;
+          }
+        }
       }
+      const TT m = warp_min<TT>(lt);
+      evals += V;
+      if (m == ~TT(0)) return false;  // no bin fits: LPT(V) = bottom (warp-uniform)
+      const uint32_t bstar = __reduce_min_sync(HYD_FULL, lt == m ? (uint32_t)lane + 32u * lr : 0xFFFFFFFFu);
+      if ((bstar & 31u) == (uint32_t)lane) {
+        const uint32_t rs = bstar >> 5;
+        if (R > 0) {
+#pragma unroll
+          for (int r = 0; r < RR; ++r) {  // branch-free (a switch compiles to a jump table)
+            const bool h = (uint32_t)r == rs;
+            tm[r] += h ? tau : (TT)0;
+            tk[r] += h ? l : 0u;
+          }
+        } else {
+          scr_t[bstar] += (uint64_t)tau;
+          scr_k[bstar] += l;
+        }
+        if (write) mrow[iq] = (uint16_t)bstar;
+      }
+      const TT nt = m + tau;
+      mx = nt > mx ? nt : mx;
+      if (mx > thr) return false;
     }
-    const TT nt = m + tau;
-    mx = nt > mx ? nt : mx;
-    if (mx > thr) return false;
-    if (lane == 0) mbr[q] = (uint16_t)bstar;
   }
   maxbin = (uint64_t)mx;
   return true;
 }
 
 template <typename TT>
-__device__ __forceinline__ bool lpt_warp_dispatch(const uint16_t* lst, uint16_t* mbr, uint32_t U,
-                                                  uint32_t V, uint32_t M, const uint32_t* sl,
-                                                  const uint32_t* cs, int kp, uint32_t k,
-                                                  const uint32_t* el, const uint32_t* ta,
-                                                  uint64_t thr, uint64_t& maxbin, uint64_t* st,
+__device__ __forceinline__ bool lpt_warp_dispatch(const uint32_t* mw, uint32_t nwords, uint32_t V,
+                                                  uint32_t M, const uint32_t* sl, const uint32_t* cs,
+                                                  int kp, uint32_t k, uint64_t thr, bool write,
+                                                  uint16_t* mrow, uint64_t& maxbin, uint64_t* st,
                                                   uint32_t* sk, uint64_t& ev) {
-  if (V <= 32) return lpt_warp<1, TT>(lst, mbr, U, V, M, sl, cs, kp, k, el, ta, thr, maxbin, st, sk, ev);
-  if (V <= 64) return lpt_warp<2, TT>(lst, mbr, U, V, M, sl, cs, kp, k, el, ta, thr, maxbin, st, sk, ev);
-  if (V <= 128) return lpt_warp<4, TT>(lst, mbr, U, V, M, sl, cs, kp, k, el, ta, thr, maxbin, st, sk, ev);
-  if (V <= 32 * kBigRMax) return lpt_warp<kBigRMax, TT>(lst, mbr, U, V, M, sl, cs, kp, k, el, ta, thr, maxbin, st, sk, ev);
-  return lpt_warp<0, TT>(lst, mbr, U, V, M, sl, cs, kp, k, el, ta, thr, maxbin, st, sk, ev);
+  if (V <= 32) return lpt_warp<1, TT>(mw, nwords, V, M, sl, cs, kp, k, thr, write, mrow, maxbin, st, sk, ev);
+  if (V <= 64) return lpt_warp<2, TT>(mw, nwords, V, M, sl, cs, kp, k, thr, write, mrow, maxbin, st, sk, ev);
+  if (V <= 128) return lpt_warp<4, TT>(mw, nwords, V, M, sl, cs, kp, k, thr, write, mrow, maxbin, st, sk, ev);
+  if (V <= 32 * kBigRMax) return lpt_warp<kBigRMax, TT>(mw, nwords, V, M, sl, cs, kp, k, thr, write, mrow, maxbin, st, sk, ev);
+  return lpt_warp<0, TT>(mw, nwords, V, M, sl, cs, kp, k, thr, write, mrow, maxbin, st, sk, ev);
 }
 
-__global__ void __launch_bounds__(256) k_pack_big(PackArgs a, int stage_items) {
-  extern __shared__ __align__(16) uint32_t sm[];
+// Persistent warps over the queue: one pipeline per warp, the sequential exact search
+// (V_a, ascending scan with the exact pruning, extension above the range).
+__global__ void __launch_bounds__(256) k_pack_big(PackArgs a) {
   const int B = a.batch, kp = a.k_pad;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw = blockIdx.x * (blockDim.x >> 5) + warp;  // scratch slot
-  // per warp: [el B u32][ta B u32] (if stage_items) [lst B u16][mbr B u16]
-  uint32_t* wbase = sm + (size_t)warp * (stage_items ? 3 : 1) * B;
-  uint32_t* el = stage_items ? wbase : nullptr;
-  uint32_t* ta = stage_items ? wbase + B : nullptr;
-  uint16_t* lst = reinterpret_cast<uint16_t*>(stage_items ? wbase + 2 * B : wbase);
-  uint16_t* mbr = lst + B;
   uint64_t* scr_t = a.scr_time + (size_t)gw * B;
   uint32_t* scr_k = a.scr_tok + (size_t)gw * B;
   const unsigned long long total = min(*a.q_count, a.q_cap);
@@ -888,69 +949,39 @@ __global__ void __launch_bounds__(256) k_pack_big(PackArgs a, int stage_items) {
     const unsigned long long e = a.queue[task];
     const int c = (int)(e >> 37), t = (int)((e >> 5) & 0xFFFFFFFFull), j = (int)(e & 31);
     const size_t row = (size_t)c * a.n_iter + t;
+    const size_t srow = ((size_t)t * a.n_cand + c) * a.mnp + j;
     const uint32_t* sl = a.sorted_len + (size_t)t * B;
     const uint32_t* cs = a.cost + (size_t)t * B * kp;
+    const uint32_t* mw = a.members + srow * a.nwords;
     const uint32_t k = a.cand[(size_t)c * HYD_MAX_PIPES + j];
+    const hyd_pipe_stats st = a.stats[srow];
     Search s;
     s.M = a.schemes[k].max_len;
     s.P = a.schemes[k].pp;
     s.UL = a.schemes[k].util_len;
-    // member list from the membership bitmap: one word per lane per round, warp scan of counts
-    const uint32_t* mw = a.members + (((size_t)t * a.n_cand + c) * a.mnp + j) * a.nwords;
-    uint32_t n = 0;
-    uint64_t S = 0, sumT = 0;
-    for (int base = 0; base < a.nwords; base += 32) {
-      const int w = base + lane;
-      uint32_t bits = w < a.nwords ? __ldg(mw + w) : 0u;
-      const uint32_t cnt = __popc(bits);
-      uint32_t incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(HYD_FULL, incl, o);
-        if (lane >= o) incl += y;
-      }
-      uint32_t pos = n + incl - cnt;
-      while (bits) {
-        const int b = __ffs(bits) - 1;
-        bits &= bits - 1;
-        const uint32_t idx = (uint32_t)(32 * w + b);
-        const uint32_t l = __ldg(sl + idx), tau = __ldg(cs + (size_t)idx * kp + k);
-        if (stage_items) {
-          el[pos] = l;
-          ta[pos] = tau;
-        }
-        lst[pos++] = (uint16_t)idx;
-        S += l;
-        sumT += tau;
-      }
-      n += __shfl_sync(HYD_FULL, incl, 31);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      S += __shfl_xor_sync(HYD_FULL, S, o);
-      sumT += __shfl_xor_sync(HYD_FULL, sumT, o);
-    }
-    __syncwarp();
-    s.U = n;
-    s.S = S;
-    s.sumT = sumT;
-    s.tau_max = n ? __ldg(cs + (size_t)lst[0] * kp + k) : 0u;
+    s.U = st.u;
+    s.S = st.s;
+    s.sumT = st.sum_t;
+    s.tau_max = st.tau_max;
     uint16_t* mrow = a.mb + row * B;
-    if (n) {
+    if (s.U) {
       search_init(s);
       const bool narrow = s.sumT < 0xFFFFFFFFull;
-      uint32_t V;
+      uint32_t V, wV = 0;
+      bool first = true;
       while ((V = search_next(s)) != 0) {
-        const uint64_t thr = search_thr_approx(s, V);
+        const uint64_t thr = first ? ~0ull : search_thr_approx(s, V);
         uint64_t mx = 0;
-        const bool ok = narrow ? lpt_warp_dispatch<uint32_t>(lst, mbr, s.U, V, s.M, sl, cs, kp, k, el, ta, thr, mx, scr_t, scr_k, ev)
-                               : lpt_warp_dispatch<uint64_t>(lst, mbr, s.U, V, s.M, sl, cs, kp, k, el, ta, thr, mx, scr_t, scr_k, ev);
-        __syncwarp();
-        if (ok && search_improves(s, V, mx)) {
-          search_take(s, V, mx);
-          for (uint32_t q = lane; q < s.U; q += 32) mrow[lst[q]] = mbr[q];
-        }
-        __syncwarp();
+        const bool ok = narrow ? lpt_warp_dispatch<uint32_t>(mw, a.nwords, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, scr_t, scr_k, ev)
+                               : lpt_warp_dispatch<uint64_t>(mw, a.nwords, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, scr_t, scr_k, ev);
+        if (ok && first) wV = V;
+        first = false;
+        if (ok && search_improves(s, V, mx)) search_take(s, V, mx);
+      }
+      if (s.have && s.vbest != wV) {  // the winner's mb was not written by the first run
+        uint64_t mx = 0;
+        if (narrow) lpt_warp_dispatch<uint32_t>(mw, a.nwords, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, scr_t, scr_k, ev);
+        else lpt_warp_dispatch<uint64_t>(mw, a.nwords, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, scr_t, scr_k, ev);
       }
     } else {
       s.best = 0;
@@ -962,7 +993,6 @@ __global__ void __launch_bounds__(256) k_pack_big(PackArgs a, int stage_items) {
       atomicMax(reinterpret_cast<unsigned long long*>(a.makespan + (size_t)t * a.n_cand + c),
                 (unsigned long long)s.best);
     }
-    __syncwarp();
   }
   if (lane == 0 && ev) atomicAdd(a.evals, (unsigned long long)ev);
 }
@@ -1073,16 +1103,8 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
   note_launch();
   if (e != cudaSuccess) return record_cuda_error(e);
 
-  // warp per pipeline for the queue (V > 16, wide sums, ragged batches); members' (l, tau)
-  // staged in smem next to the list when they fit
-  const int stage_items = batch <= 1024 ? 1 : 0;
-  const size_t per_warp = (size_t)batch * 4 * (stage_items ? 3 : 1);
-  int wpb = 8;
-  while (wpb > 1 && (size_t)wpb * per_warp > 96 * 1024) wpb >>= 1;
-  const size_t bsm = (size_t)wpb * per_warp;
-  e = cudaFuncSetAttribute(k_pack_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
-  if (e != cudaSuccess) return record_cuda_error(e);
-  k_pack_big<<<kBigWarps / wpb, wpb * 32, bsm, s>>>(a, stage_items);
+  // warp per pipeline for the queue (V > 32, wide sums, infeasible V_a): persistent, no smem
+  k_pack_big<<<kBigWarps / 8, 256, 0, s>>>(a);
   note_launch();
   e = cudaGetLastError();
   return e == cudaSuccess ? HYD_OK : record_cuda_error(e);
