@@ -131,11 +131,12 @@ class Assigner:
     def pack_counters(self) -> dict:
         """Work counter written by the last hyd_pack (include/hyd.h: u64 at ws offset 16)."""
         self.torch.cuda.synchronize(self.dev)
-        w = self.ws[0:112].cpu().numpy().view(np.uint64)
+        w = self.ws[0:256].cpu().numpy().view(np.uint64)
         names = ["sumt16", "va16", "bottom16", "cand16", "sumt32", "bottom32", "cand32", "overflow",
-                 "cand_total16", "tasks_total16", "cand_max_cta16"]
+                 "clk_records", "clk_phase1", "clk_phase1b", "clk_walk", "clk_phase2", "clk_phase3",
+                 "units_phase2", "tasks_lanes16"]
         return {"bin_evals": int(w[2]), "queued_tasks": int(w[0]),
-                "handoff": {n: int(x) for n, x in zip(names, w[3:14])}}
+                "handoff": {n: int(x) for n, x in zip(names, w[3:19])}}
 
     def dispatch_evals(self, lengths) -> int:
         """Sum over feasible (c,t) of sum_i J_i (feasible pipelines per sequence): the

@@ -310,13 +310,16 @@ __device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords,
                                          const uint32_t* __restrict__ slen,
                                          const uint32_t* __restrict__ cst, int kp, uint64_t& ev) {
   constexpr int SH = LaneCfg<VM>::SH;
-  while (u.cur == 0) {  // next membership word (prefetched one ahead)
-    if (u.qw >= nwords) return 1;
+  // next membership word (prefetched one ahead); a single-exit loop so the compiler places the
+  // reconvergence point right after it (an early return here splits the warp for the whole step)
+  while (u.cur == 0 && u.qw < nwords) {
     u.cur = u.nxtw;
     u.wbase = u.qw * 32u;
     ++u.qw;
     u.nxtw = u.qw < nwords ? __ldg(u.mw + u.qw) : 0u;
   }
+  __syncwarp(__activemask());
+  if (u.cur == 0) return 1;  // every member placed
   const uint32_t i = u.wbase + (uint32_t)(__ffs(u.cur) - 1);
   u.cur &= u.cur - 1u;
   const uint32_t l = slen[i];
@@ -403,6 +406,14 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
     }
   };
 
+  long long t_mark = clock64();
+  auto phase_clock = [&](int slot) {  // diagnostic: per-phase SM cycles (thread 0, VM = 16)
+    if (VM == 16 && tid == 0) {
+      const long long now = clock64();
+      atomicAdd(a.why + 8 + slot, (unsigned long long)(now - t_mark));
+      t_mark = now;
+    }
+  };
   // ---- task records (parallel, compacted), bucketed by (class, U) for LPT-order processing
   for (int e = tid; e < ntile; e += kLaneThreads) {
     const int c = c0 + e / mnp, j = e % mnp;
@@ -508,34 +519,32 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
     u.write = write;
     unit_start<VM>(u, V, thr);
   };
-  // Warp-batch scheduling: a warp takes 32 consecutive units of a list sorted by (class, U), so
-  // its lanes run the same code path over nearly the same number of sequences and finish
-  // together; it takes the next batch when all 32 are done.  Inside a batch, lanes step in
-  // epochs of kLaneEpoch sequences.  pull(q) prepares unit q (false: nothing to run).
+  // Lanes pull consecutive units of a list sorted by (class, U) -- so the units a warp holds at
+  // any time have the same class and similar U -- and refill as soon as their unit ends.
+  // Between epochs of kLaneEpoch sequences, all lanes whose unit ended record it and pull the
+  // next one together (converged); the VMAX code path is chosen per epoch for the whole warp.
   auto run_units = [&](int n_units, auto&& pull, auto&& finish) {
     if (tid == 0) s_next = 0;
     __syncthreads();
+    bool have = false, done = false;
     while (true) {
-      int base = 0;
-      if (lane == 0) base = atomicAdd(&s_next, 32);
-      base = __shfl_sync(HYD_FULL, base, 0);
-      if (base >= n_units) break;
-      const int q = base + lane;
-      bool have = q < n_units && pull(q);
-      // one code path per batch: the widest unit decides (narrower units run with sentinel bins)
+      while (!have && !done) {
+        const int q = atomicAdd(&s_next, 1);
+        if (q >= n_units) done = true;
+        else have = pull(q);
+      }
+      if (__all_sync(HYD_FULL, !have)) break;
       const bool narrow = __all_sync(HYD_FULL, !have || u.V <= 8u);
-      while (__any_sync(HYD_FULL, have)) {
-        if (have) {
-          int st = 0;
+      if (have) {
+        int st = 0;
 #pragma unroll 1
-          for (int e = 0; e < kLaneEpoch && st == 0; ++e) {
-            if (VM == 16 && narrow) st = unit_step<8, VM>(u, nwords, slen, cst, kp, ev);
-            else st = unit_step<VM, VM>(u, nwords, slen, cst, kp, ev);
-          }
-          if (st) {
-            finish(st);
-            have = false;
-          }
+        for (int e = 0; e < kLaneEpoch && st == 0; ++e) {
+          if (VM == 16 && narrow) st = unit_step<8, VM>(u, nwords, slen, cst, kp, ev);
+          else st = unit_step<VM, VM>(u, nwords, slen, cst, kp, ev);
+        }
+        if (st) {
+          finish(st);
+          have = false;
         }
       }
     }
@@ -563,6 +572,7 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
     return s_n2a;
   };
 
+  phase_clock(0);
   // ---- phase 1: the V_a run of every task (writes mb)
   run_units(
       nrec,
@@ -573,6 +583,7 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
       },
       [&](int st) { R.key[u.e] = st == 1 ? obj_key(u) : kBottom; });
 
+  phase_clock(1);
   // ---- phase 1b: where LPT(V_a) is infeasible (capacity), V_a + 1 is tried; it then takes
   //      V_a's place as the reference run of the exact tests below
   {
@@ -594,6 +605,7 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
         });
   }
 
+  phase_clock(2);
   // ---- phase 1.5 (thread per task): every V of App. D's range that survives the exact tests
   //      against the reference run, bucket-sorted by (class, U) into list2; tasks that do not
   //      fit are handed off
@@ -697,6 +709,8 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
   }
   __syncthreads();
 
+  phase_clock(3);
+  if (VM == 16 && tid == 0) atomicAdd(a.why + 14, (unsigned long long)s_n2b);
   // ---- phase 2: the surviving V, each an independent run against the reference; argmin by
   //      atomicMin on (obj << 16 | V)
   run_units(
@@ -719,6 +733,7 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
         if (st == 1) atomicMin(&R.key[u.e], obj_key(u));
       });
 
+  phase_clock(4);
   // ---- phase 3: tasks whose winner is not the reference run write their mb with one more run
   {
     const int n3 = compact([&](int r) {
@@ -734,6 +749,8 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
         [&](int) {});
   }
 
+  phase_clock(5);
+  if (VM == 16 && tid == 0) atomicAdd(a.why + 15, (unsigned long long)nrec);
   // ---- outputs (parallel over tasks)
   for (int r = tid; r < nrec; r += kLaneThreads) {
     if (R.state[r] == 1) continue;
@@ -1069,7 +1086,7 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
   w += align256((size_t)kBigWarps * batch * 4);
   a.flags = reinterpret_cast<uint32_t*>(w);
 
-  cudaError_t e = cudaMemsetAsync(a.q_count, 0, 112, s);
+  cudaError_t e = cudaMemsetAsync(a.q_count, 0, 256, s);
   if (e != cudaSuccess) return record_cuda_error(e);
   e = cudaMemsetAsync(a.flags, 0, flag_bytes(n_iter, n_cand, max_np), s);
   if (e != cudaSuccess) return record_cuda_error(e);
