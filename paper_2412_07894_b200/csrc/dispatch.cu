@@ -45,11 +45,42 @@ __device__ __forceinline__ uint32_t dispatch_step(uint32_t l, const uint32_t* __
   // branch-free update of pipeline bj (a switch here compiles to a divergent jump table)
 #pragma unroll
   for (int j = 0; j < DP; ++j) {
-    const uint32_t hit = 0u - (uint32_t)((uint32_t)j == bj);
-    const TT hitw = (TT)0 - (TT)((uint32_t)j == bj);
-    base[j] = (base[j] & ~hitw) | (best & hitw);
-    mult[j] = (mult[j] & ~hit) | (1u & hit);
-    bits[j] |= bit & hit;
+    const bool hit = (uint32_t)j == bj;
+    base[j] = hit ? best : base[j];
+    mult[j] = hit ? 1u : mult[j];
+    bits[j] |= hit ? bit : 0u;
+  }
+  return bj;
+}
+
+// Packed-key step (all loads < 2^(31 - SH)): key_j = (C_j + E_j) << SH | j, so the candidate
+// key is one IMAD, the argmin is a VIMNMX tree with no index bookkeeping, and the winner's new
+// key is the minimum itself.  FEAS masks pipelines with MaxLen_j < l via bit 31.
+template <int DP, bool FEAS>
+__device__ __forceinline__ uint32_t key_step(uint32_t l, const uint32_t* __restrict__ crow,
+                                             bool staged, const uint32_t (&ml)[DP],
+                                             const uint32_t (&kk)[DP], uint32_t (&key)[DP],
+                                             uint32_t (&mults)[DP], uint32_t (&bits)[DP],
+                                             uint32_t bit, uint32_t one_sh) {
+  uint32_t m[DP];
+#pragma unroll
+  for (int j = 0; j < DP; ++j) {
+    const uint32_t tau = staged ? crow[kk[j]] : __ldg(crow + kk[j]);
+    m[j] = key[j] + tau * mults[j];
+    if (FEAS) m[j] |= (l > ml[j]) ? 0x80000000u : 0u;
+  }
+#pragma unroll
+  for (int w = DP / 2; w > 0; w >>= 1)
+#pragma unroll
+    for (int j = 0; j < w; ++j) m[j] = min(m[j], m[j + w]);
+  const uint32_t mk = m[0];
+  const uint32_t bj = mk & (uint32_t)(DP - 1);
+#pragma unroll
+  for (int j = 0; j < DP; ++j) {
+    const bool hit = (uint32_t)j == bj;
+    key[j] = hit ? mk : key[j];
+    mults[j] = hit ? one_sh : mults[j];
+    bits[j] |= hit ? bit : 0u;
   }
   return bj;
 }
@@ -62,7 +93,8 @@ __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
                                              uint8_t* __restrict__ prow, unsigned long long* s_sum,
                                              uint32_t* __restrict__ mbits, int np, int nwords,
                                              uint64_t& lb_out, TT (&base)[DP], uint32_t (&cnt)[DP],
-                                             uint32_t (&tmax)[DP]) {
+                                             uint32_t (&tmax)[DP], bool packed) {
+  constexpr int SH = DP <= 2 ? 1 : DP <= 4 ? 2 : DP <= 8 ? 3 : DP <= 16 ? 4 : 5;
   uint32_t mult[DP], bits[DP];
   uint32_t ml_min = 0xFFFFFFFFu;
 #pragma unroll
@@ -74,14 +106,28 @@ __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
     tmax[j] = 0u;
     if (j < np) ml_min = min(ml_min, ml[j]);
   }
+  uint32_t key[DP], mults[DP];
+  if (packed) {
+#pragma unroll
+    for (int j = 0; j < DP; ++j) {
+      key[j] = j < np ? (uint32_t)j : 0x7FFFFFFFu;  // unused slots never win (bit 31 clear, > any)
+      mults[j] = mult[j] << SH;
+    }
+  }
   const bool words = (B & 3) == 0;
   uint32_t word = 0u;
   for (int i = 0; i < B; ++i) {
     const uint32_t l = sl[i];
     const uint32_t* crow = cs + (size_t)i * k_pad;
     const uint32_t bit = 1u << (i & 31);
-    const uint32_t bj = l > ml_min ? dispatch_step<DP, TT, true>(l, crow, staged, ml, kk, base, mult, bits, bit)
-                                   : dispatch_step<DP, TT, false>(l, crow, staged, ml, kk, base, mult, bits, bit);
+    uint32_t bj;
+    if (packed) {
+      bj = l > ml_min ? key_step<DP, true>(l, crow, staged, ml, kk, key, mults, bits, bit, 1u << SH)
+                      : key_step<DP, false>(l, crow, staged, ml, kk, key, mults, bits, bit, 1u << SH);
+    } else {
+      bj = l > ml_min ? dispatch_step<DP, TT, true>(l, crow, staged, ml, kk, base, mult, bits, bit)
+                      : dispatch_step<DP, TT, false>(l, crow, staged, ml, kk, base, mult, bits, bit);
+    }
     s_sum[bj * kDispatchThreads] += l;  // S_j column of this thread
     if ((i & 31) == 31 || i == B - 1) {  // flush one membership word per pipeline; U_j, tau_max_j
       const int w0 = i & ~31;
@@ -107,6 +153,10 @@ __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
     } else {
       prow[i] = (uint8_t)bj;
     }
+  }
+  if (packed) {
+#pragma unroll
+    for (int j = 0; j < DP; ++j) base[j] = j < np ? (TT)(key[j] >> SH) : (TT)~(TT)0;
   }
   uint64_t m = 0ull;
 #pragma unroll
@@ -171,6 +221,8 @@ __global__ void __launch_bounds__(kDispatchThreads)
   bound = 0ull;
   for (int w = 0; w < kDispatchThreads / 32; ++w) bound += s_bound[w];
   const bool narrow = bound < 0xFFFFFFFFull;
+  constexpr int SHK = DP <= 2 ? 1 : DP <= 4 ? 2 : DP <= 8 ? 3 : DP <= 16 ? 4 : 5;
+  const bool packed = bound < (1ull << (31 - SHK));  // keys (load << SHK | j) stay below 2^31
 
   const int lt = tid / ct, lc = tid - lt * ct;
   const int c = c0 + lc, t = t0 + lt;
@@ -226,12 +278,12 @@ __global__ void __launch_bounds__(kDispatchThreads)
   if (narrow) {
     uint32_t base[DP];
     dispatch_run<DP, uint32_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, ssum, mbits, np, nwords,
-                               lbv, base, cnt, tmx);
+                               lbv, base, cnt, tmx, packed);
 #pragma unroll
     for (int j = 0; j < DP; ++j) base64[j] = base[j];
   } else {
     dispatch_run<DP, uint64_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, ssum, mbits, np, nwords,
-                               lbv, base64, cnt, tmx);
+                               lbv, base64, cnt, tmx, false);
   }
   lb[row] = lbv;
   hyd_pipe_stats* st = stats + srow * max_np;
