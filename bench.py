@@ -344,6 +344,23 @@ def main():
     return 0
 
 
+def ncu_traffic(cfg, prefix):
+    """DRAM bytes per launch of the kernels named ``prefix*`` from the newest committed
+    `ncu --set full` summary of this config (profiles/rNN/ncu_cfgX_summary.json), else None."""
+    import glob
+
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"ncu_cfg{cfg}_summary.json")))
+    if not paths:
+        return None, None
+    try:
+        d = json.load(open(paths[-1]))
+        tot = sum(e["dram_bytes"] for e in d.get("full_capture", [])
+                  if any(e["kernel"].replace("void ", "").startswith(p) for p in prefix) and e.get("dram_bytes"))
+        return (tot or None), os.path.relpath(paths[-1], ROOT)
+    except Exception:
+        return None, None
+
+
 def roofline(name, ms, W, A, pk, how, local_ci):
     """Algorithmic work per launch / CUDA-event duration."""
     B, D = W.batch, int(W.cand_np.max())
@@ -354,8 +371,11 @@ def roofline(name, ms, W, A, pk, how, local_ci):
         cnt = A.pack_counters()
         ops = 6.0 * cnt["bin_evals"]  # ~6 int32 ops per (item, bin) evaluation
         achieved = ops / (ms / 1000.0) / 1e9
+        traffic, src = ncu_traffic(W.cfg, ("k_pack_",))
         return {"kernel": "pack (k_pack_init + k_pack_lanes + k_pack_big)", "bound": "alu", "achieved": achieved,
-                "peak": alu_peak, "unit": "Gop/s", "frac": achieved / alu_peak, "traffic": None,
+                "peak": alu_peak, "unit": "Gop/s", "frac": achieved / alu_peak, "traffic": traffic,
+                "traffic_unit": "bytes/launch (dram read+write, ncu --set full)", "traffic_source": src,
+                "algorithmic_bytes_per_launch": local_ci * (3 * B + 10 * D + 8),
                 "algorithmic_ops_per_launch": ops, "bin_evals_per_launch": cnt["bin_evals"],
                 "queued_tasks": cnt["queued_tasks"], "handoff": cnt.get("handoff"),
                 "hbm_algorithmic_GBps": local_ci * (3 * B + 10 * D + 8) / (ms / 1000.0) / 1e9,

@@ -40,6 +40,9 @@ def report(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[0]
+    units = dict(zip(hdr, rows[1]))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+             "nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "ns": 1, "us": 1e3, "ms": 1e6, "s": 1e9}
     res = []
     for r in rows[2:]:
         d = dict(zip(hdr, r))
@@ -47,9 +50,12 @@ def report(path):
         for m, name in WANT.items():
             v = d.get(m)
             try:
-                e[name] = float(v.replace(",", "")) if v not in (None, "", "n/a") else None
+                x = float(v.replace(",", "")) if v not in (None, "", "n/a") else None
             except ValueError:
-                e[name] = None
+                x = None
+            if x is not None:
+                x *= scale.get(units.get(m, ""), 1)
+            e[name] = x
         if e.get("dram_read_bytes") is not None and e.get("dram_write_bytes") is not None:
             e["dram_bytes"] = e["dram_read_bytes"] + e["dram_write_bytes"]
         res.append(e)
