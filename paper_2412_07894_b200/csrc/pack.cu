@@ -546,10 +546,7 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
           if (VM == 16 && narrow) st = unit_step<8, VM>(u, nwords, slen, cst, kp, ev);
           else st = unit_step<VM, VM>(u, nwords, slen, cst, kp, ev);
         }
-        if (st) {
-          finish(st);
-          have = false;
-        }
+        if (st) have = finish(st);  // finish may load a follow-up unit into this lane
       }
     }
     __syncthreads();
@@ -577,7 +574,9 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
   };
 
   phase_clock(0);
-  // ---- phase 1: the V_a run of every task (writes mb)
+  // ---- phase 1: the V_a run of every task (writes mb); where LPT(V_a) is infeasible
+  //      (capacity), the same lane goes on with V_a + 1, which then takes V_a's place as the
+  //      reference run of the exact tests below
   run_units(
       nrec,
       [&](int q) {
@@ -585,30 +584,20 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
         load_unit(r, R.va[r], 0xFFFFFFFFu, true);
         return true;
       },
-      [&](int st) { R.key[u.e] = st == 1 ? obj_key(u) : kBottom; });
-
+      [&](int st) -> bool {
+        const int r = u.e;
+        if (st == 1) {
+          R.key[r] = obj_key(u);
+          return false;
+        }
+        R.key[r] = kBottom;
+        const uint32_t V = u.V + 1u;
+        if (V > (uint32_t)R.vhi[r] || V > (uint32_t)VM || V != (uint32_t)R.va[r] + 1u) return false;
+        R.va[r] = (uint16_t)V;
+        load_unit(r, V, 0xFFFFFFFFu, true);
+        return true;  // keep the lane on this task
+      });
   phase_clock(1);
-  // ---- phase 1b: where LPT(V_a) is infeasible (capacity), V_a + 1 is tried; it then takes
-  //      V_a's place as the reference run of the exact tests below
-  {
-    const int n1b = compact([&](int r) {
-      const uint32_t V = (uint32_t)R.va[r] + 1u;
-      return R.key[r] == kBottom && V <= (uint32_t)R.vhi[r] && V <= (uint32_t)VM;
-    });
-    run_units(
-        n1b,
-        [&](int q) {
-          const int r = (int)R.list2[q];
-          const uint32_t V = (uint32_t)R.va[r] + 1u;
-          R.va[r] = (uint16_t)V;
-          load_unit(r, V, 0xFFFFFFFFu, true);
-          return true;
-        },
-        [&](int st) {
-          if (st == 1) R.key[u.e] = obj_key(u);
-        });
-  }
-
   phase_clock(2);
   // ---- phase 1.5 (thread per task): every V of App. D's range that survives the exact tests
   //      against the reference run, bucket-sorted by (class, U) into list2; tasks that do not
@@ -715,6 +704,12 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
 
   phase_clock(3);
   if (VM == 16 && tid == 0) atomicAdd(a.why + 14, (unsigned long long)s_n2b);
+  // pending phase-2 units per task (sum_t is no longer needed: reused as the counter)
+  for (int r = tid; r < nrec; r += kLaneThreads) {
+    const int packed = R.ncand[r];
+    R.sum_t[r] = (R.state[r] == 1) ? 0u : (uint32_t)((packed & 0xFF) + (packed >> 8));
+  }
+  __syncthreads();
   // ---- phase 2: the surviving V, each an independent run against the reference; argmin by
   //      atomicMin on (obj << 16 | V)
   run_units(
@@ -733,26 +728,20 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
         load_unit(r, V, th > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)th, false);
         return true;
       },
-      [&](int st) {
-        if (st == 1) atomicMin(&R.key[u.e], obj_key(u));
+      [&](int st) -> bool {
+        const int r = u.e;
+        if (st == 1 && !u.write) atomicMin(&R.key[r], obj_key(u));
+        if (u.write) return false;  // this was the task's final mb run
+        // the lane finishing a task's last candidate writes the winner's mb if it is not the
+        // reference run (whose mb phase 1 already wrote)
+        if (atomicSub(&R.sum_t[r], 1u) != 1u) return false;
+        const uint32_t V = (uint32_t)(R.key[r] & 0xFFFFu);
+        if (V == (uint32_t)R.va[r]) return false;
+        load_unit(r, V, 0xFFFFFFFFu, true);
+        return true;
       });
 
   phase_clock(4);
-  // ---- phase 3: tasks whose winner is not the reference run write their mb with one more run
-  {
-    const int n3 = compact([&](int r) {
-      return R.state[r] != 1 && (uint32_t)(R.key[r] & 0xFFFFu) != (uint32_t)R.va[r];
-    });
-    run_units(
-        n3,
-        [&](int q) {
-          const int r = (int)R.list2[q];
-          load_unit(r, (uint32_t)(R.key[r] & 0xFFFFu), 0xFFFFFFFFu, true);
-          return true;
-        },
-        [&](int) {});
-  }
-
   phase_clock(5);
   if (VM == 16 && tid == 0) atomicAdd(a.why + 15, (unsigned long long)nrec);
   // ---- outputs (parallel over tasks)
