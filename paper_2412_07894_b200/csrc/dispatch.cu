@@ -14,13 +14,19 @@
 // Per-pipeline statistics for the packing stage: S_j in a shared-memory column indexed by j*
 // (one LDS/STS per sequence); U_j and tau_max,j from the membership bitmap words, which are
 // flushed every 32 sequences.
-// The sums run in u32 when a per-CTA bound proves every load < 2^32, else in u64.
+// A per-CTA bound on every load picks the arithmetic: packed u32 keys (packed_run, MODE 0
+// kernel) when loads < 2^(31 - log2 DP), else u32 or u64 sums (dispatch_run, MODE 1 kernel).
 // Outputs: pipe[c][t][i] (4 decisions per u32 store), lb[c][t] = max_j base_j, stats.
 #include "hyd_internal.cuh"
 
 namespace hyd {
 
 constexpr int kDispatchThreads = 128;
+
+// staged words: [tt][B] lengths + costs (rows [tt][B][k_pad], or transposed [tt][k_pad][B | 1])
+__host__ __device__ inline size_t dispatch_stage_words(int tt, int B, int k_pad) {
+  return (size_t)tt * B + (size_t)tt * k_pad * (size_t)(B | 1);
+}
 
 // One sequence step: candidate loads, argmin (new_j, j), branch-free update of pipeline j*.
 // FEAS: test MaxLen_j >= l (only needed while l exceeds the smallest MaxLen of the candidate;
@@ -53,38 +59,6 @@ __device__ __forceinline__ uint32_t dispatch_step(uint32_t l, const uint32_t* __
   return bj;
 }
 
-// Packed-key step (all loads < 2^(31 - SH)): key_j = (C_j + E_j) << SH | j, so the candidate
-// key is one IMAD, the argmin is a VIMNMX tree with no index bookkeeping, and the winner's new
-// key is the minimum itself.  FEAS masks pipelines with MaxLen_j < l via bit 31.
-template <int DP, bool FEAS>
-__device__ __forceinline__ uint32_t key_step(uint32_t l, const uint32_t* __restrict__ crow,
-                                             bool staged, const uint32_t (&ml)[DP],
-                                             const uint32_t (&kk)[DP], uint32_t (&key)[DP],
-                                             uint32_t (&mults)[DP], uint32_t (&bits)[DP],
-                                             uint32_t bit, uint32_t one_sh) {
-  uint32_t m[DP];
-#pragma unroll
-  for (int j = 0; j < DP; ++j) {
-    const uint32_t tau = staged ? crow[kk[j]] : __ldg(crow + kk[j]);
-    m[j] = key[j] + tau * mults[j];
-    if (FEAS) m[j] |= (l > ml[j]) ? 0x80000000u : 0u;
-  }
-#pragma unroll
-  for (int w = DP / 2; w > 0; w >>= 1)
-#pragma unroll
-    for (int j = 0; j < w; ++j) m[j] = min(m[j], m[j + w]);
-  const uint32_t mk = m[0];
-  const uint32_t bj = mk & (uint32_t)(DP - 1);
-#pragma unroll
-  for (int j = 0; j < DP; ++j) {
-    const bool hit = (uint32_t)j == bj;
-    key[j] = hit ? mk : key[j];
-    mults[j] = hit ? one_sh : mults[j];
-    bits[j] |= hit ? bit : 0u;
-  }
-  return bj;
-}
-
 template <int DP, typename TT>
 __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
                                              const uint32_t* __restrict__ cs, bool staged, int B,
@@ -92,9 +66,8 @@ __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
                                              const uint32_t (&pp)[DP], const uint32_t (&kk)[DP],
                                              uint8_t* __restrict__ prow, unsigned long long* s_sum,
                                              uint32_t* __restrict__ mbits, int np, int nwords,
-                                             uint64_t& lb_out, TT (&base)[DP], uint32_t (&cnt)[DP],
-                                             uint32_t (&tmax)[DP], bool packed) {
-  constexpr int SH = DP <= 2 ? 1 : DP <= 4 ? 2 : DP <= 8 ? 3 : DP <= 16 ? 4 : 5;
+                                             uint64_t& lb_out, TT (&base)[DP],
+                                             uint32_t (&cf)[DP]) {
   uint32_t mult[DP], bits[DP];
   uint32_t ml_min = 0xFFFFFFFFu;
 #pragma unroll
@@ -102,17 +75,8 @@ __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
     base[j] = j < np ? (TT)0 : (TT)~(TT)0;
     mult[j] = j < np ? pp[j] : 0u;
     bits[j] = 0u;
-    cnt[j] = 0u;
-    tmax[j] = 0u;
+    cf[j] = 0u;
     if (j < np) ml_min = min(ml_min, ml[j]);
-  }
-  uint32_t key[DP], mults[DP];
-  if (packed) {
-#pragma unroll
-    for (int j = 0; j < DP; ++j) {
-      key[j] = j < np ? (uint32_t)j : 0x7FFFFFFFu;  // unused slots never win (bit 31 clear, > any)
-      mults[j] = mult[j] << SH;
-    }
   }
   const bool words = (B & 3) == 0;
   uint32_t word = 0u;
@@ -120,26 +84,19 @@ __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
     const uint32_t l = sl[i];
     const uint32_t* crow = cs + (size_t)i * k_pad;
     const uint32_t bit = 1u << (i & 31);
-    uint32_t bj;
-    if (packed) {
-      bj = l > ml_min ? key_step<DP, true>(l, crow, staged, ml, kk, key, mults, bits, bit, 1u << SH)
-                      : key_step<DP, false>(l, crow, staged, ml, kk, key, mults, bits, bit, 1u << SH);
-    } else {
-      bj = l > ml_min ? dispatch_step<DP, TT, true>(l, crow, staged, ml, kk, base, mult, bits, bit)
-                      : dispatch_step<DP, TT, false>(l, crow, staged, ml, kk, base, mult, bits, bit);
-    }
+    const uint32_t bj =
+        l > ml_min ? dispatch_step<DP, TT, true>(l, crow, staged, ml, kk, base, mult, bits, bit)
+                   : dispatch_step<DP, TT, false>(l, crow, staged, ml, kk, base, mult, bits, bit);
     s_sum[bj * kDispatchThreads] += l;  // S_j column of this thread
-    if ((i & 31) == 31 || i == B - 1) {  // flush one membership word per pipeline; U_j, tau_max_j
-      const int w0 = i & ~31;
+    if ((i & 31) == 31 || i == B - 1) {  // flush one membership word per pipeline
+      const uint32_t w0 = (uint32_t)(i & ~31);
 #pragma unroll
       for (int j = 0; j < DP; ++j) {
         if (j < np) {
           mbits[(size_t)j * nwords + (i >> 5)] = bits[j];
-          if (cnt[j] == 0u && bits[j] != 0u) {  // first (= longest) member of pipeline j
-            const uint32_t* frow = cs + (size_t)(w0 + __ffs(bits[j]) - 1) * k_pad;
-            tmax[j] = staged ? frow[kk[j]] : __ldg(frow + kk[j]);
-          }
-          cnt[j] += __popc(bits[j]);
+          // cf_j = U_j << 16 | (index of the first (= longest) member + 1), B <= 16384
+          const uint32_t f = (cf[j] & 0xFFFFu) == 0u && bits[j] != 0u ? w0 + __ffs(bits[j]) : 0u;
+          cf[j] += (__popc(bits[j]) << 16) + f;
         }
         bits[j] = 0u;
       }
@@ -154,10 +111,6 @@ __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
       prow[i] = (uint8_t)bj;
     }
   }
-  if (packed) {
-#pragma unroll
-    for (int j = 0; j < DP; ++j) base[j] = j < np ? (TT)(key[j] >> SH) : (TT)~(TT)0;
-  }
   uint64_t m = 0ull;
 #pragma unroll
   for (int j = 0; j < DP; ++j)
@@ -165,7 +118,184 @@ __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
   lb_out = m;
 }
 
-template <int DP, bool STAGED>
+// Packed-key run (MODE 0: every load of the CTA < 2^(31 - SH)).  key_j = (C_j + E_j) << SH | j,
+// so a candidate key is one IMAD, the argmin is a VIMNMX tree with no index bookkeeping and the
+// winner's new key is the minimum itself.  Same decisions as dispatch_run, with a steady-state
+// step of about half its instructions:
+//  * feasibility is folded into the keys: a pipeline with MaxLen_j < l carries bit 31 in key_j
+//    (it never wins while a feasible pipeline exists, and j = 0 always is), cleared on the rare
+//    step where l drops to its MaxLen -- the canonical order makes the infeasible set a suffix,
+//    so one compare per step against the largest pending MaxLen suffices;
+//  * the empty-pipeline multiplier PP_j (Eq. 2's first-member term) matters only until every
+//    pipeline of the thread holds a sequence; 32-step chunks run a multiplier-free step once the
+//    whole warp is past that point (warp vote: no divergence);
+//  * membership is kept as log2(DP) bit planes of j* (plane_b bit q = bit b of the q-th
+//    decision), expanded into per-pipeline words once per chunk; the chunk's 32 decision bytes
+//    leave as two 16-byte stores (one full sector);
+//  * staged cost rows are transposed to [scheme][sequence] (odd row stride: no bank conflicts),
+//    so a pipeline's costs for 4 consecutive sequences are one base register + immediates.
+template <int DP, bool EMPTY>
+__device__ __forceinline__ uint32_t packed_pick(const uint32_t (&tau)[DP], uint32_t (&key)[DP],
+                                                uint32_t (&mults)[DP], uint32_t one_sh) {
+  uint32_t m[DP];
+#pragma unroll
+  for (int j = 0; j < DP; ++j) m[j] = tau[j] * (EMPTY ? mults[j] : one_sh) + key[j];
+#pragma unroll
+  for (int w = DP / 2; w > 0; w >>= 1)
+#pragma unroll
+    for (int j = 0; j < w; ++j) m[j] = min(m[j], m[j + w]);
+  const uint32_t mk = m[0];
+  const uint32_t bj = mk & (uint32_t)(DP - 1);
+#pragma unroll
+  for (int j = 0; j < DP; ++j) {
+    const bool hit = (uint32_t)j == bj;
+    key[j] = hit ? mk : key[j];
+    if (EMPTY) mults[j] = hit ? one_sh : mults[j];
+  }
+  return bj;
+}
+
+// one decision: feasibility release (EMPTY phase only), pick, plane bits, S_j
+template <int DP, int SH, bool EMPTY>
+__device__ __forceinline__ uint32_t packed_step(uint32_t l, const uint32_t (&tau)[DP],
+                                                uint32_t (&key)[DP], uint32_t (&mults)[DP],
+                                                const uint32_t (&ml)[DP], int np, uint32_t& pend,
+                                                uint32_t (&plane)[SH],
+                                                unsigned long long* s_sum) {
+  if (EMPTY && l <= pend) {  // rare: pipelines become feasible as l drops to their MaxLen
+    uint32_t np2 = 0u;
+#pragma unroll
+    for (int j = 0; j < DP; ++j) {
+      if (j < np && (key[j] >> 31) != 0u) {
+        if (ml[j] >= l) key[j] &= 0x7FFFFFFFu;
+        else np2 = max(np2, ml[j]);
+      }
+    }
+    pend = np2;
+  }
+  const uint32_t bj = packed_pick<DP, EMPTY>(tau, key, mults, 1u << SH);
+#pragma unroll  // shift bit b of j* in from the top: after the chunk, bit q = decision q
+  for (int b = 0; b < SH; ++b) plane[b] = __funnelshift_r(plane[b], bj >> b, 1);
+  s_sum[bj * kDispatchThreads] += l;  // S_j column of this thread
+  return bj;
+}
+
+// TRANS: cost staged in smem as [lt][k][Bp] (cost(i, k) at ct[k * Bp + i] for this thread's lt);
+// else global rows [t][i][k_pad].
+template <int DP, bool TRANS>
+__device__ __forceinline__ void packed_run(const uint32_t* __restrict__ sl,
+                                           const uint32_t* __restrict__ cst, int B, int stride,
+                                           const uint32_t (&ml)[DP], const uint32_t (&pp)[DP],
+                                           const uint32_t (&kk)[DP], uint8_t* __restrict__ prow,
+                                           unsigned long long* s_sum, uint32_t* __restrict__ mbits,
+                                           int np, int nwords, uint64_t& lb_out,
+                                           uint32_t (&base)[DP], uint32_t (&cf)[DP],
+                                           unsigned amask) {
+  constexpr int SH = DP <= 2 ? 1 : DP <= 4 ? 2 : DP <= 8 ? 3 : DP <= 16 ? 4 : 5;
+  const uint32_t one_sh = 1u << SH;
+  const uint32_t l0 = sl[0];
+  uint32_t key[DP], mults[DP];
+  uint32_t pend = 0u;  // largest MaxLen among still-infeasible pipelines (0: none)
+  const uint32_t* pj[DP];  // TRANS: row of pipeline j's scheme; else column offset kk_j
+#pragma unroll
+  for (int j = 0; j < DP; ++j) {
+    const bool used = j < np;
+    const bool feas = used && ml[j] >= l0;
+    key[j] = !used ? 0x7FFFFFFFu : feas ? (uint32_t)j : (0x80000000u | (uint32_t)j);
+    mults[j] = used ? pp[j] << SH : 0u;
+    if (used && !feas) pend = max(pend, ml[j]);
+    cf[j] = 0u;
+    pj[j] = TRANS ? cst + (size_t)kk[j] * stride : cst + kk[j];
+  }
+  const bool full_sectors = (B & 31) == 0;
+  for (int i0 = 0; i0 < B; i0 += 32) {
+    const int n = min(32, B - i0);
+    bool empty = false;
+#pragma unroll
+    for (int j = 0; j < DP; ++j) empty |= j < np && (key[j] < one_sh || (key[j] >> 31) != 0u);
+    const bool warp_empty = __any_sync(amask, empty);
+    uint32_t plane[SH];
+#pragma unroll
+    for (int b = 0; b < SH; ++b) plane[b] = 0u;
+    if (TRANS) {  // n % 4 == 0 (staging requires B % 4 == 0)
+      for (int g = 0; g < n; g += 4) {
+        const int i = i0 + g;
+        const uint4 l4 = *reinterpret_cast<const uint4*>(sl + i);
+        const uint32_t lq[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint32_t tau[DP];
+#pragma unroll
+          for (int j = 0; j < DP; ++j) tau[j] = pj[j][i + u];
+          if (warp_empty)
+            packed_step<DP, SH, true>(lq[u], tau, key, mults, ml, np, pend, plane, s_sum);
+          else
+            packed_step<DP, SH, false>(lq[u], tau, key, mults, ml, np, pend, plane, s_sum);
+        }
+      }
+    } else {
+      for (int q = 0; q < n; ++q) {
+        const int i = i0 + q;
+        const uint32_t l = sl[i];
+        uint32_t tau[DP];
+#pragma unroll
+        for (int j = 0; j < DP; ++j) tau[j] = __ldg(pj[j] + (size_t)i * stride);
+        if (warp_empty)
+          packed_step<DP, SH, true>(l, tau, key, mults, ml, np, pend, plane, s_sum);
+        else
+          packed_step<DP, SH, false>(l, tau, key, mults, ml, np, pend, plane, s_sum);
+      }
+    }
+    if (n < 32) {
+#pragma unroll
+      for (int b = 0; b < SH; ++b) plane[b] >>= 32 - n;
+    }
+    // decisions of the chunk: byte q = sum_b bit q of plane_b << b
+    uint32_t wd[8];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      uint32_t x = 0u;
+#pragma unroll
+      for (int b = 0; b < SH; ++b)
+        x |= ((((plane[b] >> (4 * w)) & 0xFu) * 0x00204081u) & 0x01010101u) << b;
+      wd[w] = x;
+    }
+    if (full_sectors) {
+      uint4* dst = reinterpret_cast<uint4*>(prow + i0);
+      dst[0] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+      dst[1] = make_uint4(wd[4], wd[5], wd[6], wd[7]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        if (q < n) prow[i0 + q] = (uint8_t)(wd[q >> 2] >> (8 * (q & 3)));
+    }
+    // membership words per pipeline; U_j and first member in cf_j
+    const uint32_t valid = n == 32 ? 0xFFFFFFFFu : (1u << n) - 1u;
+#pragma unroll
+    for (int j = 0; j < DP; ++j) {
+      if (j < np) {
+        uint32_t x = valid;
+#pragma unroll
+        for (int b = 0; b < SH; ++b) x &= ((j >> b) & 1) ? plane[b] : ~plane[b];
+        mbits[(size_t)j * nwords + (i0 >> 5)] = x;
+        const uint32_t f = (cf[j] & 0xFFFFu) == 0u && x != 0u ? (uint32_t)i0 + __ffs(x) : 0u;
+        cf[j] += (__popc(x) << 16) + f;
+      }
+    }
+  }
+  uint64_t mx = 0ull;
+#pragma unroll
+  for (int j = 0; j < DP; ++j) {
+    base[j] = j < np ? (key[j] & 0x7FFFFFFFu) >> SH : 0xFFFFFFFFu;  // never-feasible: 0
+    if (j < np) mx = max(mx, (uint64_t)base[j]);
+  }
+  lb_out = mx;
+}
+
+// MODE 0: CTAs whose load bound admits packed keys; MODE 1: the others (u32 / u64 sums).  Both
+// kernels are launched; each computes the same per-CTA bound and leaves the other's CTAs alone,
+// so the common packed case runs with the packed kernel's smaller register footprint.
+template <int DP, bool STAGED, int MODE>
 __global__ void __launch_bounds__(kDispatchThreads)
     k_dispatch(const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ cost,
                int n_iter, int batch, int k_pad, const hyd_scheme* __restrict__ schemes,
@@ -174,25 +304,42 @@ __global__ void __launch_bounds__(kDispatchThreads)
                uint64_t* __restrict__ lb, hyd_pipe_stats* __restrict__ stats,
                uint32_t* __restrict__ members, uint32_t* __restrict__ status) {
   extern __shared__ __align__(16) uint32_t sm[];
-  // dynamic smem: [stage: tt*B*(1+k_pad) u32 if STAGED] [s_sum u64 columns]
-  const size_t stage_words = STAGED ? (size_t)tt * batch * (1 + k_pad) : 0;
+  // dynamic smem: [stage if STAGED] [s_sum u64 columns]; stage = [tt][B] lengths, then the
+  // costs: MODE 1 as global rows [tt][B][k_pad]; MODE 0 transposed [tt][k_pad][Bp], Bp = B | 1
+  constexpr bool TRANS = STAGED && MODE == 0;
+  const int B = batch;
+  const int Bp = B | 1;
+  const size_t stage_words = STAGED ? dispatch_stage_words(tt, B, k_pad) : 0;
   unsigned long long* s_sum = reinterpret_cast<unsigned long long*>(sm + ((stage_words + 3) & ~(size_t)3));
   __shared__ unsigned long long s_bound[kDispatchThreads / 32];
   __shared__ uint32_t s_ppmax;
-  const int B = batch;
   const int tid = threadIdx.x;
   const int c0 = blockIdx.x * ct, t0 = blockIdx.y * tt;
   const int ntt = min(tt, n_iter - t0);
   if (STAGED) {
-    // [tt][B] lengths then [tt][B][k_pad] costs, both contiguous in global memory per t
     const uint4* gl = reinterpret_cast<const uint4*>(sorted_len + (size_t)t0 * B);
     uint4* sl4 = reinterpret_cast<uint4*>(sm);
     const int nl = ntt * B / 4;
     for (int e = tid; e < nl; e += kDispatchThreads) sl4[e] = __ldg(gl + e);
     const uint4* gc = reinterpret_cast<const uint4*>(cost + (size_t)t0 * B * k_pad);
-    uint4* sc4 = reinterpret_cast<uint4*>(sm + (size_t)tt * B);
     const int nc = ntt * B * k_pad / 4;
-    for (int e = tid; e < nc; e += kDispatchThreads) sc4[e] = __ldg(gc + e);
+    if (TRANS) {
+      uint32_t* st = sm + (size_t)tt * B;
+      for (int e = tid; e < nc; e += kDispatchThreads) {
+        const uint4 v = __ldg(gc + e);
+        const int f = e * 4;  // flat index (lt * B + i) * k_pad + k, k % 4 == 0
+        const int row = f / k_pad, k = f - row * k_pad;
+        const int lt = row / B, i = row - lt * B;
+        uint32_t* d = st + ((size_t)lt * k_pad + k) * Bp + i;
+        d[0] = v.x;
+        d[Bp] = v.y;
+        d[2 * Bp] = v.z;
+        d[3 * Bp] = v.w;
+      }
+    } else {
+      uint4* sc4 = reinterpret_cast<uint4*>(sm + (size_t)tt * B);
+      for (int e = tid; e < nc; e += kDispatchThreads) sc4[e] = __ldg(gc + e);
+    }
   }
   if (tid == 0) {
     uint32_t m = 1u;
@@ -207,10 +354,15 @@ __global__ void __launch_bounds__(kDispatchThreads)
   unsigned long long bound = 0ull;
   for (int e = tid; e < ntt * B; e += kDispatchThreads) {
     const int lt = e / B, i = e - lt * B;
-    const uint32_t* crow = STAGED ? sm + (size_t)tt * B + ((size_t)lt * B + i) * k_pad
-                                  : cost + ((size_t)(t0 + lt) * B + i) * k_pad;
     uint32_t mx = 0u;
-    for (int k = 0; k < n_schemes; ++k) mx = max(mx, STAGED ? crow[k] : __ldg(crow + k));
+    if (TRANS) {
+      const uint32_t* col = sm + (size_t)tt * B + (size_t)lt * k_pad * Bp + i;
+      for (int k = 0; k < n_schemes; ++k) mx = max(mx, col[(size_t)k * Bp]);
+    } else {
+      const uint32_t* crow = STAGED ? sm + (size_t)tt * B + ((size_t)lt * B + i) * k_pad
+                                    : cost + ((size_t)(t0 + lt) * B + i) * k_pad;
+      for (int k = 0; k < n_schemes; ++k) mx = max(mx, STAGED ? crow[k] : __ldg(crow + k));
+    }
     unsigned long long v = (unsigned long long)mx;
     if (i == 0) v += (unsigned long long)mx * (s_ppmax - 1u);
     bound += v;
@@ -223,6 +375,7 @@ __global__ void __launch_bounds__(kDispatchThreads)
   const bool narrow = bound < 0xFFFFFFFFull;
   constexpr int SHK = DP <= 2 ? 1 : DP <= 4 ? 2 : DP <= 8 ? 3 : DP <= 16 ? 4 : 5;
   const bool packed = bound < (1ull << (31 - SHK));  // keys (load << SHK | j) stay below 2^31
+  if ((MODE == 0) != packed) return;  // the other kernel owns this CTA
 
   const int lt = tid / ct, lc = tid - lt * ct;
   const int c = c0 + lc, t = t0 + lt;
@@ -274,30 +427,61 @@ __global__ void __launch_bounds__(kDispatchThreads)
   unsigned long long* ssum = s_sum + tid;
   uint64_t lbv = 0ull;
   uint64_t base64[DP];
-  uint32_t cnt[DP], tmx[DP];
-  if (narrow) {
+  uint32_t cf[DP];
+  if constexpr (MODE == 0) {
+    const unsigned amask = __activemask();
+    const uint32_t* cst = TRANS ? sm + (size_t)tt * B + (size_t)lt * k_pad * Bp : cs;
     uint32_t base[DP];
-    dispatch_run<DP, uint32_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, ssum, mbits, np, nwords,
-                               lbv, base, cnt, tmx, packed);
+    packed_run<DP, TRANS>(sl, cst, B, TRANS ? Bp : k_pad, ml, pp, kk, prow, ssum, mbits, np, nwords,
+                          lbv, base, cf, amask);
 #pragma unroll
     for (int j = 0; j < DP; ++j) base64[j] = base[j];
   } else {
-    dispatch_run<DP, uint64_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, ssum, mbits, np, nwords,
-                               lbv, base64, cnt, tmx, false);
+    if (narrow) {
+      uint32_t base[DP];
+      dispatch_run<DP, uint32_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, ssum, mbits, np,
+                                        nwords, lbv, base, cf);
+#pragma unroll
+      for (int j = 0; j < DP; ++j) base64[j] = base[j];
+    } else {
+      dispatch_run<DP, uint64_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, ssum, mbits, np,
+                                        nwords, lbv, base64, cf);
+    }
   }
   lb[row] = lbv;
   hyd_pipe_stats* st = stats + srow * max_np;
 #pragma unroll
   for (int j = 0; j < DP; ++j) {
     if (j < np) {
+      const uint32_t first = cf[j] & 0xFFFFu;  // 0: no member
+      const uint32_t tm = !first ? 0u
+                          : TRANS ? sm[(size_t)tt * B + ((size_t)lt * k_pad + kk[j]) * Bp + first - 1u]
+                                  : cs[(size_t)(first - 1u) * k_pad + kk[j]];
       hyd_pipe_stats e;
-      e.u = cnt[j];
-      e.tau_max = tmx[j];
+      e.u = cf[j] >> 16;
+      e.tau_max = tm;
       e.s = ssum[j * kDispatchThreads];
-      e.sum_t = base64[j] - (uint64_t)tmx[j] * (pp[j] - 1u);  // base_j = C_j + E_j
+      e.sum_t = base64[j] - (uint64_t)tm * (pp[j] - 1u);  // base_j = C_j + E_j
       st[j] = e;
     }
   }
+}
+
+template <int DP, bool STAGED, int MODE>
+static cudaError_t launch_mode(dim3 grid, size_t smem, cudaStream_t s, const uint32_t* sorted_len,
+                               const uint32_t* cost, int n_iter, int batch, int k_pad,
+                               const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
+                               const uint8_t* cand_np, int n_cand, int max_np, int ct, int tt,
+                               uint8_t* pipe, uint64_t* lb, hyd_pipe_stats* stats, uint32_t* members,
+                               uint32_t* status) {
+  cudaError_t e = cudaFuncSetAttribute(k_dispatch<DP, STAGED, MODE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_dispatch<DP, STAGED, MODE><<<grid, kDispatchThreads, smem, s>>>(
+      sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct,
+      tt, pipe, lb, stats, members, status);
+  note_launch();
+  return cudaGetLastError();
 }
 
 template <int DP>
@@ -308,22 +492,18 @@ static cudaError_t launch_dp(bool staged, dim3 grid, size_t smem_stage, cudaStre
                              int ct, int tt, uint8_t* pipe, uint64_t* lb, hyd_pipe_stats* stats,
                              uint32_t* members, uint32_t* status) {
   const size_t cols = (size_t)DP * kDispatchThreads * 8;
+  const size_t smem = staged ? ((smem_stage + 15) & ~(size_t)15) + cols : cols;
   cudaError_t e;
   if (staged) {
-    const size_t smem = ((smem_stage + 15) & ~(size_t)15) + cols;
-    e = cudaFuncSetAttribute(k_dispatch<DP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    k_dispatch<DP, true><<<grid, kDispatchThreads, smem, s>>>(
-        sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np,
-        ct, tt, pipe, lb, stats, members, status);
+    e = launch_mode<DP, true, 0>(grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status);
+    if (e == cudaSuccess)
+      e = launch_mode<DP, true, 1>(grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status);
   } else {
-    e = cudaFuncSetAttribute(k_dispatch<DP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols);
-    if (e != cudaSuccess) return e;
-    k_dispatch<DP, false><<<grid, kDispatchThreads, cols, s>>>(
-        sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np,
-        ct, tt, pipe, lb, stats, members, status);
+    e = launch_mode<DP, false, 0>(grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status);
+    if (e == cudaSuccess)
+      e = launch_mode<DP, false, 1>(grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status);
   }
-  return cudaGetLastError();
+  return e;
 }
 
 int launch_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch,
@@ -333,7 +513,7 @@ int launch_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter
   if (n_iter == 0 || n_cand == 0) return HYD_OK;
   const int ct = n_cand < kDispatchThreads ? n_cand : kDispatchThreads;
   const int tt = kDispatchThreads / ct;
-  const size_t smem = (size_t)tt * batch * 4 * (1 + (size_t)k_pad);
+  const size_t smem = dispatch_stage_words(tt, batch, k_pad) * 4;
   const int dp = max_np <= 2 ? 2 : max_np <= 4 ? 4 : max_np <= 8 ? 8 : max_np <= 16 ? 16 : 32;
   const size_t static_smem = (size_t)dp * kDispatchThreads * 8 + 64;
   // stage when the rows fit comfortably (leaves room for several CTAs per SM)
@@ -347,7 +527,6 @@ int launch_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter
     case 16: e = launch_dp<16>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status); break;
     default: e = launch_dp<32>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status); break;
   }
-  note_launch();
   return e == cudaSuccess ? HYD_OK : record_cuda_error(e);
 }
 
