@@ -299,7 +299,7 @@ __device__ __forceinline__ void unit_start(LaneUnit<VM>& u, uint32_t V, uint32_t
   u.mx = 0;
 #pragma unroll
   for (int b = 0; b < VM; ++b) {
-    u.keys[b] = (uint32_t)b < V ? (uint32_t)b : 0xFFFFFFFFu;
+    u.keys[b] = (uint32_t)b < V ? (uint32_t)b : 0xFFFFFFFEu;  // unused: never fits, never 'mk'
     u.toks[b] = 0u;
   }
   u.qw = 0;
@@ -309,32 +309,36 @@ __device__ __forceinline__ void unit_start(LaneUnit<VM>& u, uint32_t V, uint32_t
 
 // Advance the unit by one sequence.  Returns 0 while running, 1 when the run completed,
 // 2 when it failed (no micro-batch fits: LPT(V) infeasible, or it cannot beat u.thr).
-template <int N, int VM>
-__device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords,
+// Straight-line apart from the membership-word refill: a lane whose current word is used up
+// takes the next one (an all-zero word costs it one idle step), and the step's placement is
+// predicated on having a member, so the warp never splits inside the bin arithmetic.
+// STAGED: lengths at sm[0, B), costs at sm[B + i * kp + k] (shared window, 32-bit addressing).
+template <int N, int VM, bool STAGED>
+__device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, int B,
                                          const uint32_t* __restrict__ slen,
-                                         const uint32_t* __restrict__ cst, int kp, uint64_t& ev) {
+                                         const uint32_t* __restrict__ cst, int kp, uint32_t& ev) {
+  extern __shared__ __align__(16) uint32_t sm[];
   constexpr int SH = LaneCfg<VM>::SH;
-  // next membership word (prefetched one ahead); a single-exit loop so the compiler places the
-  // reconvergence point right after it (an early return here splits the warp for the whole step)
-  while (u.cur == 0 && u.qw < nwords) {
+  if (u.cur == 0 && u.qw < nwords) {
     u.cur = u.nxtw;
     u.wbase = u.qw * 32u;
     ++u.qw;
     u.nxtw = u.qw < nwords ? __ldg(u.mw + u.qw) : 0u;
   }
-  __syncwarp(__activemask());
-  if (u.cur == 0) return 1;  // every member placed
-  const uint32_t i = u.wbase + (uint32_t)(__ffs(u.cur) - 1);
+  const bool valid = u.cur != 0u;
+  const uint32_t i = valid ? u.wbase + (uint32_t)(__ffs(u.cur) - 1) : 0u;
   u.cur &= u.cur - 1u;
-  const uint32_t l = slen[i];
-  const uint32_t tau = cst[(size_t)i * kp + u.k];
-  ev += u.V;
-  const uint32_t mk = argmin_keys<N, VM>(u.keys, u.toks, u.M - l);
-  if (mk >> 31) return 2;
+  const uint32_t l = STAGED ? sm[i] : slen[i];
+  const uint32_t tau = STAGED ? sm[B + i * kp + u.k] : cst[(size_t)i * kp + u.k];
+  const uint32_t m0 = argmin_keys<N, VM>(u.keys, u.toks, u.M - l);
+  const bool ok = valid && (m0 >> 31) == 0u;
+  const uint32_t mk = ok ? m0 : 0xFFFFFFFFu;  // matches no bin key: placement is a no-op
   place_key<N, VM>(u.keys, u.toks, mk, tau << SH, l);
-  u.mx = max(u.mx, (mk >> SH) + tau);
-  if (u.write) u.mrow[i] = (uint16_t)(mk & ((1u << SH) - 1u));
-  return u.mx > u.thr ? 2 : 0;
+  u.mx = ok ? max(u.mx, (mk >> SH) + tau) : u.mx;
+  if (u.write && ok) u.mrow[i] = (uint16_t)(mk & ((1u << SH) - 1u));
+  ev += valid ? u.V : 0u;
+  if (!valid) return u.qw >= nwords ? 1 : 0;  // every member placed / empty word
+  return (!ok || u.mx > u.thr) ? 2 : 0;
 }
 
 // VM = 16: every (c,t,j) of the tile, classes 8 / 16; a task needing some V > 16 is flagged
@@ -510,7 +514,7 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
   const uint32_t* cst = STAGED ? sm + B : a.cost + (size_t)t * B * kp;
 
   LaneUnit<VM> u;
-  uint64_t ev = 0;
+  uint32_t ev = 0;
   auto load_unit = [&](int r, uint32_t V, uint32_t thr, bool write) {
     const int e = (int)R.eid[r];
     const int c = c0 + e / mnp;
@@ -543,8 +547,8 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
         int st = 0;
 #pragma unroll 1
         for (int e = 0; e < kLaneEpoch && st == 0; ++e) {
-          if (VM == 16 && narrow) st = unit_step<8, VM>(u, nwords, slen, cst, kp, ev);
-          else st = unit_step<VM, VM>(u, nwords, slen, cst, kp, ev);
+          if (VM == 16 && narrow) st = unit_step<8, VM, STAGED>(u, nwords, B, slen, cst, kp, ev);
+          else st = unit_step<VM, VM, STAGED>(u, nwords, B, slen, cst, kp, ev);
         }
         if (st) have = finish(st);  // finish may load a follow-up unit into this lane
       }
@@ -755,9 +759,7 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
     a.ptime[row * HYD_MAX_PIPES + j] = key >> 16;
     atomicMax(reinterpret_cast<unsigned long long*>(a.makespan + (size_t)t * a.n_cand + c), key >> 16);
   }
-  __syncwarp();
-  ev = __reduce_add_sync(HYD_FULL, (uint32_t)min(ev, (uint64_t)0xFFFFFFFFull));
-  if (lane == 0 && ev) atomicAdd(a.evals, (unsigned long long)ev);
+  if (ev) atomicAdd(a.evals, (unsigned long long)ev);
 }
 
 // ------------------------------------------------------------------ LPT, one warp per pipeline
