@@ -17,18 +17,19 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SRC = os.path.join(_HERE, "hydref.c")
+_SRCS = [os.path.join(_HERE, "hydref.c"), os.path.join(_HERE, "alg1ref.c")]
 _HDR = os.path.join(_HERE, "hydref.h")
 _LIB = os.path.join(_HERE, "libhydref.so")
 
 
 def build(force: bool = False) -> str:
     """Compile oracle/libhydref.so with gcc (idempotent)."""
-    stale = not os.path.exists(_LIB) or max(os.path.getmtime(_SRC), os.path.getmtime(_HDR)) > os.path.getmtime(_LIB)
+    newest = max(os.path.getmtime(f) for f in _SRCS + [_HDR])
+    stale = not os.path.exists(_LIB) or newest > os.path.getmtime(_LIB)
     if force or stale:
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(
-            ["gcc", "-std=gnu11", "-O2", "-g", "-Wall", "-Wextra", "-shared", "-fPIC", "-pthread", _SRC, "-o", tmp]
+            ["gcc", "-std=gnu11", "-O2", "-g", "-Wall", "-Wextra", "-shared", "-fPIC", "-pthread", *_SRCS, "-o", tmp]
         )
         os.replace(tmp, _LIB)
     return _LIB
@@ -74,6 +75,24 @@ def lib():
         L.hydref_assign_pairs.argtypes = [
             _u32p, _u32p, I, I, I, _voidp, _u8p, _u8p, _i32p, _i32p, I,
             _u8p, _u64p, _u16p, _u16p, _u64p, _u64p, U32P, I,
+        ]
+        # NEXT-1 (alg1ref.c)
+        U64 = C.c_uint64
+        L.hydref_philox4x32_10.argtypes = [_u32p, _u32p, _u32p]
+        L.hydref_alg1_permutation.argtypes = [U64, I, I, I, _u32p]
+        L.hydref_alg1_trial.argtypes = [_u32p, _u32p, I, I, _voidp, _u8p, I, _u32p, _u8p]
+        L.hydref_alg1_trial.restype = U64
+        L.hydref_alg1_dispatch.argtypes = [
+            _u32p, _u32p, I, I, _voidp, _u8p, I, U64, I, I, _u8p, C.POINTER(U64), C.POINTER(C.c_int32),
+        ]
+        L.hydref_alg1_dispatch.restype = I
+        L.hydref_assign_batch_ex.argtypes = [
+            _u32p, I, I, _voidp, I, I, _u8p, _u8p, I, I, I, U64, _u32p, _u32p, _u32p,
+            _u8p, _u64p, _u16p, _u16p, _u64p, _u64p, _i64p, _i32p, U32P, I,
+        ]
+        L.hydref_assign_pairs_ex.argtypes = [
+            _u32p, _u32p, I, I, I, _voidp, _u8p, _u8p, _i32p, _i32p, I, I, U64,
+            _u8p, _u64p, _u16p, _u16p, _u64p, _u64p, _i32p, U32P, I,
         ]
         _lib = L
     return _lib
@@ -149,8 +168,11 @@ def select(makespan, cand_offset=0):
     return int(k), int(st.value)
 
 
-def assign_batch(W, n_threads=0, cand_offset=0):
-    """All outputs of steps 1-7 for a ``workload.Workload``; dict of numpy arrays."""
+def assign_batch(W, n_threads=0, cand_offset=0, trials=0, seed=0):
+    """All outputs of steps 1-7 for a ``workload.Workload``; dict of numpy arrays.
+
+    ``trials`` > 0 replaces the HYD-H1 dispatch by Alg. 1 with that many random trials
+    (NEXT-1, seeded by ``seed``); ``best_trial`` [C][It] is then part of the result."""
     It, B, Cn, kp = W.n_iter, W.batch, W.n_cand, W.k_pad
     o = dict(
         sorted_len=np.empty((It, B), np.uint32),
@@ -163,15 +185,18 @@ def assign_batch(W, n_threads=0, cand_offset=0):
         ptime=np.empty((Cn, It, 32), np.uint64),
         makespan=np.empty((It, Cn), np.uint64),
         key=np.empty(It, np.int64),
+        best_trial=np.full((Cn, It), -1, np.int32),
     )
     st = C.c_uint32(0)
-    lib().hydref_assign_batch(
+    lib().hydref_assign_batch_ex(
         np.ascontiguousarray(W.lengths, np.uint32), It, B, _sch_ptr(W.schemes), W.n_schemes, kp,
-        np.ascontiguousarray(W.cand), np.ascontiguousarray(W.cand_np), Cn, int(cand_offset),
-        o["sorted_len"], o["perm"], o["cost"], o["pipe"], o["lb"], o["mb"], o["v"], o["ptime"],
-        o["makespan"], o["key"], C.byref(st), int(n_threads),
+        np.ascontiguousarray(W.cand), np.ascontiguousarray(W.cand_np), Cn, int(cand_offset), int(trials),
+        int(seed), o["sorted_len"], o["perm"], o["cost"], o["pipe"], o["lb"], o["mb"], o["v"], o["ptime"],
+        o["makespan"], o["key"], o["best_trial"], C.byref(st), int(n_threads),
     )
     o["status"] = int(st.value)
+    if not trials:
+        del o["best_trial"]
     return o
 
 
@@ -192,8 +217,8 @@ def cost_tables(W):
     return s, p, cst, status
 
 
-def assign_pairs(W, pairs_c, pairs_t, tables=None, n_threads=0):
-    """Outputs for selected (c,t) pairs only; rows indexed by pair."""
+def assign_pairs(W, pairs_c, pairs_t, tables=None, n_threads=0, trials=0, seed=0):
+    """Outputs for selected (c,t) pairs only; rows indexed by pair (``trials`` as assign_batch)."""
     if tables is None:
         tables = cost_tables(W)
     s, _, cst, status = tables
@@ -207,12 +232,56 @@ def assign_pairs(W, pairs_c, pairs_t, tables=None, n_threads=0):
         v=np.empty((n, 32), np.uint16),
         ptime=np.empty((n, 32), np.uint64),
         makespan=np.empty(n, np.uint64),
+        best_trial=np.full(n, -1, np.int32),
     )
     st = C.c_uint32(0)
-    lib().hydref_assign_pairs(
+    lib().hydref_assign_pairs_ex(
         s, cst.reshape(-1), W.n_iter, B, W.k_pad, _sch_ptr(W.schemes), np.ascontiguousarray(W.cand),
-        np.ascontiguousarray(W.cand_np), pc, pt, n, o["pipe"], o["lb"], o["mb"], o["v"], o["ptime"],
-        o["makespan"], C.byref(st), int(n_threads),
+        np.ascontiguousarray(W.cand_np), pc, pt, n, int(trials), int(seed), o["pipe"], o["lb"], o["mb"],
+        o["v"], o["ptime"], o["makespan"], o["best_trial"], C.byref(st), int(n_threads),
     )
     o["status"] = status | int(st.value)
+    if not trials:
+        del o["best_trial"]
     return o
+
+
+# ------------------------------------------------------------------ NEXT-1 (alg1ref.c)
+def philox4x32_10(ctr, key):
+    c = np.ascontiguousarray(ctr, np.uint32)
+    k = np.ascontiguousarray(key, np.uint32)
+    out = np.empty(4, np.uint32)
+    lib().hydref_philox4x32_10(c, k, out)
+    return out
+
+
+def alg1_permutation(seed, t, trial, batch):
+    order = np.empty(max(batch, 1), np.uint32)
+    lib().hydref_alg1_permutation(int(seed), int(t), int(trial), int(batch), order)
+    return order[:batch]
+
+
+def alg1_trial(sorted_len, cost_tab, schemes, cand_row, order):
+    B, k_pad = cost_tab.shape
+    row = np.full(32, 0xFF, np.uint8)
+    row[: len(cand_row)] = cand_row
+    pipe = np.empty(B, np.uint8)
+    o = lib().hydref_alg1_trial(
+        np.ascontiguousarray(sorted_len, np.uint32), np.ascontiguousarray(cost_tab, np.uint32).ravel(), B, k_pad,
+        _sch_ptr(schemes), row, len(cand_row), np.ascontiguousarray(order, np.uint32), pipe,
+    )
+    return int(o), pipe
+
+
+def alg1_dispatch(sorted_len, cost_tab, schemes, cand_row, seed, t, trials):
+    B, k_pad = cost_tab.shape
+    row = np.full(32, 0xFF, np.uint8)
+    row[: len(cand_row)] = cand_row
+    pipe = np.empty(B, np.uint8)
+    lb = C.c_uint64(0)
+    bt = C.c_int32(0)
+    ok = lib().hydref_alg1_dispatch(
+        np.ascontiguousarray(sorted_len, np.uint32), np.ascontiguousarray(cost_tab, np.uint32).ravel(), B, k_pad,
+        _sch_ptr(schemes), row, len(cand_row), int(seed), int(t), int(trials), pipe, C.byref(lb), C.byref(bt),
+    )
+    return bool(ok), pipe, int(lb.value), int(bt.value)

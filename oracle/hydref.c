@@ -241,19 +241,13 @@ void hydref_pack_pipeline(const uint32_t* ell, const uint32_t* tau, int u, const
   }
 }
 
-/* ---------------------------------------------------------------- steps 4-6 for one (c,t) */
-uint64_t hydref_assign_pair(const uint32_t* sorted, const uint32_t* cost, int batch, int k_pad,
-                            const hydref_scheme* schemes, const uint8_t* cand_row, int np,
-                            uint8_t* pipe, uint64_t* lb, uint16_t* mb, uint16_t* v, uint64_t* ptime,
-                            uint32_t* status) {
-  for (int j = 0; j < 32; ++j) {
-    v[j] = 0;
-    ptime[j] = 0;
-  }
-  if (!hydref_dispatch(sorted, cost, batch, k_pad, schemes, cand_row, np, pipe, lb)) {
-    for (int i = 0; i < batch; ++i) mb[i] = 0xFFFF;
-    return UINT64_MAX;
-  }
+/* ---------------------------------------------------------------- steps 5-6 for one (c,t)
+ * Given a stage-1 assignment pipe[B] (sorted positions), pack every pipeline (step 5) and
+ * return the makespan max_j ptime_j (step 6). */
+uint64_t hydref_pack_pair(const uint32_t* sorted, const uint32_t* cost, int batch, int k_pad,
+                          const hydref_scheme* schemes, const uint8_t* cand_row, int np,
+                          const uint8_t* pipe, uint16_t* mb, uint16_t* v, uint64_t* ptime,
+                          uint32_t* status) {
   uint32_t* ell = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(batch > 0 ? batch : 1));
   uint32_t* tau = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(batch > 0 ? batch : 1));
   int* pos = (int*)malloc(sizeof(int) * (size_t)(batch > 0 ? batch : 1));
@@ -277,6 +271,23 @@ uint64_t hydref_assign_pair(const uint32_t* sorted, const uint32_t* cost, int ba
   free(pos);
   free(mbq);
   return makespan;
+}
+
+/* ---------------------------------------------------------------- steps 4-6 for one (c,t) */
+uint64_t hydref_assign_pair(const uint32_t* sorted, const uint32_t* cost, int batch, int k_pad,
+                            const hydref_scheme* schemes, const uint8_t* cand_row, int np,
+                            uint8_t* pipe, uint64_t* lb, uint16_t* mb, uint16_t* v, uint64_t* ptime,
+                            uint32_t* status) {
+  for (int j = 0; j < 32; ++j) {
+    v[j] = 0;
+    ptime[j] = 0;
+  }
+  if (!hydref_dispatch(sorted, cost, batch, k_pad, schemes, cand_row, np, pipe, lb)) {
+    for (int i = 0; i < batch; ++i) mb[i] = 0xFFFF;
+    return UINT64_MAX;
+  }
+  return hydref_pack_pair(sorted, cost, batch, k_pad, schemes, cand_row, np, pipe, mb, v, ptime,
+                          status);
 }
 
 /* ---------------------------------------------------------------- step 7: select
@@ -317,33 +328,44 @@ typedef struct {
   uint16_t* v;
   uint64_t* ptime;
   uint64_t* makespan;
+  int trials;         /* > 0: stage 1 is Alg. 1 with this many random trials (NEXT-1) */
+  uint64_t seed;
+  int32_t* best_trial; /* [C][It] (batch) or [n_pairs] (pairs) when trials > 0 */
   int tid, nthreads;
   uint32_t status;
 } job;
+
+static uint64_t job_pair(job* J, int c, int t, size_t orow, int32_t* best) {
+  const uint32_t* sorted = J->sorted + (size_t)t * J->batch;
+  const uint32_t* cost = J->cost + (size_t)t * J->batch * J->k_pad;
+  if (J->trials > 0)
+    return hydref_alg1_assign_pair(sorted, cost, J->batch, J->k_pad, J->schemes,
+                                   J->cand + (size_t)c * 32, J->cand_np[c], J->seed, t, J->trials,
+                                   J->pipe + orow * J->batch, J->lb + orow,
+                                   J->mb + orow * J->batch, J->v + orow * 32,
+                                   J->ptime + orow * 32, best, &J->status);
+  return hydref_assign_pair(sorted, cost, J->batch, J->k_pad, J->schemes, J->cand + (size_t)c * 32,
+                            J->cand_np[c], J->pipe + orow * J->batch, J->lb + orow,
+                            J->mb + orow * J->batch, J->v + orow * 32, J->ptime + orow * 32,
+                            &J->status);
+}
 
 static void* batch_worker(void* arg) {
   job* J = (job*)arg;
   for (int c = J->tid; c < J->n_cand; c += J->nthreads)
     for (int t = 0; t < J->n_iter; ++t) {
       size_t row = (size_t)c * J->n_iter + t;
-      J->makespan[(size_t)t * J->n_cand + c] = hydref_assign_pair(
-          J->sorted + (size_t)t * J->batch, J->cost + (size_t)t * J->batch * J->k_pad, J->batch,
-          J->k_pad, J->schemes, J->cand + (size_t)c * 32, J->cand_np[c], J->pipe + row * J->batch,
-          J->lb + row, J->mb + row * J->batch, J->v + row * 32, J->ptime + row * 32, &J->status);
+      J->makespan[(size_t)t * J->n_cand + c] =
+          job_pair(J, c, t, row, J->best_trial ? J->best_trial + row : NULL);
     }
   return NULL;
 }
 
 static void* pairs_worker(void* arg) {
   job* J = (job*)arg;
-  for (int p = J->tid; p < J->n_pairs; p += J->nthreads) {
-    int c = J->pair_c[p], t = J->pair_t[p];
-    J->makespan[p] = hydref_assign_pair(
-        J->sorted + (size_t)t * J->batch, J->cost + (size_t)t * J->batch * J->k_pad, J->batch,
-        J->k_pad, J->schemes, J->cand + (size_t)c * 32, J->cand_np[c],
-        J->pipe + (size_t)p * J->batch, J->lb + p, J->mb + (size_t)p * J->batch, J->v + (size_t)p * 32,
-        J->ptime + (size_t)p * 32, &J->status);
-  }
+  for (int p = J->tid; p < J->n_pairs; p += J->nthreads)
+    J->makespan[p] =
+        job_pair(J, J->pair_c[p], J->pair_t[p], (size_t)p, J->best_trial ? J->best_trial + p : NULL);
   return NULL;
 }
 
@@ -379,6 +401,18 @@ void hydref_assign_batch(const uint32_t* len, int n_iter, int batch, const hydre
                          uint32_t* cost, uint8_t* pipe, uint64_t* lb, uint16_t* mb, uint16_t* v,
                          uint64_t* ptime, uint64_t* makespan, int64_t* key, uint32_t* status,
                          int n_threads) {
+  hydref_assign_batch_ex(len, n_iter, batch, schemes, n_schemes, k_pad, cand, cand_np, n_cand,
+                         cand_offset, 0, 0, sorted, perm, cost, pipe, lb, mb, v, ptime, makespan,
+                         key, NULL, status, n_threads);
+}
+
+void hydref_assign_batch_ex(const uint32_t* len, int n_iter, int batch,
+                            const hydref_scheme* schemes, int n_schemes, int k_pad,
+                            const uint8_t* cand, const uint8_t* cand_np, int n_cand,
+                            int cand_offset, int trials, uint64_t seed, uint32_t* sorted,
+                            uint32_t* perm, uint32_t* cost, uint8_t* pipe, uint64_t* lb,
+                            uint16_t* mb, uint16_t* v, uint64_t* ptime, uint64_t* makespan,
+                            int64_t* key, int32_t* best_trial, uint32_t* status, int n_threads) {
   for (int t = 0; t < n_iter; ++t)
     hydref_cost_table(len + (size_t)t * batch, batch, schemes, n_schemes, k_pad,
                       sorted + (size_t)t * batch, perm + (size_t)t * batch,
@@ -400,6 +434,9 @@ void hydref_assign_batch(const uint32_t* len, int n_iter, int batch, const hydre
   proto.v = v;
   proto.ptime = ptime;
   proto.makespan = makespan;
+  proto.trials = trials;
+  proto.seed = seed;
+  proto.best_trial = best_trial;
   int nt = resolve_threads(n_threads);
   if (nt > n_cand) nt = n_cand > 0 ? n_cand : 1;
   *status |= run_jobs(&proto, nt, batch_worker);
@@ -412,6 +449,17 @@ void hydref_assign_pairs(const uint32_t* sorted, const uint32_t* cost, int n_ite
                          const uint8_t* cand_np, const int32_t* pair_c, const int32_t* pair_t,
                          int n_pairs, uint8_t* pipe, uint64_t* lb, uint16_t* mb, uint16_t* v,
                          uint64_t* ptime, uint64_t* makespan, uint32_t* status, int n_threads) {
+  hydref_assign_pairs_ex(sorted, cost, n_iter, batch, k_pad, schemes, cand, cand_np, pair_c,
+                         pair_t, n_pairs, 0, 0, pipe, lb, mb, v, ptime, makespan, NULL, status,
+                         n_threads);
+}
+
+void hydref_assign_pairs_ex(const uint32_t* sorted, const uint32_t* cost, int n_iter, int batch,
+                            int k_pad, const hydref_scheme* schemes, const uint8_t* cand,
+                            const uint8_t* cand_np, const int32_t* pair_c, const int32_t* pair_t,
+                            int n_pairs, int trials, uint64_t seed, uint8_t* pipe, uint64_t* lb,
+                            uint16_t* mb, uint16_t* v, uint64_t* ptime, uint64_t* makespan,
+                            int32_t* best_trial, uint32_t* status, int n_threads) {
   job proto;
   memset(&proto, 0, sizeof(proto));
   proto.sorted = sorted;
@@ -431,6 +479,9 @@ void hydref_assign_pairs(const uint32_t* sorted, const uint32_t* cost, int n_ite
   proto.v = v;
   proto.ptime = ptime;
   proto.makespan = makespan;
+  proto.trials = trials;
+  proto.seed = seed;
+  proto.best_trial = best_trial;
   int nt = resolve_threads(n_threads);
   if (nt > n_pairs) nt = n_pairs > 0 ? n_pairs : 1;
   *status |= run_jobs(&proto, nt, pairs_worker);

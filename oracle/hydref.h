@@ -61,6 +61,13 @@ int hydref_lpt(const uint32_t* ell, const uint32_t* tau, int u, int v, uint32_t 
 void hydref_pack_pipeline(const uint32_t* ell, const uint32_t* tau, int u, const hydref_scheme* s,
                           uint16_t* v_out, uint64_t* ptime_out, uint16_t* mb_q, uint32_t* status);
 
+/* Steps 5-6 for one (c,t) given its stage-1 assignment pipe[B]: pack every pipeline,
+ * return the makespan. */
+uint64_t hydref_pack_pair(const uint32_t* sorted, const uint32_t* cost, int batch, int k_pad,
+                          const hydref_scheme* schemes, const uint8_t* cand_row, int np,
+                          const uint8_t* pipe, uint16_t* mb, uint16_t* v, uint64_t* ptime,
+                          uint32_t* status);
+
 /* Steps 4-6 for one (c,t): dispatch, pack every pipeline, makespan.  Outputs are
  * rows: pipe[B], mb[B], v[32], ptime[32]; returns makespan (UINT64_MAX if infeasible). */
 uint64_t hydref_assign_pair(const uint32_t* sorted, const uint32_t* cost, int batch, int k_pad,
@@ -88,6 +95,56 @@ void hydref_assign_pairs(const uint32_t* sorted, const uint32_t* cost, int n_ite
                          const uint8_t* cand_np, const int32_t* pair_c, const int32_t* pair_t,
                          int n_pairs, uint8_t* pipe, uint64_t* lb, uint16_t* mb, uint16_t* v,
                          uint64_t* ptime, uint64_t* makespan, uint32_t* status, int n_threads);
+
+/* ------------------------------------------------------------------ NEXT-1 (alg1ref.c)
+ * Paper-faithful Alg. 1: T random-permutation trials, best by (O, trial). */
+
+/* Philox4x32-10 (Salmon et al., SC'11): 10 rounds of the Philox S-P network on a 128-bit
+ * counter under a 64-bit key. */
+void hydref_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+
+/* Trial permutation of the B sorted positions for (seed, iteration t, trial): Fisher-Yates
+ * (Durstenfeld), for k = B-1 down to 1: r = Philox(ctr = (k / 4, t, trial, 0),
+ * key = (seed lo, seed hi))[k % 4], j = (r * (k + 1)) >> 32, swap(order[k], order[j]).
+ * DESIGN.md reading 21: one permutation per (t, trial), shared by every candidate. */
+void hydref_alg1_permutation(uint64_t seed, int t, int trial, int batch, uint32_t* order);
+
+/* One trial: Alg. 1 lines 3-14 over the sequences in `order` (sorted positions).  Writes
+ * pipe[i] for each sorted position i; returns O_trial = max_j (C_j + E_j) (line 15). */
+uint64_t hydref_alg1_trial(const uint32_t* sorted, const uint32_t* cost, int batch, int k_pad,
+                           const hydref_scheme* schemes, const uint8_t* cand_row, int np,
+                           const uint32_t* order, uint8_t* pipe);
+
+/* Alg. 1 with T = trials: the trial with the smallest (O_trial, trial) wins (lines 16-17,
+ * strict <).  Returns 1 if feasible (pipe, lb = O_best, *best_trial), 0 if the candidate
+ * cannot hold sorted[0] (pipe = 0xFF.., lb = UINT64_MAX, *best_trial = -1). */
+int hydref_alg1_dispatch(const uint32_t* sorted, const uint32_t* cost, int batch, int k_pad,
+                         const hydref_scheme* schemes, const uint8_t* cand_row, int np,
+                         uint64_t seed, int t, int trials, uint8_t* pipe, uint64_t* lb,
+                         int32_t* best_trial);
+
+/* Steps 4-6 with Alg. 1 as stage 1 (best_trial may be NULL). */
+uint64_t hydref_alg1_assign_pair(const uint32_t* sorted, const uint32_t* cost, int batch,
+                                 int k_pad, const hydref_scheme* schemes, const uint8_t* cand_row,
+                                 int np, uint64_t seed, int t, int trials, uint8_t* pipe,
+                                 uint64_t* lb, uint16_t* mb, uint16_t* v, uint64_t* ptime,
+                                 int32_t* best_trial, uint32_t* status);
+
+/* Batch / pairs drivers with a stage-1 choice: trials = 0 -> HYD-H1 dispatch, else Alg. 1
+ * with that many trials; best_trial [C][It] / [n_pairs] may be NULL. */
+void hydref_assign_batch_ex(const uint32_t* len, int n_iter, int batch,
+                            const hydref_scheme* schemes, int n_schemes, int k_pad,
+                            const uint8_t* cand, const uint8_t* cand_np, int n_cand,
+                            int cand_offset, int trials, uint64_t seed, uint32_t* sorted,
+                            uint32_t* perm, uint32_t* cost, uint8_t* pipe, uint64_t* lb,
+                            uint16_t* mb, uint16_t* v, uint64_t* ptime, uint64_t* makespan,
+                            int64_t* key, int32_t* best_trial, uint32_t* status, int n_threads);
+void hydref_assign_pairs_ex(const uint32_t* sorted, const uint32_t* cost, int n_iter, int batch,
+                            int k_pad, const hydref_scheme* schemes, const uint8_t* cand,
+                            const uint8_t* cand_np, const int32_t* pair_c, const int32_t* pair_t,
+                            int n_pairs, int trials, uint64_t seed, uint8_t* pipe, uint64_t* lb,
+                            uint16_t* mb, uint16_t* v, uint64_t* ptime, uint64_t* makespan,
+                            int32_t* best_trial, uint32_t* status, int n_threads);
 
 #ifdef __cplusplus
 }

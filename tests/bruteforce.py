@@ -135,3 +135,18 @@ def makespan_opt_identical(costs, m):
             loads[a] += c
         best = min(best, max(loads))
     return best
+
+
+def eq3_opt(lengths, schemes, cand_row):
+    """Eq. 3 optimum: min over every dispatch respecting MaxLen of
+    max_j LowerBound_j (Eq. 2), by enumeration of all D^B assignments."""
+    D = len(cand_row)
+    sch = [schemes[k] for k in cand_row]
+    B = len(lengths)
+    best = float("inf")
+    for assign in itertools.product(range(D), repeat=B):
+        if any(lengths[i] > int(sch[assign[i]]["max_len"]) for i in range(B)):
+            continue
+        o = max(lower_bound([lengths[i] for i in range(B) if assign[i] == j], sch[j]) for j in range(D))
+        best = min(best, o)
+    return best

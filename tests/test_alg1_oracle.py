@@ -1,0 +1,185 @@
+"""Pins of the NEXT-1 oracle (oracle/alg1ref.c): the paper's randomized greedy dispatcher,
+Alg. 1, against facts that do not come from the oracle itself.
+
+* Philox4x32-10: the published known-answer vectors (tests/golden/philox4x32_10_kat.json).
+* The trial permutation (reading 21): a permutation; uniform over S_3.
+* One trial: a literal Python transcription of the pseudo-code (dispatch matrix m_ij, l_max
+  as the max over m_ij * l_i, E' through the closed-form cost App. C.2, O_max as the
+  max over every other pipeline, strict < so the first j wins).
+* Objective: O_trial equals Eq. 2/3 recomputed from the returned assignment;
+  the one-pipeline closed form; O_best >= the exhaustive Eq. 3 optimum; the paper's
+  "within 10% of the optimum" claim on tiny heterogeneous instances.
+* Trials: O_best(T) = min over the first T trials, non-increasing in T, ties to the lower
+  trial index (P:1149 strict <).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workload as w
+from tests import bruteforce as bf
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def tables(W, t=0):
+    s, _, cst, st = oracle.cost_table(W.lengths[t], W.schemes, W.k_pad)
+    assert st == 0
+    return s, cst
+
+
+def test_philox_known_answers():
+    kat = json.load(open(os.path.join(GOLD, "philox4x32_10_kat.json")))
+    assert len(kat["vectors"]) == 3
+    for v in kat["vectors"]:
+        ctr = [int(x, 16) for x in v["ctr"]]
+        key = [int(x, 16) for x in v["key"]]
+        out = oracle.philox4x32_10(ctr, key)
+        assert [int(x) for x in out] == [int(x, 16) for x in v["out"]]
+
+
+@pytest.mark.parametrize("B", [1, 2, 5, 32, 33, 512])
+def test_permutation_is_a_permutation(B):
+    for trial in range(4):
+        p = oracle.alg1_permutation(12345, 7, trial, B)
+        assert sorted(p.tolist()) == list(range(B))
+
+
+def test_permutation_uniform_on_s3():
+    # 6 equally likely orders: 6000 draws, each count within 5 sigma of 1000
+    counts = {}
+    for trial in range(6000):
+        p = tuple(oracle.alg1_permutation(99, trial // 256, trial % 256, 3).tolist())
+        counts[p] = counts.get(p, 0) + 1
+    assert len(counts) == 6
+    sigma = (6000 * (1 / 6) * (5 / 6)) ** 0.5
+    assert all(abs(c - 1000) < 5 * sigma for c in counts.values()), counts
+
+
+def test_permutation_depends_on_every_key_part():
+    base = oracle.alg1_permutation(1, 2, 3, 64).tolist()
+    assert oracle.alg1_permutation(2, 2, 3, 64).tolist() != base
+    assert oracle.alg1_permutation(1, 3, 3, 64).tolist() != base
+    assert oracle.alg1_permutation(1, 2, 4, 64).tolist() != base
+    assert oracle.alg1_permutation(1 << 40, 2, 3, 64).tolist() != oracle.alg1_permutation(0, 2, 3, 64).tolist()
+
+
+def alg1_trial_literal(sorted_len, schemes, cand_row, order):
+    """Alg. 1 lines 3-15, transcribed literally."""
+    D, B = len(cand_row), len(sorted_len)
+    P = [schemes[k] for k in cand_row]
+    C = [0] * D
+    E = [0] * D
+    m = [[0] * D for _ in range(B)]
+    for i in order:  # line 4-5: i <- pi_k
+        li = int(sorted_len[i])
+        o_min, jstar, cs, es = None, -1, 0, 0
+        J = [j for j in range(D) if int(P[j]["max_len"]) >= li]  # J_i
+        for j in J:  # line 6
+            lmax = max([li] + [m[q][j] * int(sorted_len[q]) for q in range(B)])  # line 7
+            cj = C[j] + bf.T(P[j], li)  # line 8
+            ej = bf.T(P[j], lmax) * (int(P[j]["pp"]) - 1)  # line 9
+            o_max = max([cj + ej] + [C[k] + E[k] for k in range(D) if k != j])  # line 10
+            if o_min is None or o_max < o_min:  # line 11-12
+                o_min, jstar, cs, es = o_max, j, cj, ej
+        m[i][jstar] = 1  # line 13
+        C[jstar], E[jstar] = cs, es
+    pipe = [next(j for j in range(D) if m[i][j]) for i in range(B)]
+    return max(C[j] + E[j] for j in range(D)), pipe  # line 15
+
+
+def test_trial_matches_literal_transcription():
+    rng = np.random.default_rng(2024)
+    n = 0
+    for _ in range(150):
+        B = int(rng.integers(1, 13))
+        D = int(rng.integers(1, 5))
+        W = w.random_small_instance(rng, B, D, K=4)
+        s, cst = tables(W)
+        row = [int(k) for k in W.cand[0, : W.cand_np[0]]]
+        order = rng.permutation(B).astype(np.uint32)
+        o, pipe = oracle.alg1_trial(s, cst, W.schemes, row, order)
+        o_ref, pipe_ref = alg1_trial_literal(s, W.schemes, row, order.tolist())
+        assert o == o_ref
+        assert pipe.tolist() == pipe_ref
+        n += 1
+    assert n == 150
+
+
+def test_trial_objective_is_eq3_of_its_assignment():
+    rng = np.random.default_rng(7)
+    for _ in range(60):
+        W = w.random_small_instance(rng, int(rng.integers(2, 40)), int(rng.integers(1, 6)), K=5)
+        s, cst = tables(W)
+        row = [int(k) for k in W.cand[0, : W.cand_np[0]]]
+        order = oracle.alg1_permutation(5, 0, int(rng.integers(0, 100)), W.batch)
+        o, pipe = oracle.alg1_trial(s, cst, W.schemes, row, order)
+        groups = [[int(s[i]) for i in range(W.batch) if pipe[i] == j] for j in range(len(row))]
+        for j, g in enumerate(groups):  # MaxLen respected
+            assert all(l <= int(W.schemes[row[j]]["max_len"]) for l in g)
+        assert o == max(bf.lower_bound(g, W.schemes[row[j]]) for j, g in enumerate(groups))
+
+
+def test_single_pipeline_closed_form():
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        W = w.random_small_instance(rng, int(rng.integers(1, 30)), 1)
+        s, cst = tables(W)
+        row = [int(W.cand[0, 0])]
+        ok, pipe, lb, bt = oracle.alg1_dispatch(s, cst, W.schemes, row, 11, 0, 5)
+        assert ok and bt == 0 and (pipe == 0).all()  # every trial ties: the first is kept
+        assert lb == bf.lower_bound([int(x) for x in s], W.schemes[row[0]])
+
+
+def test_best_trial_is_min_over_trials_and_monotone():
+    rng = np.random.default_rng(11)
+    for _ in range(12):
+        W = w.random_small_instance(rng, int(rng.integers(5, 30)), int(rng.integers(2, 5)), K=4)
+        s, cst = tables(W)
+        row = [int(k) for k in W.cand[0, : W.cand_np[0]]]
+        per_trial = []
+        for trial in range(16):
+            order = oracle.alg1_permutation(77, 3, trial, W.batch)
+            per_trial.append(oracle.alg1_trial(s, cst, W.schemes, row, order))
+        prev = None
+        for T in (1, 2, 5, 16):
+            ok, pipe, lb, bt = oracle.alg1_dispatch(s, cst, W.schemes, row, 77, 3, T)
+            objs = [o for o, _ in per_trial[:T]]
+            assert ok and lb == min(objs) and bt == objs.index(min(objs))
+            assert pipe.tolist() == per_trial[bt][1].tolist()
+            if prev is not None:
+                assert lb <= prev
+            prev = lb
+
+
+def test_infeasible_candidate():
+    W = w.random_small_instance(np.random.default_rng(5), 6, 2)
+    s, cst = tables(W)
+    row = [int(k) for k in W.cand[0, : W.cand_np[0]]]
+    s2 = s.copy()
+    s2[0] = int(W.schemes[row[0]]["max_len"]) + 1
+    ok, pipe, lb, bt = oracle.alg1_dispatch(s2, cst, W.schemes, row, 1, 0, 4)
+    assert not ok and (pipe == 0xFF).all() and lb == 2**64 - 1 and bt == -1
+
+
+def test_dominates_exact_optimum_and_paper_gap_claim():
+    """O_best >= Eq. 3 optimum always; the paper reports the gap < 10%."""
+    rng = np.random.default_rng(654)
+    ratios = []
+    for _ in range(120):
+        B = int(rng.integers(2, 8))
+        D = int(rng.integers(2, 4))
+        W = w.random_small_instance(rng, B, D, K=4)
+        s, cst = tables(W)
+        row = [int(k) for k in W.cand[0, : W.cand_np[0]]]
+        ok, _, lb, _ = oracle.alg1_dispatch(s, cst, W.schemes, row, 2024, 0, 100)
+        assert ok
+        opt = bf.eq3_opt([int(x) for x in s], W.schemes, row)
+        assert lb >= opt
+        ratios.append(lb / opt)
+    within = np.mean(np.array(ratios) <= 1.10)
+    print(f"Alg. 1 (T=100) / Eq. 3 optimum: within 10% on {within:.1%}, max {max(ratios):.3f}")
+    assert within >= 0.90
