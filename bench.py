@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu/clocks)")
+    ap.add_argument("--trials", type=int, default=0,
+                    help="NEXT-1: stage 1 = Alg. 1 with this many random trials per (c,t) (0: HYD-H1 dispatch)")
+    ap.add_argument("--seed", type=int, default=2024, help="Alg. 1 permutation seed")
     return ap.parse_args()
 
 
@@ -115,7 +118,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU oracle leg
-def oracle_sample(W, target_s, rng_seed=0, max_cand=None):
+def oracle_sample(W, target_s, rng_seed=0, max_cand=None, trials=0, seed=0):
     """Time the oracle (as it stands) on a bounded slice of W: a1-a5 for C' candidates x It' iterations."""
     import oracle
 
@@ -127,13 +130,13 @@ def oracle_sample(W, target_s, rng_seed=0, max_cand=None):
     ncal = min(W.n_cand, 16)
     sub = wl.Workload(W.cfg, W.name, W.lengths[its], W.schemes, W.cand[:ncal], W.cand_np[:ncal], W.k_pad)
     t0 = time.perf_counter()
-    oracle.assign_batch(sub, n_threads=0)
+    oracle.assign_batch(sub, n_threads=0, trials=trials, seed=seed)
     per = (time.perf_counter() - t0) / (ncal * n_it)
     nc = int(max(1, min(W.n_cand if max_cand is None else max_cand, target_s / max(per, 1e-9) / n_it)))
     cs = np.sort(rng.choice(W.n_cand, nc, replace=False))
     sub = wl.Workload(W.cfg, W.name, W.lengths[its], W.schemes, W.cand[cs], W.cand_np[cs], W.k_pad)
     t0 = time.perf_counter()
-    oracle.assign_batch(sub, n_threads=0)
+    oracle.assign_batch(sub, n_threads=0, trials=trials, seed=seed)
     dt = time.perf_counter() - t0
     cores = os.cpu_count() or 1
     return {
@@ -141,7 +144,8 @@ def oracle_sample(W, target_s, rng_seed=0, max_cand=None):
         "unit": UNIT,
         "cores": min(cores, nc),
         "kind": "oracle",
-        "sample": f"{nc} candidates x {n_it} iterations of cfg{W.cfg} ({nc * n_it} c-i, steps a1-a5), "
+        "sample": f"{nc} candidates x {n_it} iterations of cfg{W.cfg} ({nc * n_it} c-i, steps a1-a5"
+                  + (f", Alg. 1 with {trials} trials" if trials else "") + "), "
                   f"{dt:.1f} s on {min(cores, nc)} threads",
         "seconds": dt,
     }
@@ -216,7 +220,8 @@ def main():
     cand_np = W.cand_np[sh.cand_lo:sh.cand_hi]
     lens = W.lengths[sh.iter_lo:sh.iter_hi]
     It_local, C_local = lens.shape[0], cand.shape[0]
-    A = assign.Assigner(W.schemes, cand, cand_np, It_local, W.batch, W.k_pad, cand_offset=sh.cand_lo, device=dev)
+    A = assign.Assigner(W.schemes, cand, cand_np, It_local, W.batch, W.k_pad, cand_offset=sh.cand_lo, device=dev,
+                        trials=args.trials, seed=args.seed)
     len_dev = assign.lengths_to_device(lens, dev)
     A._lens_host = lens
     stream = torch.cuda.current_stream()
@@ -231,8 +236,13 @@ def main():
         hyd.cost_table(len_dev, It, B, A.schemes, K, kp, A.sorted_len, A.perm, A.cost, A.status)
         if evs:
             evs[1].record(stream)
-        hyd.dispatch(A.sorted_len, A.cost, It, B, kp, A.schemes, K, A.cand, A.cand_np, Cn, A.max_np, A.pipe, A.lb,
-                     A.stats, A.members, A.status)
+        if A.trials:  # NEXT-1: Alg. 1 (permutations drawn every step, as Alg. 1 line 2 does)
+            hyd.alg1_permutations(A.seed, It, B, A.trials, A.order)
+            hyd.dispatch_alg1(A.sorted_len, A.cost, It, B, kp, A.schemes, K, A.cand, A.cand_np, Cn, A.max_np,
+                              A.trials, A.order, A.best, A.pipe, A.lb, A.stats, A.members, A.status, A.alg1_ws)
+        else:
+            hyd.dispatch(A.sorted_len, A.cost, It, B, kp, A.schemes, K, A.cand, A.cand_np, Cn, A.max_np, A.pipe,
+                         A.lb, A.stats, A.members, A.status)
         if evs:
             evs[2].record(stream)
         hyd.pack(A.sorted_len, A.cost, It, B, kp, A.schemes, K, A.cand, A.cand_np, Cn, A.max_np, A.pipe, A.stats,
@@ -294,12 +304,12 @@ def main():
 
     # ---- end-to-end through the public host-buffer API (hyd_assign_host)
     e2e = None
-    if not args.no_e2e and not args.profile:
+    if not args.no_e2e and not args.profile and not args.trials:  # hyd_assign_host runs HYD-H1 only
         e2e = run_e2e(args, W, sh, cand, cand_np, lens, world, dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
-        cpu = oracle_sample(W, args.cpu_seconds)
+        cpu = oracle_sample(W, args.cpu_seconds, trials=args.trials, seed=args.seed)
 
     if rank == 0:
         line = {
@@ -326,6 +336,7 @@ def main():
                 "parallelism": f"candidates/{world}" if sh.by == "cand" else (f"iterations/{world}" if sh.by == "iter" else "single"),
                 "l2": "flushed: 256 MiB memset between steps, outside the timed events",
                 "cost_model": W.meta.get("model"),
+                "stage1": f"Alg. 1, {args.trials} random trials (NEXT-1)" if args.trials else "HYD-H1 LPT dispatch",
             },
             "kernel_ms": {n: float(x) for n, x in zip(names, per_kernel)},
             "roofline": roof,
@@ -381,10 +392,10 @@ def roofline(name, ms, W, A, pk, how, local_ci):
                 "hbm_algorithmic_GBps": local_ci * (3 * B + 10 * D + 8) / (ms / 1000.0) / 1e9,
                 "peak_source": f"148 SM x 128 INT32 lanes x {sm_mhz:.0f} MHz ({how} clock)"}
     if name == "dispatch":
-        ev = A.dispatch_evals(A._lens_host)
-        ops = 6.0 * ev
+        ev = A.dispatch_evals(A._lens_host) * max(A.trials, 1)
+        ops = (8.0 if A.trials else 6.0) * ev  # int ops per (sequence, feasible pipeline)
         achieved = ops / (ms / 1000.0) / 1e9
-        return {"kernel": "dispatch", "bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Gop/s",
+        return {"kernel": "dispatch" + (f" (Alg. 1, {A.trials} trials)" if A.trials else ""), "bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Gop/s",
                 "frac": achieved / alu_peak, "traffic": None, "algorithmic_ops_per_launch": ops,
                 "peak_source": f"148 SM x 128 INT32 lanes x {sm_mhz:.0f} MHz ({how} clock)"}
     byts = {"sort_cost": A.n_iter * B * (4 + 8 + 4 * A.k_pad), "select": A.n_iter * A.n_cand * 8 + 8 * A.n_iter}[name]

@@ -178,6 +178,32 @@ int hyd_assign_host(const uint32_t* len_host, int n_iter, int batch, const hyd_s
                     uint32_t* status_host, hyd_reduce_fn reduce, void* reduce_user, void* ws,
                     size_t ws_bytes, void* stream);
 
+/* ---- NEXT-1: Alg. 1 as stage 1 (T random trials) ----------------------
+ * hyd_alg1_permutations: the trial orders, order [n_iter][trials][batch] u16 (a permutation of
+ * the sorted positions 0..batch-1 per (t, trial)): Fisher-Yates (Durstenfeld); for k = batch-1
+ * down to 1: r = Philox4x32-10(counter = (k / 4, t, trial, 0), key = (seed mod 2^32,
+ * seed / 2^32)) word k % 4, j = (r (k + 1)) >> 32, swap(order[k], order[j]).  One order per
+ * (t, trial), shared by every candidate.  1 <= trials <= HYD_MAX_TRIALS.
+ *
+ * hyd_dispatch_alg1: same inputs and outputs as hyd_dispatch (pipe, lb, stats, members; the
+ * pack stage is unchanged), but each (c,t) runs `trials` greedy trials: the sequences arrive
+ * in order[t][trial] and each goes to the feasible pipeline j minimising
+ * O_max = max(C_j' + E_j', C_k + E_k for k != j), C_j' = C_j + T(l,P_j),
+ * E_j' = T(max length on j incl. l, P_j)(PP_j - 1), the first j on ties (Alg. 1 lines 5-14);
+ * the trial with the smallest (O_trial = max_j C_j + E_j, trial) is kept and lb = its O.
+ * best [n_cand][n_iter] u64 (caller-owned) receives O_best << 8 | trial (UINT64_MAX for an
+ * infeasible pair).  ws: hyd_alg1_workspace(n_iter) bytes of device scratch. */
+#define HYD_MAX_TRIALS 256
+size_t hyd_alg1_workspace(int n_iter);
+int hyd_alg1_permutations(uint64_t seed, int n_iter, int batch, int trials, uint16_t* order,
+                          void* stream);
+int hyd_dispatch_alg1(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch,
+                      int k_pad, const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
+                      const uint8_t* cand_np, int n_cand, int max_np, int trials,
+                      const uint16_t* order, uint64_t* best, uint8_t* pipe, uint64_t* lb,
+                      hyd_pipe_stats* stats, uint32_t* members, uint32_t* status, void* ws,
+                      size_t ws_bytes, void* stream);
+
 /* ---- host utilities --------------------------------------------------------------------
  * hyd_check_candidates: HOST tables; HYD_OK, HYD_E_INVALID or HYD_E_NOT_CANONICAL; writes
  * max over c of cand_np to *max_np_out (if non-null). */

@@ -70,9 +70,12 @@ class Assigner:
 
     ``schemes``: structured array (48-byte hyd_scheme records); ``cand`` [C][32] u8;
     ``cand_np`` [C] u8 -- this rank's candidates, global index = cand_offset + local.
+    ``trials`` > 0 replaces the HYD-H1 dispatch by Alg. 1 with that many random trials per
+    (c,t) (NEXT-1, include/hyd.h hyd_dispatch_alg1), its permutations drawn from ``seed``.
     """
 
-    def __init__(self, schemes, cand, cand_np, n_iter, batch, k_pad, cand_offset=0, device=None):
+    def __init__(self, schemes, cand, cand_np, n_iter, batch, k_pad, cand_offset=0, device=None, trials=0,
+                 seed=0):
         import torch
 
         self.torch = torch
@@ -113,20 +116,29 @@ class Assigner:
         self.key = torch.empty((It,), dtype=torch.int64, device=dev)
         self.status = torch.zeros((1,), dtype=i32, device=dev)
         self.ws = torch.empty((max(hyd.pack_workspace(It, B, Cn, self.max_np), 1),), dtype=u8, device=dev)
+        self.trials, self.seed = int(trials), int(seed)
+        if self.trials:
+            self.order = torch.empty((It, self.trials, B), dtype=torch.int16, device=dev)
+            self.best = torch.empty((Cn, It), dtype=torch.int64, device=dev)
+            self.alg1_ws = torch.empty((max(hyd.alg1_workspace(It), 1),), dtype=u8, device=dev)
 
     # a1-a5; ``len_dev`` int32/uint32-bit tensor [It][B] on the device
     def run(self, len_dev, stream=None):
         It, B, K, kp, Cn = self.n_iter, self.batch, self.n_schemes, self.k_pad, self.n_cand
         hyd.cost_table(len_dev, It, B, self.schemes, K, kp, self.sorted_len, self.perm, self.cost, self.status, stream)
-        hyd.dispatch(self.sorted_len, self.cost, It, B, kp, self.schemes, K, self.cand, self.cand_np, Cn,
-                     self.max_np, self.pipe, self.lb, self.stats, self.members, self.status, stream)
+        if self.trials:
+            hyd.alg1_permutations(self.seed, It, B, self.trials, self.order, stream)
+            hyd.dispatch_alg1(self.sorted_len, self.cost, It, B, kp, self.schemes, K, self.cand, self.cand_np, Cn,
+                              self.max_np, self.trials, self.order, self.best, self.pipe, self.lb, self.stats,
+                              self.members, self.status, self.alg1_ws, stream)
+        else:
+            hyd.dispatch(self.sorted_len, self.cost, It, B, kp, self.schemes, K, self.cand, self.cand_np, Cn,
+                         self.max_np, self.pipe, self.lb, self.stats, self.members, self.status, stream)
         hyd.pack(self.sorted_len, self.cost, It, B, kp, self.schemes, K, self.cand, self.cand_np, Cn, self.max_np,
                  self.pipe, self.stats, self.members, self.mb, self.v, self.ptime, self.makespan, self.status, self.ws,
                  stream)
         hyd.select_best(self.makespan, It, Cn, self.cand_offset, self.key, self.status, stream)
         return self.key
-
-    KERNELS_PER_RUN = 6  # sort_cost, dispatch, pack_init, pack_lanes, pack_big, select
 
     def pack_counters(self) -> dict:
         """Work counter written by the last hyd_pack (include/hyd.h: u64 at ws offset 16)."""
@@ -172,6 +184,9 @@ class Assigner:
             makespan=u(self.makespan, np.uint64),
             key=u(self.key, np.int64),
             status=self.status_bits(),
+            **({"best_trial": np.where(u(self.best, np.uint64) == np.uint64(2**64 - 1), -1,
+                                       (u(self.best, np.uint64) & np.uint64(0xFF)).astype(np.int64)).astype(np.int32),
+                "best_obj": u(self.best, np.uint64) >> np.uint64(8)} if self.trials else {}),
         )
 
 

@@ -22,6 +22,12 @@ int launch_gather(const int64_t*, const uint32_t*, const uint8_t*, const uint16_
                   const uint64_t*, int, int, int, int, uint8_t*, uint16_t*, uint16_t*, uint64_t*,
                   cudaStream_t);
 
+int launch_alg1_perm(uint64_t, int, int, int, uint16_t*, cudaStream_t);
+size_t alg1_workspace(int);
+int launch_alg1(const uint32_t*, const uint32_t*, int, int, int, const hyd_scheme*, int,
+                const uint8_t*, const uint8_t*, int, int, int, const uint16_t*, uint64_t*, uint8_t*,
+                uint64_t*, hyd_pipe_stats*, uint32_t*, uint32_t*, void*, cudaStream_t);
+
 static std::atomic<int> g_launches{0};
 static thread_local char g_err[256] = "no CUDA error";
 
@@ -156,6 +162,35 @@ int hyd_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, i
     return HYD_E_INVALID;
   return launch_dispatch(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np,
                          n_cand, max_np, pipe, lb, stats, members, status, (cudaStream_t)stream);
+}
+
+size_t hyd_alg1_workspace(int n_iter) {
+  if (n_iter < 0) return 0;
+  return alg1_workspace(n_iter);
+}
+
+int hyd_alg1_permutations(uint64_t seed, int n_iter, int batch, int trials, uint16_t* order,
+                          void* stream) {
+  if (!order || n_iter < 0 || batch < 1 || batch > HYD_MAX_BATCH || trials < 1 ||
+      trials > HYD_MAX_TRIALS)
+    return HYD_E_INVALID;
+  return launch_alg1_perm(seed, n_iter, batch, trials, order, (cudaStream_t)stream);
+}
+
+int hyd_dispatch_alg1(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch,
+                      int k_pad, const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
+                      const uint8_t* cand_np, int n_cand, int max_np, int trials,
+                      const uint16_t* order, uint64_t* best, uint8_t* pipe, uint64_t* lb,
+                      hyd_pipe_stats* stats, uint32_t* members, uint32_t* status, void* ws,
+                      size_t ws_bytes, void* stream) {
+  if (!sorted_len || !cost || !schemes || !cand || !cand_np || !order || !best || !pipe || !lb ||
+      !stats || !members || !status || !common_ok(n_iter, batch, n_schemes, k_pad) ||
+      !cand_ok(n_cand, max_np) || trials < 1 || trials > HYD_MAX_TRIALS)
+    return HYD_E_INVALID;
+  if (!ws || ws_bytes < alg1_workspace(n_iter)) return HYD_E_WORKSPACE;
+  return launch_alg1(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np,
+                     n_cand, max_np, trials, order, best, pipe, lb, stats, members, status, ws,
+                     (cudaStream_t)stream);
 }
 
 size_t hyd_pack_workspace(int n_iter, int batch, int n_cand, int max_np) {

@@ -35,6 +35,9 @@ EXPORTS = (
     "hyd_status_string",
     "hyd_last_cuda_error",
     "hyd_kernel_launches",
+    "hyd_alg1_workspace",
+    "hyd_alg1_permutations",
+    "hyd_dispatch_alg1",
 )
 
 
@@ -69,6 +72,9 @@ def lib():
         "hyd_status_string": ([I], C.c_char_p),
         "hyd_last_cuda_error": ([], C.c_char_p),
         "hyd_kernel_launches": ([], I),
+        "hyd_alg1_workspace": ([I], Z),
+        "hyd_alg1_permutations": ([U64, I, I, I, P, P], I),
+        "hyd_dispatch_alg1": ([P, P, I, I, I, P, I, P, P, I, I, I, P, P, P, P, P, P, P, P, Z, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -148,6 +154,23 @@ def pack(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_
                           _dev(ptime),
                           _dev(makespan), _dev(status), _dev(ws), ws.numel() * ws.element_size(),
                           _stream(stream)), "hyd_pack")
+
+
+def alg1_workspace(n_iter) -> int:
+    return int(lib().hyd_alg1_workspace(n_iter))
+
+
+def alg1_permutations(seed, n_iter, batch, trials, order, stream=None):
+    _check(lib().hyd_alg1_permutations(int(seed) & 0xFFFFFFFFFFFFFFFF, n_iter, batch, trials, _dev(order),
+                                       _stream(stream)), "hyd_alg1_permutations")
+
+
+def dispatch_alg1(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, trials,
+                  order, best, pipe, lb, stats, members, status, ws, stream=None):
+    _check(lib().hyd_dispatch_alg1(_dev(sorted_len), _dev(cost), n_iter, batch, k_pad, _dev(schemes), n_schemes,
+                                   _dev(cand), _dev(cand_np), n_cand, max_np, trials, _dev(order), _dev(best),
+                                   _dev(pipe), _dev(lb), _dev(stats), _dev(members), _dev(status), _dev(ws),
+                                   ws.numel() * ws.element_size(), _stream(stream)), "hyd_dispatch_alg1")
 
 
 def select_best(makespan, n_iter, n_cand, cand_offset, key, status, stream=None):

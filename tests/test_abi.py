@@ -23,7 +23,7 @@ def hyd():
 def declared_functions():
     src = open(os.path.join(ROOT, "include", "hyd.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(hyd_[a-z_]+)\s*\(", src)) - {"hyd_reduce_fn"})
+    return sorted(set(re.findall(r"\b(hyd_[a-z0-9_]+)\s*\(", src)) - {"hyd_reduce_fn"})
 
 
 def test_exports_every_declared_symbol(hyd):
@@ -54,6 +54,13 @@ def test_host_validation_is_synchronous(hyd):
     assert L.hyd_dispatch(P, P, 1, 16, 4, P, 1, P, P, 1, 2, P, P, None, P, P, None) == -1  # stats null
     assert L.hyd_select_best(P, 4, 10, (1 << 20) - 5, P, P, None) == -1  # key range
     assert L.hyd_pack(P, P, 1, 16, 4, P, 1, P, P, 1, 2, P, P, P, P, P, P, P, P, None, 0, None) == -6
+    # NEXT-1: trials in [1, HYD_MAX_TRIALS], workspace
+    assert L.hyd_alg1_permutations(1, 1, 16, 0, P, None) == -1
+    assert L.hyd_alg1_permutations(1, 1, 16, 257, P, None) == -1
+    assert L.hyd_alg1_permutations(1, 1, 16, 4, None, None) == -1
+    assert L.hyd_dispatch_alg1(P, P, 1, 16, 4, P, 1, P, P, 1, 2, 0, P, P, P, P, P, P, P, P, 4096, None) == -1
+    assert L.hyd_dispatch_alg1(P, P, 1, 16, 4, P, 1, P, P, 1, 2, 4, P, P, P, P, P, P, P, None, 0, None) == -6
+    assert L.hyd_alg1_workspace(1024) >= 1024 * 8
 
 
 def test_workspace_sizes(hyd):
