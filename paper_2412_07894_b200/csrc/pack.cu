@@ -631,7 +631,8 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
       }
     }
   };
-  for (int b = tid; b < NB; b += kLaneThreads) s_hist[b] = 0;
+  // pass A (thread per task): candidate counts (class <= 8 / > 8) and bucket of every task
+  if (tid == 0) s_n2a = 0;
   __syncthreads();
   for (int r = tid; r < nrec; r += kLaneThreads) {
     R.ncand[r] = 0;
@@ -658,92 +659,120 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
       continue;
     }
     if (n_lo + n_hi == 0) continue;
-    const int ub = min(31, (int)(R.u[r] >> 3));
     R.ncand[r] = (uint16_t)(n_lo | (n_hi << 8));
-    R.cbucket[r] = (uint8_t)ub;
-    if (n_lo) atomicAdd(&s_hist[ub], n_lo);
-    if (n_hi) atomicAdd(&s_hist[32 + ub], n_hi);
+    R.cbucket[r] = (uint8_t)min(31, (int)(R.u[r] >> 3));
+    atomicAdd(&s_n2a, n_lo + n_hi);
   }
   __syncthreads();
-  if (tid == 0) {  // exclusive scan, descending buckets
-    int run = 0;
-    for (int b = NB - 1; b >= 0; --b) {
-      const int h = s_hist[b];
-      s_hist[b] = run;
-      run += h;
+  phase_clock(3);
+  const int total2 = s_n2a;
+  if (VM == 16 && tid == 0) atomicAdd(a.why + 14, (unsigned long long)total2);
+  // ---- phase 2 in rounds of whole tasks whose units fit list2 (one round unless the tile
+  //      has more than ncap surviving V): the surviving V, each an independent run against
+  //      the reference; argmin by atomicMin on (obj << 16 | V)
+  for (int r0 = 0; r0 < nrec;) {
+    __syncthreads();
+    if (tid < 32) {  // round end r1: longest task range from r0 whose units fit ncap
+      int r1 = nrec;
+      if (total2 > ncap) {
+        int acc = 0;
+        r1 = r0;
+        for (int q0 = r0; q0 < nrec; q0 += 32) {
+          const int q = q0 + lane;
+          const int packed = q < nrec ? (int)R.ncand[q] : 0;
+          int x = (q < nrec && R.state[q] != 1) ? (packed & 0xFF) + (packed >> 8) : 0;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {  // inclusive warp scan
+            const int y = __shfl_up_sync(HYD_FULL, x, o);
+            if (lane >= o) x += y;
+          }
+          const unsigned fit = __ballot_sync(HYD_FULL, q < nrec && acc + x <= ncap);
+          const int nfit = __popc(fit);  // prefix property: the fitting lanes are 0..nfit-1
+          r1 = q0 + nfit;
+          if (nfit < 32) break;
+          acc += __shfl_sync(HYD_FULL, x, 31);
+        }
+        if (r1 == r0) r1 = r0 + 1;  // cannot happen (a task has <= VM <= ncap units)
+      }
+      if (lane == 0) s_n2b = r1;
     }
-    s_n2b = min(run, ncap);
-  }
-  __syncthreads();
-  for (int r = tid; r < nrec; r += kLaneThreads) {
-    const int packed = R.ncand[r];
-    if (packed == 0) continue;
-    const int n_lo = packed & 0xFF, n_hi = packed >> 8;
-    const int ub = R.cbucket[r];
-    const int p_lo = n_lo ? atomicAdd(&s_hist[ub], n_lo) : 0;
-    const int p_hi = n_hi ? atomicAdd(&s_hist[32 + ub], n_hi) : 0;
-    if ((n_lo && p_lo + n_lo > ncap) || (n_hi && p_hi + n_hi > ncap)) {
-      // does not fit: void its slots below ncap, hand it off
-      if (n_lo) for (int q = p_lo; q < min(p_lo + n_lo, ncap); ++q) R.list2[q] = 0xFFFFFFFFu;
-      if (n_hi) for (int q = p_hi; q < min(p_hi + n_hi, ncap); ++q) R.list2[q] = 0xFFFFFFFFu;
-      atomicAdd(a.why + 7, 1ull);
-      hand_off_e((int)R.eid[r]);
-      R.state[r] = 1;
-      continue;
+    for (int b = tid; b < NB; b += kLaneThreads) s_hist[b] = 0;
+    __syncthreads();
+    const int r1 = s_n2b;
+    for (int r = r0 + tid; r < r1; r += kLaneThreads) {
+      const int packed = R.ncand[r];
+      if (packed == 0 || R.state[r] == 1) continue;
+      const int ub = R.cbucket[r];
+      if (packed & 0xFF) atomicAdd(&s_hist[ub], packed & 0xFF);
+      if (packed >> 8) atomicAdd(&s_hist[32 + ub], packed >> 8);
     }
-    Search s;
-    walk(r, s);
-    uint32_t V;
-    int i_lo = 0, i_hi = 0;
-    while ((V = search_next(s)) != 0) {
-      const uint32_t w = ((uint32_t)r << 16) | V;
-      if (VM == 16 && V <= 8) {
-        if (i_lo < n_lo) R.list2[p_lo + i_lo++] = w;
-      } else {
-        if (i_hi < n_hi) R.list2[p_hi + i_hi++] = w;
+    __syncthreads();
+    if (tid == 0) {  // exclusive scan, descending buckets
+      int run = 0;
+      for (int b = NB - 1; b >= 0; --b) {
+        const int h = s_hist[b];
+        s_hist[b] = run;
+        run += h;
+      }
+      s_n2b = run;  // <= ncap by construction
+    }
+    __syncthreads();
+    // pass B: bucket-sorted units of the round (slot << 16 | V)
+    for (int r = r0 + tid; r < r1; r += kLaneThreads) {
+      const int packed = R.ncand[r];
+      if (packed == 0 || R.state[r] == 1) continue;
+      const int n_lo = packed & 0xFF, n_hi = packed >> 8;
+      const int ub = R.cbucket[r];
+      const int p_lo = n_lo ? atomicAdd(&s_hist[ub], n_lo) : 0;
+      const int p_hi = n_hi ? atomicAdd(&s_hist[32 + ub], n_hi) : 0;
+      Search s;
+      walk(r, s);
+      uint32_t V;
+      int i_lo = 0, i_hi = 0;
+      while ((V = search_next(s)) != 0) {
+        const uint32_t w = ((uint32_t)r << 16) | V;
+        if (VM == 16 && V <= 8) {
+          if (i_lo < n_lo) R.list2[p_lo + i_lo++] = w;
+        } else {
+          if (i_hi < n_hi) R.list2[p_hi + i_hi++] = w;
+        }
       }
     }
+    // pending phase-2 units per task of the round (its walks are done: sum_t is reused as the
+    // counter; later rounds walk only later tasks)
+    for (int r = r0 + tid; r < r1; r += kLaneThreads) {
+      const int packed = R.ncand[r];
+      R.sum_t[r] = (R.state[r] == 1) ? 0u : (uint32_t)((packed & 0xFF) + (packed >> 8));
+    }
+    __syncthreads();
+    run_units(
+        s_n2b,
+        [&](int q) {
+          const uint32_t w = R.list2[q];
+          const int r = (int)(w >> 16);
+          const uint32_t V = w & 0xFFFFu;
+          Search s;
+          s.P = s_pp[R.k[r]];
+          s.have = true;
+          s.best = R.key[r] >> 16;
+          const uint64_t th = search_thr_approx(s, V);
+          load_unit(r, V, th > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)th, false);
+          return true;
+        },
+        [&](int st) -> bool {
+          const int r = u.e;
+          if (st == 1 && !u.write) atomicMin(&R.key[r], obj_key(u));
+          if (u.write) return false;  // this was the task's final mb run
+          // the lane finishing a task's last candidate writes the winner's mb if it is not the
+          // reference run (whose mb phase 1 already wrote)
+          if (atomicSub(&R.sum_t[r], 1u) != 1u) return false;
+          const uint32_t V = (uint32_t)(R.key[r] & 0xFFFFu);
+          if (V == (uint32_t)R.va[r]) return false;
+          load_unit(r, V, 0xFFFFFFFFu, true);
+          return true;
+        });
+    r0 = r1;
   }
-  __syncthreads();
-
-  phase_clock(3);
-  if (VM == 16 && tid == 0) atomicAdd(a.why + 14, (unsigned long long)s_n2b);
-  // pending phase-2 units per task (sum_t is no longer needed: reused as the counter)
-  for (int r = tid; r < nrec; r += kLaneThreads) {
-    const int packed = R.ncand[r];
-    R.sum_t[r] = (R.state[r] == 1) ? 0u : (uint32_t)((packed & 0xFF) + (packed >> 8));
-  }
-  __syncthreads();
-  // ---- phase 2: the surviving V, each an independent run against the reference; argmin by
-  //      atomicMin on (obj << 16 | V)
-  run_units(
-      s_n2b,
-      [&](int q) {
-        const uint32_t w = R.list2[q];
-        if (w == 0xFFFFFFFFu) return false;
-        const int r = (int)(w >> 16);
-        if (R.state[r] == 1) return false;
-        const uint32_t V = w & 0xFFFFu;
-        Search s;
-        s.P = s_pp[R.k[r]];
-        s.have = true;
-        s.best = R.key[r] >> 16;
-        const uint64_t th = search_thr_approx(s, V);
-        load_unit(r, V, th > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)th, false);
-        return true;
-      },
-      [&](int st) -> bool {
-        const int r = u.e;
-        if (st == 1 && !u.write) atomicMin(&R.key[r], obj_key(u));
-        if (u.write) return false;  // this was the task's final mb run
-        // the lane finishing a task's last candidate writes the winner's mb if it is not the
-        // reference run (whose mb phase 1 already wrote)
-        if (atomicSub(&R.sum_t[r], 1u) != 1u) return false;
-        const uint32_t V = (uint32_t)(R.key[r] & 0xFFFFu);
-        if (V == (uint32_t)R.va[r]) return false;
-        load_unit(r, V, 0xFFFFFFFFu, true);
-        return true;
-      });
 
   phase_clock(4);
   phase_clock(5);
