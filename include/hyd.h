@@ -109,9 +109,9 @@ typedef struct {
  * Outputs pipe [n_cand][n_iter][batch] u8 (pipeline of each sorted position),
  * lb [n_cand][n_iter] u64 = max_j (C_j + E_j) (the Eq. 3 objective),
  * stats [n_iter][n_cand][max_np] (hyd_pipe_stats, for hyd_pack) and
- * members [n_iter][n_cand][max_np][ceil(batch/32)] u32: bit (i mod 32) of word i/32 of
- * pipeline j is set iff sorted position i was dispatched to j (the m_ij matrix of Eq. 3,
- * P:643-648, as bitmaps; for hyd_pack).  Rows of infeasible (c,t) are undefined.
+ * members [n_iter][n_cand][ceil(batch/32)][max_np] u32 (word-major): bit (i mod 32) of word
+ * [t][c][i/32][j] is set iff sorted position i was dispatched to pipeline j (the m_ij matrix
+ * of Eq. 3, as bitmaps; for hyd_pack).  Rows of infeasible (c,t) are undefined.
  * max_np = max over c of cand_np[c] (host-known; selects the kernel width). */
 int hyd_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch,
                  int k_pad, const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,

@@ -108,7 +108,7 @@ class Assigner:
         self.pipe = torch.empty((Cn, It, B), dtype=u8, device=dev)
         self.lb = torch.empty((Cn, It), dtype=torch.int64, device=dev)
         self.stats = torch.empty((Cn, It, self.max_np, hyd.PIPE_STATS_BYTES), dtype=u8, device=dev)
-        self.members = torch.empty((Cn, It, self.max_np, (B + 31) // 32), dtype=i32, device=dev)
+        self.members = torch.empty((It, Cn, (B + 31) // 32, self.max_np), dtype=i32, device=dev)
         self.mb = torch.empty((Cn, It, B), dtype=torch.int16, device=dev)
         self.v = torch.empty((Cn, It, hyd.MAX_PIPES), dtype=torch.int16, device=dev)
         self.ptime = torch.empty((Cn, It, hyd.MAX_PIPES), dtype=torch.int64, device=dev)

@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(kReplayThreads)
     if ((i & 31) == 31 || i == B - 1) {
 #pragma unroll
       for (int j = 0; j < DP; ++j) {
-        if (j < np) mbits[(size_t)j * nwords + (i >> 5)] = bits[j];
+        if (j < np) mbits[(size_t)(i >> 5) * max_np + j] = bits[j];  // word-major
         cnt[j] += __popc(bits[j]);
         bits[j] = 0u;
       }

@@ -65,7 +65,7 @@ __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
                                              int k_pad, const uint32_t (&ml)[DP],
                                              const uint32_t (&pp)[DP], const uint32_t (&kk)[DP],
                                              uint8_t* __restrict__ prow, unsigned long long* s_sum,
-                                             uint32_t* __restrict__ mbits, int np, int nwords,
+                                             uint32_t* __restrict__ mbits, int np, int mstride,
                                              uint64_t& lb_out, TT (&base)[DP],
                                              uint32_t (&cf)[DP]) {
   uint32_t mult[DP], bits[DP];
@@ -93,7 +93,7 @@ __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
 #pragma unroll
       for (int j = 0; j < DP; ++j) {
         if (j < np) {
-          mbits[(size_t)j * nwords + (i >> 5)] = bits[j];
+          mbits[(size_t)(i >> 5) * mstride + j] = bits[j];
           // cf_j = U_j << 16 | (index of the first (= longest) member + 1), B <= 16384
           const uint32_t f = (cf[j] & 0xFFFFu) == 0u && bits[j] != 0u ? w0 + __ffs(bits[j]) : 0u;
           cf[j] += (__popc(bits[j]) << 16) + f;
@@ -188,7 +188,7 @@ __device__ __forceinline__ void packed_run(const uint32_t* __restrict__ sl,
                                            const uint32_t (&ml)[DP], const uint32_t (&pp)[DP],
                                            const uint32_t (&kk)[DP], uint8_t* __restrict__ prow,
                                            unsigned long long* s_sum, uint32_t* __restrict__ mbits,
-                                           int np, int nwords, uint64_t& lb_out,
+                                           int np, int mstride, uint64_t& lb_out,
                                            uint32_t (&base)[DP], uint32_t (&cf)[DP],
                                            unsigned amask) {
   constexpr int SH = DP <= 2 ? 1 : DP <= 4 ? 2 : DP <= 8 ? 3 : DP <= 16 ? 4 : 5;
@@ -269,18 +269,28 @@ __device__ __forceinline__ void packed_run(const uint32_t* __restrict__ sl,
       for (int q = 0; q < 32; ++q)
         if (q < n) prow[i0 + q] = (uint8_t)(wd[q >> 2] >> (8 * (q & 3)));
     }
-    // membership words per pipeline; U_j and first member in cf_j
+    // membership words (word-major: the chunk's words of all pipelines are contiguous, so with
+    // mstride == DP they leave as full 32-byte sectors); U_j and first member in cf_j
     const uint32_t valid = n == 32 ? 0xFFFFFFFFu : (1u << n) - 1u;
+    uint32_t xw[DP];
 #pragma unroll
     for (int j = 0; j < DP; ++j) {
-      if (j < np) {
-        uint32_t x = valid;
+      uint32_t x = j < np ? valid : 0u;
 #pragma unroll
-        for (int b = 0; b < SH; ++b) x &= ((j >> b) & 1) ? plane[b] : ~plane[b];
-        mbits[(size_t)j * nwords + (i0 >> 5)] = x;
-        const uint32_t f = (cf[j] & 0xFFFFu) == 0u && x != 0u ? (uint32_t)i0 + __ffs(x) : 0u;
-        cf[j] += (__popc(x) << 16) + f;
-      }
+      for (int b = 0; b < SH; ++b) x &= ((j >> b) & 1) ? plane[b] : ~plane[b];
+      xw[j] = x;
+      const uint32_t f = (cf[j] & 0xFFFFu) == 0u && x != 0u ? (uint32_t)i0 + __ffs(x) : 0u;
+      cf[j] += (__popc(x) << 16) + f;
+    }
+    uint32_t* mrow = mbits + (size_t)(i0 >> 5) * mstride;
+    if (DP >= 4 && mstride == DP) {
+#pragma unroll
+      for (int j = 0; j < DP; j += 4)
+        *reinterpret_cast<uint4*>(mrow + j) = make_uint4(xw[j], xw[j + 1], xw[j + 2], xw[j + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < DP; ++j)
+        if (j < np) mrow[j] = xw[j];
     }
   }
   uint64_t mx = 0ull;
@@ -423,7 +433,7 @@ __global__ void __launch_bounds__(kDispatchThreads)
     return;
   }
   const int nwords = (B + 31) >> 5;
-  uint32_t* mbits = members + srow * max_np * nwords;
+  uint32_t* mbits = members + srow * max_np * nwords;  // word w of pipeline j at [w * max_np + j]
   unsigned long long* ssum = s_sum + tid;
   uint64_t lbv = 0ull;
   uint64_t base64[DP];
@@ -432,7 +442,7 @@ __global__ void __launch_bounds__(kDispatchThreads)
     const unsigned amask = __activemask();
     const uint32_t* cst = TRANS ? sm + (size_t)tt * B + (size_t)lt * k_pad * Bp : cs;
     uint32_t base[DP];
-    packed_run<DP, TRANS>(sl, cst, B, TRANS ? Bp : k_pad, ml, pp, kk, prow, ssum, mbits, np, nwords,
+    packed_run<DP, TRANS>(sl, cst, B, TRANS ? Bp : k_pad, ml, pp, kk, prow, ssum, mbits, np, max_np,
                           lbv, base, cf, amask);
 #pragma unroll
     for (int j = 0; j < DP; ++j) base64[j] = base[j];
@@ -440,12 +450,12 @@ __global__ void __launch_bounds__(kDispatchThreads)
     if (narrow) {
       uint32_t base[DP];
       dispatch_run<DP, uint32_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, ssum, mbits, np,
-                                        nwords, lbv, base, cf);
+                                        max_np, lbv, base, cf);
 #pragma unroll
       for (int j = 0; j < DP; ++j) base64[j] = base[j];
     } else {
       dispatch_run<DP, uint64_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, ssum, mbits, np,
-                                        nwords, lbv, base64, cf);
+                                        max_np, lbv, base64, cf);
     }
   }
   lb[row] = lbv;

@@ -52,7 +52,7 @@ struct PackArgs {
   int n_cand;
   const uint8_t* pipe;
   const hyd_pipe_stats* stats;
-  const uint32_t* members;  // [C][It][mnp][nwords] membership bitmaps from hyd_dispatch
+  const uint32_t* members;  // [It][C][nwords][mnp] membership words from hyd_dispatch
   int mnp, nwords;
   uint16_t* mb;
   uint16_t* v;
@@ -304,7 +304,7 @@ __device__ __forceinline__ void unit_start(LaneUnit<VM>& u, uint32_t V, uint32_t
   }
   u.qw = 0;
   u.cur = 0;
-  u.nxtw = __ldg(u.mw);
+  u.nxtw = __ldg(u.mw);  // word w of the pipeline at mw[w * mnp]
 }
 
 // Advance the unit by one sequence.  Returns 0 while running, 1 when the run completed,
@@ -314,7 +314,7 @@ __device__ __forceinline__ void unit_start(LaneUnit<VM>& u, uint32_t V, uint32_t
 // predicated on having a member, so the warp never splits inside the bin arithmetic.
 // STAGED: lengths at sm[0, B), costs at sm[B + i * kp + k] (shared window, 32-bit addressing).
 template <int N, int VM, bool STAGED>
-__device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, int B,
+__device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, uint32_t mnp, int B,
                                          const uint32_t* __restrict__ slen,
                                          const uint32_t* __restrict__ cst, int kp, uint32_t& ev) {
   extern __shared__ __align__(16) uint32_t sm[];
@@ -323,7 +323,7 @@ __device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, int B
     u.cur = u.nxtw;
     u.wbase = u.qw * 32u;
     ++u.qw;
-    u.nxtw = u.qw < nwords ? __ldg(u.mw + u.qw) : 0u;
+    u.nxtw = u.qw < nwords ? __ldg(u.mw + u.qw * mnp) : 0u;
   }
   const bool valid = u.cur != 0u;
   const uint32_t i = valid ? u.wbase + (uint32_t)(__ffs(u.cur) - 1) : 0u;
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
     u.e = r;
     u.k = R.k[r];
     u.M = s_ml[u.k];
-    u.mw = a.members + (fbase + e) * nwords;
+    u.mw = a.members + (fbase + e - e % mnp) * nwords + e % mnp;  // word-major rows of (t, c)
     u.mrow = a.mb + row * B;
     u.write = write;
     unit_start<VM>(u, V, thr);
@@ -547,8 +547,8 @@ __global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int 
         int st = 0;
 #pragma unroll 1
         for (int e = 0; e < kLaneEpoch && st == 0; ++e) {
-          if (VM == 16 && narrow) st = unit_step<8, VM, STAGED>(u, nwords, B, slen, cst, kp, ev);
-          else st = unit_step<VM, VM, STAGED>(u, nwords, B, slen, cst, kp, ev);
+          if (VM == 16 && narrow) st = unit_step<8, VM, STAGED>(u, nwords, mnp, B, slen, cst, kp, ev);
+          else st = unit_step<VM, VM, STAGED>(u, nwords, mnp, B, slen, cst, kp, ev);
         }
         if (st) have = finish(st);  // finish may load a follow-up unit into this lane
       }
@@ -810,16 +810,18 @@ __device__ __forceinline__ uint64_t warp_min<uint64_t>(uint64_t x) {
 // members at a time (word popcounts, warp prefix scan, per-lane rank search), each lane
 // gathering its member's (l, tau) so the sequential LPT loop reads them by shuffle.
 struct MemberStream {
-  const uint32_t* mw;
-  uint32_t nwords, wpos;  // next word window start
+  const uint32_t* mw;     // word w at mw[w * stride]
+  uint32_t nwords, stride, wpos;  // wpos: next word window start
   uint32_t wbits;         // this lane's word of the current window (already consumed bits cleared)
   uint32_t incl;          // inclusive prefix of remaining popcounts in the window
   uint32_t left;          // members left in the window
 };
 
-__device__ __forceinline__ void ms_open(MemberStream& m, const uint32_t* mw, uint32_t nwords) {
+__device__ __forceinline__ void ms_open(MemberStream& m, const uint32_t* mw, uint32_t nwords,
+                                        uint32_t stride) {
   m.mw = mw;
   m.nwords = nwords;
+  m.stride = stride;
   m.wpos = 0;
   m.left = 0;
   m.wbits = 0;
@@ -834,7 +836,7 @@ __device__ __forceinline__ uint32_t ms_next32(MemberStream& m, const uint32_t* _
   while (m.left == 0) {
     if (m.wpos >= m.nwords) return 0;
     const uint32_t w = m.wpos + lane;
-    m.wbits = w < m.nwords ? __ldg(m.mw + w) : 0u;
+    m.wbits = w < m.nwords ? __ldg(m.mw + (size_t)w * m.stride) : 0u;
     uint32_t c = __popc(m.wbits);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -879,7 +881,7 @@ __device__ __forceinline__ uint32_t ms_next32(MemberStream& m, const uint32_t* _
 // Writes mb when `write`; returns false if infeasible or the running max exceeds thr.
 template <int R, typename TT>
 __device__ __forceinline__ bool lpt_warp(const uint32_t* __restrict__ mw, uint32_t nwords,
-                                         uint32_t V, uint32_t M, const uint32_t* __restrict__ sl,
+                                         uint32_t mstride, uint32_t V, uint32_t M, const uint32_t* __restrict__ sl,
                                          const uint32_t* __restrict__ cs, int kp, uint32_t k,
                                          uint64_t thr64, bool write, uint16_t* __restrict__ mrow,
                                          uint64_t& maxbin, uint64_t* scr_t, uint32_t* scr_k,
@@ -903,7 +905,7 @@ __device__ __forceinline__ bool lpt_warp(const uint32_t* __restrict__ mw, uint32
     }
   }
   MemberStream ms;
-  ms_open(ms, mw, nwords);
+  ms_open(ms, mw, nwords, mstride);
   TT mx = 0;
   uint32_t cidx = 0, cl = 0, ctau = 0, n;
   while ((n = ms_next32(ms, sl, cs, kp, k, cidx, cl, ctau)) != 0) {
@@ -960,16 +962,16 @@ __device__ __forceinline__ bool lpt_warp(const uint32_t* __restrict__ mw, uint32
 }
 
 template <typename TT>
-__device__ __forceinline__ bool lpt_warp_dispatch(const uint32_t* mw, uint32_t nwords, uint32_t V,
+__device__ __forceinline__ bool lpt_warp_dispatch(const uint32_t* mw, uint32_t nwords, uint32_t mstride, uint32_t V,
                                                   uint32_t M, const uint32_t* sl, const uint32_t* cs,
                                                   int kp, uint32_t k, uint64_t thr, bool write,
                                                   uint16_t* mrow, uint64_t& maxbin, uint64_t* st,
                                                   uint32_t* sk, uint64_t& ev) {
-  if (V <= 32) return lpt_warp<1, TT>(mw, nwords, V, M, sl, cs, kp, k, thr, write, mrow, maxbin, st, sk, ev);
-  if (V <= 64) return lpt_warp<2, TT>(mw, nwords, V, M, sl, cs, kp, k, thr, write, mrow, maxbin, st, sk, ev);
-  if (V <= 128) return lpt_warp<4, TT>(mw, nwords, V, M, sl, cs, kp, k, thr, write, mrow, maxbin, st, sk, ev);
-  if (V <= 32 * kBigRMax) return lpt_warp<kBigRMax, TT>(mw, nwords, V, M, sl, cs, kp, k, thr, write, mrow, maxbin, st, sk, ev);
-  return lpt_warp<0, TT>(mw, nwords, V, M, sl, cs, kp, k, thr, write, mrow, maxbin, st, sk, ev);
+  if (V <= 32) return lpt_warp<1, TT>(mw, nwords, mstride, V, M, sl, cs, kp, k, thr, write, mrow, maxbin, st, sk, ev);
+  if (V <= 64) return lpt_warp<2, TT>(mw, nwords, mstride, V, M, sl, cs, kp, k, thr, write, mrow, maxbin, st, sk, ev);
+  if (V <= 128) return lpt_warp<4, TT>(mw, nwords, mstride, V, M, sl, cs, kp, k, thr, write, mrow, maxbin, st, sk, ev);
+  if (V <= 32 * kBigRMax) return lpt_warp<kBigRMax, TT>(mw, nwords, mstride, V, M, sl, cs, kp, k, thr, write, mrow, maxbin, st, sk, ev);
+  return lpt_warp<0, TT>(mw, nwords, mstride, V, M, sl, cs, kp, k, thr, write, mrow, maxbin, st, sk, ev);
 }
 
 // Persistent warps over the queue: one pipeline per warp, the sequential exact search
@@ -993,7 +995,7 @@ __global__ void __launch_bounds__(256) k_pack_big(PackArgs a) {
     const size_t srow = ((size_t)t * a.n_cand + c) * a.mnp + j;
     const uint32_t* sl = a.sorted_len + (size_t)t * B;
     const uint32_t* cs = a.cost + (size_t)t * B * kp;
-    const uint32_t* mw = a.members + srow * a.nwords;
+    const uint32_t* mw = a.members + (srow - j) * a.nwords + j;  // word-major rows of (t, c)
     const uint32_t k = a.cand[(size_t)c * HYD_MAX_PIPES + j];
     const hyd_pipe_stats st = a.stats[srow];
     Search s;
@@ -1013,16 +1015,16 @@ __global__ void __launch_bounds__(256) k_pack_big(PackArgs a) {
       while ((V = search_next(s)) != 0) {
         const uint64_t thr = first ? ~0ull : search_thr_approx(s, V);
         uint64_t mx = 0;
-        const bool ok = narrow ? lpt_warp_dispatch<uint32_t>(mw, a.nwords, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, scr_t, scr_k, ev)
-                               : lpt_warp_dispatch<uint64_t>(mw, a.nwords, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, scr_t, scr_k, ev);
+        const bool ok = narrow ? lpt_warp_dispatch<uint32_t>(mw, a.nwords, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, scr_t, scr_k, ev)
+                               : lpt_warp_dispatch<uint64_t>(mw, a.nwords, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, scr_t, scr_k, ev);
         if (ok && first) wV = V;
         first = false;
         if (ok && search_improves(s, V, mx)) search_take(s, V, mx);
       }
       if (s.have && s.vbest != wV) {  // the winner's mb was not written by the first run
         uint64_t mx = 0;
-        if (narrow) lpt_warp_dispatch<uint32_t>(mw, a.nwords, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, scr_t, scr_k, ev);
-        else lpt_warp_dispatch<uint64_t>(mw, a.nwords, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, scr_t, scr_k, ev);
+        if (narrow) lpt_warp_dispatch<uint32_t>(mw, a.nwords, (uint32_t)a.mnp, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, scr_t, scr_k, ev);
+        else lpt_warp_dispatch<uint64_t>(mw, a.nwords, (uint32_t)a.mnp, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, scr_t, scr_k, ev);
       }
     } else {
       s.best = 0;

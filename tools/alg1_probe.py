@@ -12,7 +12,7 @@ from paper_2412_07894_b200 import assign
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 nc = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 W = w.make_workload(cfg, n_cand=nc)
-for trials in (0, 100):
+for trials in ([0] if len(sys.argv) > 3 else [0, 100]):
     A = assign.Assigner(W.schemes, W.cand, W.cand_np, W.n_iter, W.batch, W.k_pad, trials=trials, seed=2024)
     L = assign.lengths_to_device(W.lengths)
     A.run(L)
