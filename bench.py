@@ -119,21 +119,24 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- CPU oracle leg
 def oracle_sample(W, target_s, rng_seed=0, max_cand=None, trials=0, seed=0):
-    """Time the oracle (as it stands) on a bounded slice of W: a1-a5 for C' candidates x It' iterations."""
+    """Time the oracle (as it stands) on a bounded slice of W: a1-a5 for C' candidates x It'
+    iterations, sized from a calibration run to about ``target_s`` seconds of CPU time."""
     import oracle
 
     oracle.build()
     rng = np.random.default_rng(rng_seed)
-    n_it = min(2, W.n_iter)
-    its = np.sort(rng.choice(W.n_iter, n_it, replace=False))
-    # calibrate on a few candidates, then size the sample to ~target_s
-    ncal = min(W.n_cand, 16)
+    ncal, ical = min(W.n_cand, 16), min(2, W.n_iter)
+    its = np.sort(rng.choice(W.n_iter, ical, replace=False))
     sub = wl.Workload(W.cfg, W.name, W.lengths[its], W.schemes, W.cand[:ncal], W.cand_np[:ncal], W.k_pad)
     t0 = time.perf_counter()
     oracle.assign_batch(sub, n_threads=0, trials=trials, seed=seed)
-    per = (time.perf_counter() - t0) / (ncal * n_it)
-    nc = int(max(1, min(W.n_cand if max_cand is None else max_cand, target_s / max(per, 1e-9) / n_it)))
+    per = (time.perf_counter() - t0) / (ncal * ical)  # wall seconds per c-i on all host threads
+    want = max(1, int(target_s / max(per, 1e-9)))  # c-i in the sample
+    cap = W.n_cand if max_cand is None else min(max_cand, W.n_cand)
+    nc = max(1, min(cap, want))
+    n_it = max(1, min(W.n_iter, -(-want // nc)))
     cs = np.sort(rng.choice(W.n_cand, nc, replace=False))
+    its = np.sort(rng.choice(W.n_iter, n_it, replace=False))
     sub = wl.Workload(W.cfg, W.name, W.lengths[its], W.schemes, W.cand[cs], W.cand_np[cs], W.k_pad)
     t0 = time.perf_counter()
     oracle.assign_batch(sub, n_threads=0, trials=trials, seed=seed)
@@ -145,8 +148,7 @@ def oracle_sample(W, target_s, rng_seed=0, max_cand=None, trials=0, seed=0):
         "cores": min(cores, nc),
         "kind": "oracle",
         "sample": f"{nc} candidates x {n_it} iterations of cfg{W.cfg} ({nc * n_it} c-i, steps a1-a5"
-                  + (f", Alg. 1 with {trials} trials" if trials else "") + "), "
-                  f"{dt:.1f} s on {min(cores, nc)} threads",
+                  + (f", Alg. 1 with {trials} trials" if trials else "") + f"), {dt:.1f} s on {min(cores, nc)} threads",
         "seconds": dt,
     }
 
@@ -242,7 +244,7 @@ def main():
                               A.trials, A.order, A.best, A.pipe, A.lb, A.stats, A.members, A.status, A.alg1_ws)
         else:
             hyd.dispatch(A.sorted_len, A.cost, It, B, kp, A.schemes, K, A.cand, A.cand_np, Cn, A.max_np, A.pipe,
-                         A.lb, A.stats, A.members, A.status)
+                         A.lb, A.stats, A.members, A.status, A.disp_ws)
         if evs:
             evs[2].record(stream)
         hyd.pack(A.sorted_len, A.cost, It, B, kp, A.schemes, K, A.cand, A.cand_np, Cn, A.max_np, A.pipe, A.stats,

@@ -112,11 +112,15 @@ typedef struct {
  * members [n_iter][n_cand][ceil(batch/32)][max_np] u32 (word-major): bit (i mod 32) of word
  * [t][c][i/32][j] is set iff sorted position i was dispatched to pipeline j (the m_ij matrix
  * of Eq. 3, as bitmaps; for hyd_pack).  Rows of infeasible (c,t) are undefined.
- * max_np = max over c of cand_np[c] (host-known; selects the kernel width). */
+ * max_np = max over c of cand_np[c] (host-known; selects the kernel width).
+ * ws: hyd_dispatch_workspace(n_iter) bytes of device scratch (per-iteration load bounds that
+ * pick the kernels' integer width); HYD_E_WORKSPACE if smaller. */
+size_t hyd_dispatch_workspace(int n_iter);
 int hyd_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch,
                  int k_pad, const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
                  const uint8_t* cand_np, int n_cand, int max_np, uint8_t* pipe, uint64_t* lb,
-                 hyd_pipe_stats* stats, uint32_t* members, uint32_t* status, void* stream);
+                 hyd_pipe_stats* stats, uint32_t* members, uint32_t* status, void* ws,
+                 size_t ws_bytes, void* stream);
 
 /* ---- a4: stage 2 packing (Eq. 1 + App. D) -------------------------------------------
  * Inputs include pipe, stats and members from hyd_dispatch (same n_cand/n_iter/max_np).

@@ -116,6 +116,7 @@ class Assigner:
         self.key = torch.empty((It,), dtype=torch.int64, device=dev)
         self.status = torch.zeros((1,), dtype=i32, device=dev)
         self.ws = torch.empty((max(hyd.pack_workspace(It, B, Cn, self.max_np), 1),), dtype=u8, device=dev)
+        self.disp_ws = torch.empty((max(hyd.dispatch_workspace(It), 1),), dtype=u8, device=dev)
         self.trials, self.seed = int(trials), int(seed)
         if self.trials:
             self.order = torch.empty((It, self.trials, B), dtype=torch.int16, device=dev)
@@ -133,7 +134,8 @@ class Assigner:
                               self.members, self.status, self.alg1_ws, stream)
         else:
             hyd.dispatch(self.sorted_len, self.cost, It, B, kp, self.schemes, K, self.cand, self.cand_np, Cn,
-                         self.max_np, self.pipe, self.lb, self.stats, self.members, self.status, stream)
+                         self.max_np, self.pipe, self.lb, self.stats, self.members, self.status, self.disp_ws,
+                         stream)
         hyd.pack(self.sorted_len, self.cost, It, B, kp, self.schemes, K, self.cand, self.cand_np, Cn, self.max_np,
                  self.pipe, self.stats, self.members, self.mb, self.v, self.ptime, self.makespan, self.status, self.ws,
                  stream)

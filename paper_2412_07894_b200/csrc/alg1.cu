@@ -12,7 +12,7 @@
 // Kernels:
 //   k_alg1_perm    thread per (t, trial): Fisher-Yates over the B sorted positions from
 //                  Philox4x32-10 (the counter layout of include/hyd.h); order [It][T][B] u16.
-//   k_alg1_bound   thread per t: a bound on every C + E of the iteration (packed-key choice).
+//   (k_iter_bound of dispatch.cu: a per-iteration bound on every C + E, packed-key choice.)
 //   k_alg1_trials  thread per (c, t, trial): lane = candidate, warp = trial, CTA = 8 trials of
 //                  one iteration, whose lengths / cost rows / orders are staged in smem.
 //                  MODE 0 packed u32 keys max(new_j, M) << SH | j, MODE 1 u64 (CTAs of the
@@ -63,25 +63,8 @@ __global__ void k_alg1_perm(uint64_t seed, int n_iter, int batch, int trials,
   }
 }
 
-// bound[t] = sum_i max_k tau_ik + max_ik tau_ik * (PPmax - 1) >= every C_j + E_j of iteration t
-__global__ void k_alg1_bound(const uint32_t* __restrict__ cost, int n_iter, int batch, int k_pad,
-                             const hyd_scheme* __restrict__ schemes, int n_schemes,
-                             uint64_t* __restrict__ bound) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_iter) return;
-  uint32_t ppmax = 1u;
-  for (int k = 0; k < n_schemes; ++k) ppmax = max(ppmax, schemes[k].pp);
-  uint64_t s = 0;
-  uint32_t tmx = 0u;
-  const uint32_t* c = cost + (size_t)t * batch * k_pad;
-  for (int i = 0; i < batch; ++i) {
-    uint32_t m = 0u;
-    for (int k = 0; k < n_schemes; ++k) m = max(m, __ldg(c + (size_t)i * k_pad + k));
-    s += m;
-    tmx = max(tmx, m);
-  }
-  bound[t] = s + (uint64_t)tmx * (ppmax - 1u);
-}
+int launch_iter_bound(const uint32_t* cost, int n_iter, int batch, int k_pad,
+                      const hyd_scheme* schemes, int n_schemes, uint64_t* bound, cudaStream_t s);
 
 __host__ __device__ constexpr int alg1_sh(int dp) {
   return dp <= 2 ? 1 : dp <= 4 ? 2 : dp <= 8 ? 3 : dp <= 16 ? 4 : 5;
@@ -418,9 +401,8 @@ static cudaError_t launch_alg1_dp(const uint32_t* sorted_len, const uint32_t* co
                                   uint64_t* best, uint8_t* pipe, uint64_t* lb,
                                   hyd_pipe_stats* stats, uint32_t* members, uint32_t* status,
                                   cudaStream_t s) {
-  k_alg1_bound<<<(n_iter + 127) / 128, 128, 0, s>>>(cost, n_iter, batch, k_pad, schemes, n_schemes,
-                                                    bound);
-  note_launch();
+  if (launch_iter_bound(cost, n_iter, batch, k_pad, schemes, n_schemes, bound, s) != HYD_OK)
+    return cudaGetLastError();
   cudaError_t e = cudaMemsetAsync(best, 0xFF, (size_t)n_cand * n_iter * 8, s);
   if (e != cudaSuccess) return e;
   const size_t stage = alg1_stage_bytes(batch, k_pad);

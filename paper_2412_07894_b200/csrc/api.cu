@@ -9,9 +9,10 @@ namespace hyd {
 
 int launch_sort_cost(const uint32_t*, int, int, const hyd_scheme*, int, int, uint32_t*, uint32_t*,
                      uint32_t*, uint32_t*, cudaStream_t);
+size_t dispatch_workspace(int);
 int launch_dispatch(const uint32_t*, const uint32_t*, int, int, int, const hyd_scheme*, int,
                     const uint8_t*, const uint8_t*, int, int, uint8_t*, uint64_t*, hyd_pipe_stats*,
-                    uint32_t*, uint32_t*, cudaStream_t);
+                    uint32_t*, uint32_t*, void*, cudaStream_t);
 size_t pack_workspace(int, int, int, int);
 int launch_pack(const uint32_t*, const uint32_t*, int, int, int, const hyd_scheme*, int,
                 const uint8_t*, const uint8_t*, int, int, const uint8_t*, const hyd_pipe_stats*,
@@ -53,7 +54,7 @@ static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct AssignLayout {
   size_t len, schemes, cand, cand_np, sorted, perm, cost, pipe, lb, stats, members, mb, v, ptime, makespan, key,
-      status, win_pipe, win_mb, win_v, win_ptime, pack_ws, pack_bytes, total;
+      status, win_pipe, win_mb, win_v, win_ptime, disp_ws, pack_ws, pack_bytes, total;
 };
 
 static AssignLayout assign_layout(int n_iter, int batch, int n_schemes, int k_pad, int n_cand,
@@ -87,6 +88,7 @@ static AssignLayout assign_layout(int n_iter, int batch, int n_schemes, int k_pa
   L.win_mb = put(It * B * 2);
   L.win_v = put(It * HYD_MAX_PIPES * 2);
   L.win_ptime = put(It * HYD_MAX_PIPES * 8);
+  L.disp_ws = put(dispatch_workspace(n_iter));
   L.pack_bytes = pack_workspace(n_iter, batch, n_cand, max_np);
   L.pack_ws = put(L.pack_bytes);
   L.total = o;
@@ -153,15 +155,22 @@ int hyd_cost_table(const uint32_t* len, int n_iter, int batch, const hyd_scheme*
                           status, (cudaStream_t)stream);
 }
 
+size_t hyd_dispatch_workspace(int n_iter) {
+  if (n_iter < 0) return 0;
+  return dispatch_workspace(n_iter);
+}
+
 int hyd_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch,
                  int k_pad, const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
                  const uint8_t* cand_np, int n_cand, int max_np, uint8_t* pipe, uint64_t* lb,
-                 hyd_pipe_stats* stats, uint32_t* members, uint32_t* status, void* stream) {
+                 hyd_pipe_stats* stats, uint32_t* members, uint32_t* status, void* ws,
+                 size_t ws_bytes, void* stream) {
   if (!sorted_len || !cost || !schemes || !cand || !cand_np || !pipe || !lb || !stats || !members || !status ||
       !common_ok(n_iter, batch, n_schemes, k_pad) || !cand_ok(n_cand, max_np))
     return HYD_E_INVALID;
+  if (!ws || ws_bytes < dispatch_workspace(n_iter)) return HYD_E_WORKSPACE;
   return launch_dispatch(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np,
-                         n_cand, max_np, pipe, lb, stats, members, status, (cudaStream_t)stream);
+                         n_cand, max_np, pipe, lb, stats, members, status, ws, (cudaStream_t)stream);
 }
 
 size_t hyd_alg1_workspace(int n_iter) {
@@ -296,7 +305,7 @@ int hyd_assign_host(const uint32_t* len_host, int n_iter, int batch, const hyd_s
   auto* pst = static_cast<hyd_pipe_stats*>(D(L.stats));
   auto* mem = static_cast<uint32_t*>(D(L.members));
   rc = launch_dispatch(sorted, cost, n_iter, batch, k_pad, sch, n_schemes, cand, cnp, n_cand, max_np,
-                       pipe, static_cast<uint64_t*>(D(L.lb)), pst, mem, st, s);
+                       pipe, static_cast<uint64_t*>(D(L.lb)), pst, mem, st, D(L.disp_ws), s);
   if (rc) return rc;
   rc = launch_pack(sorted, cost, n_iter, batch, k_pad, sch, n_schemes, cand, cnp, n_cand, max_np,
                    pipe, pst, mem, mb, vv, pt, ms, st, D(L.pack_ws), L.pack_bytes, s);

@@ -302,9 +302,56 @@ __device__ __forceinline__ void packed_run(const uint32_t* __restrict__ sl,
   lb_out = mx;
 }
 
+// Per-iteration bound[t] = sum_i max_k tau_ik + max_ik tau_ik (PPmax - 1): no C_j + E_j (and no
+// candidate load C_j + tau + e_j) of iteration t can exceed it.  One CTA per iteration.
+__global__ void __launch_bounds__(256)
+    k_iter_bound(const uint32_t* __restrict__ cost, int batch, int k_pad,
+                 const hyd_scheme* __restrict__ schemes, int n_schemes, uint64_t* __restrict__ bound) {
+  __shared__ unsigned long long s_part[8];
+  __shared__ uint32_t s_top;
+  const int t = blockIdx.x, tid = threadIdx.x;
+  const uint32_t* c = cost + (size_t)t * batch * k_pad;
+  unsigned long long sum = 0ull;
+  uint32_t top = 0u;
+  for (int i = tid; i < batch; i += 256) {
+    uint32_t m = 0u;
+    for (int k = 0; k < n_schemes; ++k) m = max(m, __ldg(c + (size_t)i * k_pad + k));
+    sum += m;
+    top = max(top, m);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    sum += __shfl_xor_sync(HYD_FULL, sum, o);
+    top = max(top, __shfl_xor_sync(HYD_FULL, top, o));
+  }
+  if (tid == 0) s_top = 0u;
+  __syncthreads();
+  if ((tid & 31) == 0) {
+    s_part[tid >> 5] = sum;
+    atomicMax(&s_top, top);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long b = 0ull;
+    for (int w = 0; w < 8; ++w) b += s_part[w];
+    uint32_t ppmax = 1u;
+    for (int k = 0; k < n_schemes; ++k) ppmax = max(ppmax, schemes[k].pp);
+    bound[t] = b + (unsigned long long)s_top * (ppmax - 1u);
+  }
+}
+
+int launch_iter_bound(const uint32_t* cost, int n_iter, int batch, int k_pad,
+                      const hyd_scheme* schemes, int n_schemes, uint64_t* bound, cudaStream_t s) {
+  if (n_iter == 0) return HYD_OK;
+  k_iter_bound<<<n_iter, 256, 0, s>>>(cost, batch, k_pad, schemes, n_schemes, bound);
+  note_launch();
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? HYD_OK : record_cuda_error(e);
+}
+
 // MODE 0: CTAs whose load bound admits packed keys; MODE 1: the others (u32 / u64 sums).  Both
-// kernels are launched; each computes the same per-CTA bound and leaves the other's CTAs alone,
-// so the common packed case runs with the packed kernel's smaller register footprint.
+// kernels are launched; each reads the same per-iteration bounds and leaves the other's CTAs
+// alone (before staging anything), so the common packed case runs with the packed kernel's
+// smaller register footprint.
 template <int DP, bool STAGED, int MODE>
 __global__ void __launch_bounds__(kDispatchThreads)
     k_dispatch(const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ cost,
@@ -312,7 +359,8 @@ __global__ void __launch_bounds__(kDispatchThreads)
                int n_schemes, const uint8_t* __restrict__ cand, const uint8_t* __restrict__ cand_np,
                int n_cand, int max_np, int ct, int tt, uint8_t* __restrict__ pipe,
                uint64_t* __restrict__ lb, hyd_pipe_stats* __restrict__ stats,
-               uint32_t* __restrict__ members, uint32_t* __restrict__ status) {
+               uint32_t* __restrict__ members, uint32_t* __restrict__ status,
+               const uint64_t* __restrict__ bounds) {
   extern __shared__ __align__(16) uint32_t sm[];
   // dynamic smem: [stage if STAGED] [s_sum u64 columns]; stage = [tt][B] lengths, then the
   // costs: MODE 1 as global rows [tt][B][k_pad]; MODE 0 transposed [tt][k_pad][Bp], Bp = B | 1
@@ -321,11 +369,16 @@ __global__ void __launch_bounds__(kDispatchThreads)
   const int Bp = B | 1;
   const size_t stage_words = STAGED ? dispatch_stage_words(tt, B, k_pad) : 0;
   unsigned long long* s_sum = reinterpret_cast<unsigned long long*>(sm + ((stage_words + 3) & ~(size_t)3));
-  __shared__ unsigned long long s_bound[kDispatchThreads / 32];
-  __shared__ uint32_t s_ppmax;
   const int tid = threadIdx.x;
   const int c0 = blockIdx.x * ct, t0 = blockIdx.y * tt;
   const int ntt = min(tt, n_iter - t0);
+  // every load of the CTA's threads is below the largest bound of its iterations
+  unsigned long long bound = 0ull;
+  for (int lt = 0; lt < ntt; ++lt) bound = max(bound, (unsigned long long)bounds[t0 + lt]);
+  const bool narrow = bound < 0xFFFFFFFFull;
+  constexpr int SHK = DP <= 2 ? 1 : DP <= 4 ? 2 : DP <= 8 ? 3 : DP <= 16 ? 4 : 5;
+  const bool packed = bound < (1ull << (31 - SHK));  // keys (load << SHK | j) stay below 2^31
+  if ((MODE == 0) != packed) return;  // the other kernel owns this CTA
   if (STAGED) {
     const uint4* gl = reinterpret_cast<const uint4*>(sorted_len + (size_t)t0 * B);
     uint4* sl4 = reinterpret_cast<uint4*>(sm);
@@ -351,41 +404,9 @@ __global__ void __launch_bounds__(kDispatchThreads)
       for (int e = tid; e < nc; e += kDispatchThreads) sc4[e] = __ldg(gc + e);
     }
   }
-  if (tid == 0) {
-    uint32_t m = 1u;
-    for (int k = 0; k < n_schemes; ++k) m = max(m, schemes[k].pp);
-    s_ppmax = m;
-  }
 #pragma unroll
   for (int j = 0; j < DP; ++j) s_sum[j * kDispatchThreads + tid] = 0ull;
   __syncthreads();
-  // u32 bound over the CTA's iterations: sum_i max_k tau_ik + max tau * (PPmax - 1) < 2^32-1
-  //  =>  every base_j and new_j of every thread fits u32 (strictly below the u32 sentinel).
-  unsigned long long bound = 0ull;
-  for (int e = tid; e < ntt * B; e += kDispatchThreads) {
-    const int lt = e / B, i = e - lt * B;
-    uint32_t mx = 0u;
-    if (TRANS) {
-      const uint32_t* col = sm + (size_t)tt * B + (size_t)lt * k_pad * Bp + i;
-      for (int k = 0; k < n_schemes; ++k) mx = max(mx, col[(size_t)k * Bp]);
-    } else {
-      const uint32_t* crow = STAGED ? sm + (size_t)tt * B + ((size_t)lt * B + i) * k_pad
-                                    : cost + ((size_t)(t0 + lt) * B + i) * k_pad;
-      for (int k = 0; k < n_schemes; ++k) mx = max(mx, STAGED ? crow[k] : __ldg(crow + k));
-    }
-    unsigned long long v = (unsigned long long)mx;
-    if (i == 0) v += (unsigned long long)mx * (s_ppmax - 1u);
-    bound += v;
-  }
-  for (int o = 16; o > 0; o >>= 1) bound += __shfl_xor_sync(HYD_FULL, bound, o);
-  if ((tid & 31) == 0) s_bound[tid >> 5] = bound;
-  __syncthreads();
-  bound = 0ull;
-  for (int w = 0; w < kDispatchThreads / 32; ++w) bound += s_bound[w];
-  const bool narrow = bound < 0xFFFFFFFFull;
-  constexpr int SHK = DP <= 2 ? 1 : DP <= 4 ? 2 : DP <= 8 ? 3 : DP <= 16 ? 4 : 5;
-  const bool packed = bound < (1ull << (31 - SHK));  // keys (load << SHK | j) stay below 2^31
-  if ((MODE == 0) != packed) return;  // the other kernel owns this CTA
 
   const int lt = tid / ct, lc = tid - lt * ct;
   const int c = c0 + lc, t = t0 + lt;
@@ -483,13 +504,13 @@ static cudaError_t launch_mode(dim3 grid, size_t smem, cudaStream_t s, const uin
                                const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
                                const uint8_t* cand_np, int n_cand, int max_np, int ct, int tt,
                                uint8_t* pipe, uint64_t* lb, hyd_pipe_stats* stats, uint32_t* members,
-                               uint32_t* status) {
+                               uint32_t* status, const uint64_t* bounds) {
   cudaError_t e = cudaFuncSetAttribute(k_dispatch<DP, STAGED, MODE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_dispatch<DP, STAGED, MODE><<<grid, kDispatchThreads, smem, s>>>(
       sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct,
-      tt, pipe, lb, stats, members, status);
+      tt, pipe, lb, stats, members, status, bounds);
   note_launch();
   return cudaGetLastError();
 }
@@ -500,27 +521,33 @@ static cudaError_t launch_dp(bool staged, dim3 grid, size_t smem_stage, cudaStre
                              int k_pad, const hyd_scheme* schemes, int n_schemes,
                              const uint8_t* cand, const uint8_t* cand_np, int n_cand, int max_np,
                              int ct, int tt, uint8_t* pipe, uint64_t* lb, hyd_pipe_stats* stats,
-                             uint32_t* members, uint32_t* status) {
+                             uint32_t* members, uint32_t* status, const uint64_t* bounds) {
   const size_t cols = (size_t)DP * kDispatchThreads * 8;
   const size_t smem = staged ? ((smem_stage + 15) & ~(size_t)15) + cols : cols;
   cudaError_t e;
   if (staged) {
-    e = launch_mode<DP, true, 0>(grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status);
+    e = launch_mode<DP, true, 0>(grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds);
     if (e == cudaSuccess)
-      e = launch_mode<DP, true, 1>(grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status);
+      e = launch_mode<DP, true, 1>(grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds);
   } else {
-    e = launch_mode<DP, false, 0>(grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status);
+    e = launch_mode<DP, false, 0>(grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds);
     if (e == cudaSuccess)
-      e = launch_mode<DP, false, 1>(grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status);
+      e = launch_mode<DP, false, 1>(grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds);
   }
   return e;
 }
 
+size_t dispatch_workspace(int n_iter) { return ((size_t)n_iter * 8 + 255) & ~(size_t)255; }
+
 int launch_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch,
                     int k_pad, const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
                     const uint8_t* cand_np, int n_cand, int max_np, uint8_t* pipe, uint64_t* lb,
-                    hyd_pipe_stats* stats, uint32_t* members, uint32_t* status, cudaStream_t s) {
+                    hyd_pipe_stats* stats, uint32_t* members, uint32_t* status, void* ws,
+                    cudaStream_t s) {
   if (n_iter == 0 || n_cand == 0) return HYD_OK;
+  uint64_t* bounds = static_cast<uint64_t*>(ws);
+  const int rb = launch_iter_bound(cost, n_iter, batch, k_pad, schemes, n_schemes, bounds, s);
+  if (rb != HYD_OK) return rb;
   const int ct = n_cand < kDispatchThreads ? n_cand : kDispatchThreads;
   const int tt = kDispatchThreads / ct;
   const size_t smem = dispatch_stage_words(tt, batch, k_pad) * 4;
@@ -531,11 +558,11 @@ int launch_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter
   dim3 grid((n_cand + ct - 1) / ct, (n_iter + tt - 1) / tt);
   cudaError_t e;
   switch (dp) {
-    case 2: e = launch_dp<2>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status); break;
-    case 4: e = launch_dp<4>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status); break;
-    case 8: e = launch_dp<8>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status); break;
-    case 16: e = launch_dp<16>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status); break;
-    default: e = launch_dp<32>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status); break;
+    case 2: e = launch_dp<2>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds); break;
+    case 4: e = launch_dp<4>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds); break;
+    case 8: e = launch_dp<8>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds); break;
+    case 16: e = launch_dp<16>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds); break;
+    default: e = launch_dp<32>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds); break;
   }
   return e == cudaSuccess ? HYD_OK : record_cuda_error(e);
 }

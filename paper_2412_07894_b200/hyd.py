@@ -23,6 +23,7 @@ INT64_MAX = 2**63 - 1
 # every function include/hyd.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "hyd_cost_table",
+    "hyd_dispatch_workspace",
     "hyd_dispatch",
     "hyd_pack_workspace",
     "hyd_pack",
@@ -60,7 +61,8 @@ def lib():
     I, P, Z, U64 = C.c_int, C.c_void_p, C.c_size_t, C.c_uint64
     sig = {
         "hyd_cost_table": ([P, I, I, P, I, I, P, P, P, P, P], I),
-        "hyd_dispatch": ([P, P, I, I, I, P, I, P, P, I, I, P, P, P, P, P, P], I),
+        "hyd_dispatch_workspace": ([I], Z),
+        "hyd_dispatch": ([P, P, I, I, I, P, I, P, P, I, I, P, P, P, P, P, P, Z, P], I),
         "hyd_pack_workspace": ([I, I, I, I], Z),
         "hyd_pack": ([P, P, I, I, I, P, I, P, P, I, I, P, P, P, P, P, P, P, P, P, Z, P], I),
         "hyd_select_best": ([P, I, I, I, P, P, P], I),
@@ -136,11 +138,16 @@ def cost_table(len_, n_iter, batch, schemes, n_schemes, k_pad, sorted_len, perm,
                                 _dev(perm), _dev(cost), _dev(status), _stream(stream)), "hyd_cost_table")
 
 
+def dispatch_workspace(n_iter) -> int:
+    return int(lib().hyd_dispatch_workspace(n_iter))
+
+
 def dispatch(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, pipe, lb,
-             stats, members, status, stream=None):
+             stats, members, status, ws, stream=None):
     _check(lib().hyd_dispatch(_dev(sorted_len), _dev(cost), n_iter, batch, k_pad, _dev(schemes), n_schemes,
                               _dev(cand), _dev(cand_np), n_cand, max_np, _dev(pipe), _dev(lb), _dev(stats),
-                              _dev(members), _dev(status), _stream(stream)), "hyd_dispatch")
+                              _dev(members), _dev(status), _dev(ws), ws.numel() * ws.element_size(),
+                              _stream(stream)), "hyd_dispatch")
 
 
 def pack_workspace(n_iter, batch, n_cand, max_np) -> int:

@@ -50,8 +50,10 @@ def test_host_validation_is_synchronous(hyd):
     assert L.hyd_cost_table(P, 1, 16, P, 5, 4, P, P, P, P, None) == -1  # k_pad < K
     assert L.hyd_cost_table(P, 1, 16, P, 3, 6, P, P, P, P, None) == -1  # k_pad % 4
     assert L.hyd_cost_table(P, 1, 16385, P, 1, 4, P, P, P, P, None) == -1  # batch limit
-    assert L.hyd_dispatch(P, P, 1, 16, 4, P, 1, P, P, 1, 33, P, P, P, P, P, None) == -1  # max_np > 32
-    assert L.hyd_dispatch(P, P, 1, 16, 4, P, 1, P, P, 1, 2, P, P, None, P, P, None) == -1  # stats null
+    assert L.hyd_dispatch(P, P, 1, 16, 4, P, 1, P, P, 1, 33, P, P, P, P, P, P, 4096, None) == -1  # max_np > 32
+    assert L.hyd_dispatch(P, P, 1, 16, 4, P, 1, P, P, 1, 2, P, P, None, P, P, P, 4096, None) == -1  # stats null
+    assert L.hyd_dispatch(P, P, 1, 16, 4, P, 1, P, P, 1, 2, P, P, P, P, P, None, 0, None) == -6  # no workspace
+    assert L.hyd_dispatch_workspace(1024) >= 1024 * 8
     assert L.hyd_select_best(P, 4, 10, (1 << 20) - 5, P, P, None) == -1  # key range
     assert L.hyd_pack(P, P, 1, 16, 4, P, 1, P, P, 1, 2, P, P, P, P, P, P, P, P, None, 0, None) == -6
     # NEXT-1: trials in [1, HYD_MAX_TRIALS], workspace
