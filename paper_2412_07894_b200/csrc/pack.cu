@@ -37,6 +37,8 @@
 namespace hyd {
 
 constexpr int kLaneThreads = 256;
+constexpr size_t kLaneSmem16 = 74 * 1024;   // VMAX 16 pass: 3 CTAs per SM
+constexpr size_t kLaneSmem32 = 110 * 1024;  // VMAX 32 pass: 2 CTAs per SM
 constexpr int kLaneEpoch = 8;     // sequences per lane between bookkeeping phases
 constexpr int kBigRMax = 8;       // k_pack_big: register bins per lane (V <= 256)
 constexpr int kBigWarps = 3584;   // persistent warps of k_pack_big (scratch slots): 148 SMs x 24
@@ -347,7 +349,7 @@ __device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, uint3
 //          limit, an infeasible V_a and V_a + 1) go to the warp queue, which runs the sequential
 //          exact search.
 template <bool STAGED, int VM>
-__global__ void __launch_bounds__(kLaneThreads, 2) k_pack_lanes(PackArgs a, int tc, int mnp, int ncap) {
+__global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(PackArgs a, int tc, int mnp, int ncap) {
   constexpr int NB = 64;  // LPT-order buckets: (class, U) descending
   constexpr unsigned long long kBottom = ~0ull;
   extern __shared__ __align__(16) uint32_t sm[];
@@ -1127,22 +1129,27 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
   // pass 2 (VMAX 32, flagged tasks, compacted records) CTA = one whole iteration
   // two CTAs per SM: ~110 KB of dynamic smem each for the staged iteration + task records
   const size_t stage = (size_t)batch * 4 * (1 + (size_t)k_pad);
-  const size_t budget = 110 * 1024;
-  const bool staged = (batch % 4) == 0 && stage + 512 * 39 <= budget;
-  int ncap = (int)(((staged ? budget - stage : budget) / 39) & ~(size_t)31);
-  ncap = ncap > 2048 ? 2048 : ncap;
-  const size_t recs = (size_t)ncap * 39;  // bytes of task records per CTA
-  const size_t smem = recs + (staged ? stage : 0);
-  const int tc1 = max(1, min(n_cand, ncap / max_np));
+  auto plan = [&](size_t budget, bool& staged, int& ncap, size_t& smem) {
+    staged = (batch % 4) == 0 && stage + 512 * 39 <= budget;
+    ncap = (int)(((staged ? budget - stage : budget) / 39) & ~(size_t)31);
+    ncap = ncap > 2048 ? 2048 : ncap;
+    smem = (size_t)ncap * 39 + (staged ? stage : 0);  // task records + staged iteration
+  };
+  bool st1, st2;
+  int ncap1, ncap2;
+  size_t smem1, smem2;
+  plan(kLaneSmem16, st1, ncap1, smem1);  // three CTAs per SM
+  plan(kLaneSmem32, st2, ncap2, smem2);  // two CTAs per SM
+  const int tc1 = max(1, min(n_cand, ncap1 / max_np));
   dim3 grid1((n_cand + tc1 - 1) / tc1, n_iter);
-  e = staged ? launch_lanes<true, 16>(grid1, smem, s, a, tc1, max_np, ncap)
-             : launch_lanes<false, 16>(grid1, smem, s, a, tc1, max_np, ncap);
+  e = st1 ? launch_lanes<true, 16>(grid1, smem1, s, a, tc1, max_np, ncap1)
+          : launch_lanes<false, 16>(grid1, smem1, s, a, tc1, max_np, ncap1);
   note_launch();
   if (e != cudaSuccess) return record_cuda_error(e);
   const int tc2 = max(1, min(n_cand, 65535 / max_np));
   dim3 grid2((n_cand + tc2 - 1) / tc2, n_iter);
-  e = staged ? launch_lanes<true, 32>(grid2, smem, s, a, tc2, max_np, ncap)
-             : launch_lanes<false, 32>(grid2, smem, s, a, tc2, max_np, ncap);
+  e = st2 ? launch_lanes<true, 32>(grid2, smem2, s, a, tc2, max_np, ncap2)
+          : launch_lanes<false, 32>(grid2, smem2, s, a, tc2, max_np, ncap2);
   note_launch();
   if (e != cudaSuccess) return record_cuda_error(e);
 
