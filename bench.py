@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
+    ap.add_argument("--cpu-seconds", type=float, default=30.0, help="target CPU time of the oracle sample")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu/clocks)")
     ap.add_argument("--trials", type=int, default=0,
                     help="NEXT-1: stage 1 = Alg. 1 with this many random trials per (c,t) (0: HYD-H1 dispatch)")
@@ -125,7 +125,7 @@ def oracle_sample(W, target_s, rng_seed=0, max_cand=None, trials=0, seed=0):
 
     oracle.build()
     rng = np.random.default_rng(rng_seed)
-    ncal, ical = min(W.n_cand, 16), min(2, W.n_iter)
+    ncal, ical = min(W.n_cand, 4 * (os.cpu_count() or 4)), min(2, W.n_iter)
     its = np.sort(rng.choice(W.n_iter, ical, replace=False))
     sub = wl.Workload(W.cfg, W.name, W.lengths[its], W.schemes, W.cand[:ncal], W.cand_np[:ncal], W.k_pad)
     t0 = time.perf_counter()
