@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--trials", type=int, default=0,
                     help="NEXT-1: stage 1 = Alg. 1 with this many random trials per (c,t) (0: HYD-H1 dispatch)")
     ap.add_argument("--seed", type=int, default=2024, help="Alg. 1 permutation seed")
+    ap.add_argument("--candidates", type=int, default=0, help="diagnostics: first N candidates only (0: all)")
     return ap.parse_args()
 
 
@@ -216,7 +217,7 @@ def main():
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
-    W = wl.make_workload(args.config)
+    W = wl.make_workload(args.config, n_cand=args.candidates or None)
     sh = assign.plan_shard(W.n_cand, W.n_iter, world, rank)
     cand = W.cand[sh.cand_lo:sh.cand_hi]
     cand_np = W.cand_np[sh.cand_lo:sh.cand_hi]
@@ -290,7 +291,11 @@ def main():
     ms_local = float(np.sum(step_ms)) / args.steps
     per_kernel /= args.steps
     t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+    rank_ms = [ms_local]
     if world > 1:
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        rank_ms = [float(x.item()) for x in allt]
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     total_ci = W.n_cand * W.n_iter
@@ -341,6 +346,7 @@ def main():
                 "stage1": f"Alg. 1, {args.trials} random trials (NEXT-1)" if args.trials else "HYD-H1 LPT dispatch",
             },
             "kernel_ms": {n: float(x) for n, x in zip(names, per_kernel)},
+            "rank_ms": rank_ms,
             "roofline": roof,
             "gpu_launches": int(launches),
             "clocks": clocks,
