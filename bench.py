@@ -118,6 +118,22 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def sub_workload(W, its, cs):
+    """Iterations ``its`` x candidates ``cs`` of W (ragged workloads keep their CSR layout)."""
+    if not W.ragged:
+        return wl.Workload(W.cfg, W.name, W.lengths[its], W.schemes, W.cand[cs], W.cand_np[cs], W.k_pad)
+    rows = [W.iteration(int(t)) for t in its]
+    off = np.concatenate([[0], np.cumsum([r.size for r in rows])]).astype(np.uint32)
+    return wl.Workload(W.cfg, W.name, np.concatenate(rows).astype(np.uint32), W.schemes, W.cand[cs], W.cand_np[cs],
+                       W.k_pad, offsets=off)
+
+
+def run_oracle(W, **kw):
+    import oracle
+
+    return oracle.assign_batch_ragged(W) if W.ragged else oracle.assign_batch(W, n_threads=0, **kw)
+
+
 # ----------------------------------------------------------------------------- CPU oracle leg
 def oracle_sample(W, target_s, rng_seed=0, max_cand=None, trials=0, seed=0):
     """Time the oracle (as it stands) on a bounded slice of W: a1-a5 for C' candidates x It'
@@ -128,9 +144,9 @@ def oracle_sample(W, target_s, rng_seed=0, max_cand=None, trials=0, seed=0):
     rng = np.random.default_rng(rng_seed)
     ncal, ical = min(W.n_cand, 4 * (os.cpu_count() or 4)), min(2, W.n_iter)
     its = np.sort(rng.choice(W.n_iter, ical, replace=False))
-    sub = wl.Workload(W.cfg, W.name, W.lengths[its], W.schemes, W.cand[:ncal], W.cand_np[:ncal], W.k_pad)
+    sub = sub_workload(W, its, np.arange(ncal))
     t0 = time.perf_counter()
-    oracle.assign_batch(sub, n_threads=0, trials=trials, seed=seed)
+    run_oracle(sub, **({"trials": trials, "seed": seed} if trials else {}))
     per = (time.perf_counter() - t0) / (ncal * ical)  # wall seconds per c-i on all host threads
     want = max(1, int(target_s / max(per, 1e-9)))  # c-i in the sample
     cap = W.n_cand if max_cand is None else min(max_cand, W.n_cand)
@@ -138,9 +154,9 @@ def oracle_sample(W, target_s, rng_seed=0, max_cand=None, trials=0, seed=0):
     n_it = max(1, min(W.n_iter, -(-want // nc)))
     cs = np.sort(rng.choice(W.n_cand, nc, replace=False))
     its = np.sort(rng.choice(W.n_iter, n_it, replace=False))
-    sub = wl.Workload(W.cfg, W.name, W.lengths[its], W.schemes, W.cand[cs], W.cand_np[cs], W.k_pad)
+    sub = sub_workload(W, its, cs)
     t0 = time.perf_counter()
-    oracle.assign_batch(sub, n_threads=0, trials=trials, seed=seed)
+    run_oracle(sub, **({"trials": trials, "seed": seed} if trials else {}))
     dt = time.perf_counter() - t0
     cores = os.cpu_count() or 1
     return {
@@ -168,9 +184,9 @@ def run_reference(args):
     for s in range(args.warmup + args.steps):
         its = np.sort(rng.choice(W.n_iter, 2, replace=False))
         cs = np.sort(rng.choice(W.n_cand, per_step, replace=False))
-        sub = wl.Workload(W.cfg, W.name, W.lengths[its], W.schemes, W.cand[cs], W.cand_np[cs], W.k_pad)
+        sub = sub_workload(W, its, cs)
         t0 = time.perf_counter()
-        oracle.assign_batch(sub, n_threads=0)
+        run_oracle(sub)
         dt = time.perf_counter() - t0
         if s >= args.warmup:
             times.append(dt)
@@ -221,12 +237,20 @@ def main():
     sh = assign.plan_shard(W.n_cand, W.n_iter, world, rank)
     cand = W.cand[sh.cand_lo:sh.cand_hi]
     cand_np = W.cand_np[sh.cand_lo:sh.cand_hi]
-    lens = W.lengths[sh.iter_lo:sh.iter_hi]
-    It_local, C_local = lens.shape[0], cand.shape[0]
+    if W.ragged:  # NEXT-2: token-budget batches; ranks split candidates only
+        assert sh.by != "iter", "ragged workloads shard by candidates"
+        lens = W.lengths
+        It_local = W.n_iter
+        A_rows = [W.iteration(t) for t in range(W.n_iter)]
+    else:
+        lens = W.lengths[sh.iter_lo:sh.iter_hi]
+        It_local = lens.shape[0]
+        A_rows = lens
+    C_local = cand.shape[0]
     A = assign.Assigner(W.schemes, cand, cand_np, It_local, W.batch, W.k_pad, cand_offset=sh.cand_lo, device=dev,
-                        trials=args.trials, seed=args.seed)
+                        trials=args.trials, seed=args.seed, offsets=W.offsets if W.ragged else None)
     len_dev = assign.lengths_to_device(lens, dev)
-    A._lens_host = lens
+    A._lens_host = A_rows
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
@@ -236,6 +260,27 @@ def main():
         It, B, K, kp, Cn = A.n_iter, A.batch, A.n_schemes, A.k_pad, A.n_cand
         if evs:
             evs[0].record(stream)
+        if A.ragged:
+            N = A.n_total
+            hyd.cost_table_ragged(len_dev, It, A.off, N, B, A.schemes, K, kp, A.sorted_len, A.perm, A.cost, A.status)
+            if evs:
+                evs[1].record(stream)
+            hyd.dispatch_ragged(A.sorted_len, A.cost, It, A.off, N, B, kp, A.schemes, K, A.cand, A.cand_np, Cn,
+                                A.max_np, A.pipe, A.lb, A.stats, A.members, A.status, A.disp_ws)
+            if evs:
+                evs[2].record(stream)
+            hyd.pack_ragged(A.sorted_len, A.cost, It, A.off, N, B, kp, A.schemes, K, A.cand, A.cand_np, Cn, A.max_np,
+                            A.pipe, A.stats, A.members, A.mb, A.v, A.ptime, A.makespan, A.status, A.ws)
+            if evs:
+                evs[3].record(stream)
+            hyd.select_best(A.makespan, It, Cn, A.cand_offset, A.key, A.status)
+            if evs:
+                evs[4].record(stream)
+            if sh.needs_reduce:
+                assign.reduce_keys(A.key)
+            if evs:
+                evs[5].record(stream)
+            return
         hyd.cost_table(len_dev, It, B, A.schemes, K, kp, A.sorted_len, A.perm, A.cost, A.status)
         if evs:
             evs[1].record(stream)
@@ -334,7 +379,8 @@ def main():
             "data": "synthetic",
             "config": {
                 "workload": W.name,
-                "batch": W.batch,
+                "batch": (f"ragged: mean {W.n_total / W.n_iter:.1f}, max {W.batch} sequences "
+                          f"({W.meta.get('tokens_per_iteration')} tokens/iteration)") if W.ragged else W.batch,
                 "pipelines": int(W.cand_np.max()),
                 "candidates": W.n_cand,
                 "iterations": W.n_iter,
@@ -382,7 +428,7 @@ def ncu_traffic(cfg, prefix):
 
 def roofline(name, ms, W, A, pk, how, local_ci):
     """Algorithmic work per launch / CUDA-event duration."""
-    B, D = W.batch, int(W.cand_np.max())
+    B, D = (W.n_total / W.n_iter if W.ragged else W.batch), int(W.cand_np.max())
     sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
     alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e9  # int32 lane-ops/s in Gop/s (DESIGN.md §5)
     hbm = float(pk.get("hbm_gbs", 6650.0))
@@ -418,7 +464,8 @@ def run_e2e(args, W, sh, cand, cand_np, lens, world, dev):
 
     from paper_2412_07894_b200 import assign
 
-    H = assign.HostAssigner(W.schemes, cand, cand_np, lens.shape[0], W.batch, W.k_pad, cand_offset=sh.cand_lo,
+    H = assign.HostAssigner(W.schemes, cand, cand_np, W.n_iter if W.ragged else lens.shape[0], W.batch, W.k_pad,
+                            cand_offset=sh.cand_lo, offsets=W.offsets if W.ragged else None,
                             reduce=sh.needs_reduce)
     lh = torch.from_numpy(np.ascontiguousarray(lens).view(np.int32)).pin_memory()
     stream = torch.cuda.current_stream()
@@ -443,7 +490,7 @@ def run_e2e(args, W, sh, cand, cand_np, lens, world, dev):
     ms = float(t.item())
     return {"value": W.n_cand * W.n_iter / (ms / 1000.0), "unit": UNIT,
             "h2d_bytes_per_step": int(lh.numel() * 4 + H.h2d_bytes_fixed), "d2h_bytes_per_step": int(H.d2h_bytes),
-            "ms_per_step": ms, "api": "hyd_assign_host (pinned host buffers)"}
+            "ms_per_step": ms, "api": ("hyd_assign_host_ragged" if W.ragged else "hyd_assign_host") + " (pinned host buffers)"}
 
 
 if __name__ == "__main__":

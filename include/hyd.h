@@ -208,6 +208,53 @@ int hyd_dispatch_alg1(const uint32_t* sorted_len, const uint32_t* cost, int n_it
                       hyd_pipe_stats* stats, uint32_t* members, uint32_t* status, void* ws,
                       size_t ws_bytes, void* stream);
 
+/* ---- NEXT-2: token-budget (ragged) batches ------------------------------
+ * Iteration t holds B_t sequences (1 <= B_t <= batch_max <= HYD_MAX_BATCH): offsets [n_iter+1]
+ * u32 CSR on the DEVICE (offsets[0] = 0, offsets[t+1] - offsets[t] = B_t, offsets[n_iter] =
+ * n_total), lengths len [n_total] concatenated by iteration.  Every iteration-indexed array
+ * keeps its meaning with the row of (t, i) at offsets[t] + i: sorted_len, perm (index within
+ * the iteration) [n_total], cost [n_total][k_pad], pipe [n_cand][n_total] u8,
+ * mb [n_cand][n_total] u16, win_pipe / win_mb [n_total]; members rows have the stride of
+ * batch_max: [n_iter][n_cand][ceil(batch_max/32)][max_np]; lb, stats, v, ptime, makespan and
+ * key are unchanged.  Results are those of the uniform entry points applied to each iteration
+ * separately.  Device faults: an iteration with B_t outside [1, batch_max] sets
+ * HYD_F_BAD_LENGTH (hyd_cost_table_ragged) and its rows are undefined.
+ * Workspaces: hyd_dispatch_workspace(n_iter), hyd_pack_workspace(n_iter, batch_max, n_cand,
+ * max_np); the e2e call takes HOST offsets and checks them synchronously (HYD_E_INVALID). */
+int hyd_cost_table_ragged(const uint32_t* len, int n_iter, const uint32_t* offsets, int n_total,
+                          int batch_max, const hyd_scheme* schemes, int n_schemes, int k_pad,
+                          uint32_t* sorted_len, uint32_t* perm, uint32_t* cost, uint32_t* status,
+                          void* stream);
+int hyd_dispatch_ragged(const uint32_t* sorted_len, const uint32_t* cost, int n_iter,
+                        const uint32_t* offsets, int n_total, int batch_max, int k_pad,
+                        const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
+                        const uint8_t* cand_np, int n_cand, int max_np, uint8_t* pipe, uint64_t* lb,
+                        hyd_pipe_stats* stats, uint32_t* members, uint32_t* status, void* ws,
+                        size_t ws_bytes, void* stream);
+int hyd_pack_ragged(const uint32_t* sorted_len, const uint32_t* cost, int n_iter,
+                    const uint32_t* offsets, int n_total, int batch_max, int k_pad,
+                    const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
+                    const uint8_t* cand_np, int n_cand, int max_np, const uint8_t* pipe,
+                    const hyd_pipe_stats* stats, const uint32_t* members, uint16_t* mb, uint16_t* v,
+                    uint64_t* ptime, uint64_t* makespan, uint32_t* status, void* ws,
+                    size_t ws_bytes, void* stream);
+int hyd_gather_winners_ragged(const int64_t* key, const uint32_t* perm, const uint8_t* pipe,
+                              const uint16_t* mb, const uint16_t* v, const uint64_t* ptime,
+                              int n_iter, const uint32_t* offsets, int n_total, int batch_max,
+                              int n_cand, int cand_offset, uint8_t* win_pipe, uint16_t* win_mb,
+                              uint16_t* win_v, uint64_t* win_ptime, void* stream);
+size_t hyd_assign_workspace_ragged(int n_iter, int n_total, int batch_max, int n_schemes, int k_pad,
+                                   int n_cand, int max_np);
+size_t hyd_assign_key_offset_ragged(int n_iter, int n_total, int batch_max, int n_schemes,
+                                    int k_pad, int n_cand, int max_np);
+int hyd_assign_host_ragged(const uint32_t* len_host, int n_iter, const uint32_t* offsets_host,
+                           int batch_max, const hyd_scheme* schemes_host, int n_schemes, int k_pad,
+                           const uint8_t* cand_host, const uint8_t* cand_np_host, int n_cand,
+                           int cand_offset, int64_t* key_host, uint8_t* win_pipe_host,
+                           uint16_t* win_mb_host, uint16_t* win_v_host, uint64_t* win_ptime_host,
+                           uint32_t* status_host, hyd_reduce_fn reduce, void* reduce_user, void* ws,
+                           size_t ws_bytes, void* stream);
+
 /* ---- host utilities --------------------------------------------------------------------
  * hyd_check_candidates: HOST tables; HYD_OK, HYD_E_INVALID or HYD_E_NOT_CANONICAL; writes
  * max over c of cand_np to *max_np_out (if non-null). */

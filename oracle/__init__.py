@@ -285,3 +285,56 @@ def alg1_dispatch(sorted_len, cost_tab, schemes, cand_row, seed, t, trials):
         _sch_ptr(schemes), row, len(cand_row), int(seed), int(t), int(trials), pipe, C.byref(lb), C.byref(bt),
     )
     return bool(ok), pipe, int(lb.value), int(bt.value)
+
+
+# ------------------------------------------------------------------ NEXT-2 (ragged batches)
+def _iteration_workload(W, t):
+    """Iteration t of a ragged workload as a one-iteration uniform workload."""
+    import workload as wl
+
+    return wl.Workload(W.cfg, W.name, np.ascontiguousarray(W.iteration(t))[None, :], W.schemes, W.cand,
+                       W.cand_np, W.k_pad)
+
+
+def assign_batch_ragged(W, n_threads=0, cand_offset=0):
+    """Steps 1-7 on token-budget batches (CSR ``W.offsets``): by definition the uniform method
+    applied to each iteration separately (include/hyd.h NEXT-2).  Row layouts as the GPU's:
+    sorted_len/perm [N], cost [N][k_pad], pipe/mb [C][N], lb [C][It], v/ptime [C][It][32],
+    makespan [It][C], key [It]."""
+    It, N, Cn, kp = W.n_iter, W.n_total, W.n_cand, W.k_pad
+    off = W.offsets.astype(np.int64)
+    o = dict(
+        sorted_len=np.empty(N, np.uint32), perm=np.empty(N, np.uint32), cost=np.empty((N, kp), np.uint32),
+        pipe=np.empty((Cn, N), np.uint8), lb=np.empty((Cn, It), np.uint64), mb=np.empty((Cn, N), np.uint16),
+        v=np.empty((Cn, It, 32), np.uint16), ptime=np.empty((Cn, It, 32), np.uint64),
+        makespan=np.empty((It, Cn), np.uint64), key=np.empty(It, np.int64), status=0,
+    )
+    for t in range(It):
+        a, b = off[t], off[t + 1]
+        r = assign_batch(_iteration_workload(W, t), n_threads=n_threads, cand_offset=cand_offset)
+        o["sorted_len"][a:b] = r["sorted_len"][0]
+        o["perm"][a:b] = r["perm"][0]
+        o["cost"][a:b] = r["cost"][0]
+        o["pipe"][:, a:b] = r["pipe"][:, 0]
+        o["mb"][:, a:b] = r["mb"][:, 0]
+        o["lb"][:, t] = r["lb"][:, 0]
+        o["v"][:, t] = r["v"][:, 0]
+        o["ptime"][:, t] = r["ptime"][:, 0]
+        o["makespan"][t] = r["makespan"][0]
+        o["key"][t] = r["key"][0]
+        o["status"] |= r["status"]
+    return o
+
+
+def assign_pairs_ragged(W, pairs_c, pairs_t, n_threads=0):
+    """Outputs for selected (c,t) pairs of a ragged workload; row r has the pair's B_t entries."""
+    pc = np.asarray(pairs_c, np.int64)
+    pt = np.asarray(pairs_t, np.int64)
+    out = [None] * pc.size
+    for t in np.unique(pt):
+        idx = np.nonzero(pt == t)[0]
+        Wt = _iteration_workload(W, int(t))
+        r = assign_pairs(Wt, pc[idx], np.zeros(idx.size, np.int64), n_threads=n_threads)
+        for q, i in enumerate(idx):
+            out[i] = {k: r[k][q] for k in ("pipe", "lb", "mb", "v", "ptime", "makespan")}
+    return out

@@ -72,10 +72,12 @@ class Assigner:
     ``cand_np`` [C] u8 -- this rank's candidates, global index = cand_offset + local.
     ``trials`` > 0 replaces the HYD-H1 dispatch by Alg. 1 with that many random trials per
     (c,t) (NEXT-1, include/hyd.h hyd_dispatch_alg1), its permutations drawn from ``seed``.
+    ``offsets`` (host CSR [It + 1], NEXT-2): ragged token-budget batches; ``batch`` is then the
+    largest batch and every iteration-indexed array has ``offsets[-1]`` rows.
     """
 
     def __init__(self, schemes, cand, cand_np, n_iter, batch, k_pad, cand_offset=0, device=None, trials=0,
-                 seed=0):
+                 seed=0, offsets=None):
         import torch
 
         self.torch = torch
@@ -102,14 +104,29 @@ class Assigner:
         self.cand_np = torch.from_numpy(np.ascontiguousarray(cand_np, dtype=np.uint8)).to(dev)
         It, B, Cn, kp = self.n_iter, self.batch, self.n_cand, self.k_pad
         i32 = torch.int32  # u32 buffers are carried as int32 storage
-        self.sorted_len = torch.empty((It, B), dtype=i32, device=dev)
-        self.perm = torch.empty((It, B), dtype=i32, device=dev)
-        self.cost = torch.empty((It, B, kp), dtype=i32, device=dev)
-        self.pipe = torch.empty((Cn, It, B), dtype=u8, device=dev)
+        self.ragged = offsets is not None
+        if self.ragged:
+            if trials:
+                raise hyd.HydError("Alg. 1 (trials) runs on uniform batches only")
+            off = np.ascontiguousarray(offsets, dtype=np.uint32)
+            assert off.shape == (It + 1,) and off[0] == 0 and (np.diff(off.astype(np.int64)) >= 1).all()
+            assert int(np.diff(off.astype(np.int64)).max()) <= B
+            self.offsets_host = off
+            self.off = torch.from_numpy(off.view(np.int32).copy()).to(dev)
+            self.n_total = int(off[-1])
+            rows = (self.n_total,)
+        else:
+            self.n_total = It * B
+            rows = (It, B)
+        N = self.n_total
+        self.sorted_len = torch.empty(rows, dtype=i32, device=dev)
+        self.perm = torch.empty(rows, dtype=i32, device=dev)
+        self.cost = torch.empty(rows + (kp,), dtype=i32, device=dev)
+        self.pipe = torch.empty((Cn, N) if self.ragged else (Cn, It, B), dtype=u8, device=dev)
         self.lb = torch.empty((Cn, It), dtype=torch.int64, device=dev)
         self.stats = torch.empty((Cn, It, self.max_np, hyd.PIPE_STATS_BYTES), dtype=u8, device=dev)
         self.members = torch.empty((It, Cn, (B + 31) // 32, self.max_np), dtype=i32, device=dev)
-        self.mb = torch.empty((Cn, It, B), dtype=torch.int16, device=dev)
+        self.mb = torch.empty((Cn, N) if self.ragged else (Cn, It, B), dtype=torch.int16, device=dev)
         self.v = torch.empty((Cn, It, hyd.MAX_PIPES), dtype=torch.int16, device=dev)
         self.ptime = torch.empty((Cn, It, hyd.MAX_PIPES), dtype=torch.int64, device=dev)
         self.makespan = torch.empty((It, Cn), dtype=torch.int64, device=dev)
@@ -126,6 +143,18 @@ class Assigner:
     # a1-a5; ``len_dev`` int32/uint32-bit tensor [It][B] on the device
     def run(self, len_dev, stream=None):
         It, B, K, kp, Cn = self.n_iter, self.batch, self.n_schemes, self.k_pad, self.n_cand
+        if self.ragged:  # NEXT-2: token-budget batches (CSR offsets)
+            N = self.n_total
+            hyd.cost_table_ragged(len_dev, It, self.off, N, B, self.schemes, K, kp, self.sorted_len, self.perm,
+                                  self.cost, self.status, stream)
+            hyd.dispatch_ragged(self.sorted_len, self.cost, It, self.off, N, B, kp, self.schemes, K, self.cand,
+                                self.cand_np, Cn, self.max_np, self.pipe, self.lb, self.stats, self.members,
+                                self.status, self.disp_ws, stream)
+            hyd.pack_ragged(self.sorted_len, self.cost, It, self.off, N, B, kp, self.schemes, K, self.cand,
+                            self.cand_np, Cn, self.max_np, self.pipe, self.stats, self.members, self.mb, self.v,
+                            self.ptime, self.makespan, self.status, self.ws, stream)
+            hyd.select_best(self.makespan, It, Cn, self.cand_offset, self.key, self.status, stream)
+            return self.key
         hyd.cost_table(len_dev, It, B, self.schemes, K, kp, self.sorted_len, self.perm, self.cost, self.status, stream)
         if self.trials:
             hyd.alg1_permutations(self.seed, It, B, self.trials, self.order, stream)
@@ -155,13 +184,13 @@ class Assigner:
     def dispatch_evals(self, lengths) -> int:
         """Sum over feasible (c,t) of sum_i J_i (feasible pipelines per sequence): the
         dispatch's algorithmic evaluation count, from the host tables (no method arithmetic)."""
-        L = np.sort(np.asarray(lengths, dtype=np.int64), axis=1)  # ascending per t
+        rows = [np.sort(np.asarray(r, dtype=np.int64)) for r in lengths]  # ascending per t (ragged ok)
         ml_k = self._ml_k  # MaxLen per scheme
         # cnt[k][t] = #{i : l_i <= MaxLen_k}
-        cnt = np.stack([np.array([np.searchsorted(L[t], m, side="right") for t in range(L.shape[0])])
-                        for m in ml_k])
+        cnt = np.stack([np.array([np.searchsorted(r, m, side="right") for r in rows]) for m in ml_k])
         per = self._mult @ cnt  # [C][It]
-        feas = L[:, -1][None, :] <= self._ml[:, 0][:, None]
+        longest = np.array([r[-1] for r in rows])
+        feas = longest[None, :] <= self._ml[:, 0][:, None]
         return int(per[feas].sum())
 
     def status_bits(self) -> int:
@@ -208,26 +237,35 @@ class HostAssigner:
     sequence order, one stream synchronisation.
     """
 
-    def __init__(self, schemes, cand, cand_np, n_iter, batch, k_pad, cand_offset=0, group=None, reduce=False):
+    def __init__(self, schemes, cand, cand_np, n_iter, batch, k_pad, cand_offset=0, group=None, reduce=False,
+                 offsets=None):
         import torch
 
         self.torch = torch
         self.n_iter, self.batch, self.k_pad = int(n_iter), int(batch), int(k_pad)
+        # NEXT-2: ragged batches -- host CSR offsets [It + 1]; ``batch`` is the largest batch
+        self.offsets = None if offsets is None else np.ascontiguousarray(offsets, dtype=np.uint32)
+        self.n_total = int(self.offsets[-1]) if self.offsets is not None else self.n_iter * self.batch
         self.schemes = np.ascontiguousarray(schemes)
         self.cand = np.ascontiguousarray(cand, dtype=np.uint8)
         self.cand_np = np.ascontiguousarray(cand_np, dtype=np.uint8)
         self.n_cand = int(self.cand.shape[0])
         self.cand_offset = int(cand_offset)
         self.max_np = hyd.check_candidates(self.cand, self.cand_np, self.schemes) if self.n_cand else 1
-        args = (self.n_iter, self.batch, len(self.schemes), self.k_pad, self.n_cand, self.max_np)
-        self.ws = torch.empty((hyd.assign_workspace(*args),), dtype=torch.uint8, device="cuda")
-        koff = hyd.assign_key_offset(*args)
+        if self.offsets is None:
+            args = (self.n_iter, self.batch, len(self.schemes), self.k_pad, self.n_cand, self.max_np)
+            wsz, koff = hyd.assign_workspace(*args), hyd.assign_key_offset(*args)
+        else:
+            args = (self.n_iter, self.n_total, self.batch, len(self.schemes), self.k_pad, self.n_cand, self.max_np)
+            wsz, koff = hyd.assign_workspace_ragged(*args), hyd.assign_key_offset_ragged(*args)
+        self.ws = torch.empty((wsz,), dtype=torch.uint8, device="cuda")
         self.key_view = self.ws[koff : koff + 8 * self.n_iter].view(torch.int64)
         pin = dict(pin_memory=True)
         It, B = self.n_iter, self.batch
+        rows = (It, B) if self.offsets is None else (self.n_total,)
         self.key = torch.empty((It,), dtype=torch.int64, **pin)
-        self.win_pipe = torch.empty((It, B), dtype=torch.uint8, **pin)
-        self.win_mb = torch.empty((It, B), dtype=torch.int16, **pin)
+        self.win_pipe = torch.empty(rows, dtype=torch.uint8, **pin)
+        self.win_mb = torch.empty(rows, dtype=torch.int16, **pin)
         self.win_v = torch.empty((It, hyd.MAX_PIPES), dtype=torch.int16, **pin)
         self.win_ptime = torch.empty((It, hyd.MAX_PIPES), dtype=torch.int64, **pin)
         self.status = torch.zeros((1,), dtype=torch.int32, **pin)
@@ -247,10 +285,13 @@ class HostAssigner:
         self._sch = torch.from_numpy(schemes_bytes(self.schemes).copy()).pin_memory()
         self._cand = torch.from_numpy(self.cand.copy()).pin_memory()
         self._cnp = torch.from_numpy(self.cand_np.copy()).pin_memory()
+        self._off = (torch.from_numpy(self.offsets.view(np.int32).copy()).pin_memory()
+                     if self.offsets is not None else None)
 
     @property
     def h2d_bytes_fixed(self) -> int:
-        return self._sch.numel() + self._cand.numel() + self._cnp.numel()
+        return self._sch.numel() + self._cand.numel() + self._cnp.numel() + (
+            self._off.numel() * 4 if self._off is not None else 0)
 
     @property
     def d2h_bytes(self) -> int:
@@ -258,8 +299,17 @@ class HostAssigner:
                                                           self.win_ptime, self.status))
 
     def __call__(self, len_host, stream=None):
-        """``len_host``: pinned int32 torch tensor [It][B] (u32 bit pattern)."""
+        """``len_host``: pinned int32 torch tensor [It][B] (u32 bit pattern), [N_total] if ragged."""
         It, B = self.n_iter, self.batch
+        if self.offsets is not None:
+            assert len_host.is_pinned() and tuple(len_host.shape) == (self.n_total,)
+            hyd.assign_host_ragged(
+                len_host.data_ptr(), It, self._off.data_ptr(), B, self._sch.data_ptr(), len(self.schemes),
+                self.k_pad, self._cand.data_ptr(), self._cnp.data_ptr(), self.n_cand, self.cand_offset,
+                self.key.data_ptr(), self.win_pipe.data_ptr(), self.win_mb.data_ptr(), self.win_v.data_ptr(),
+                self.win_ptime.data_ptr(), self.status.data_ptr(), self._cb, self.ws, stream,
+            )
+            return self.key
         assert len_host.is_pinned() and tuple(len_host.shape) == (It, B)
         hyd.assign_host(
             len_host.data_ptr(), It, B, self._sch.data_ptr(), len(self.schemes), self.k_pad, self._cand.data_ptr(),

@@ -63,7 +63,7 @@ __global__ void k_alg1_perm(uint64_t seed, int n_iter, int batch, int trials,
   }
 }
 
-int launch_iter_bound(const uint32_t* cost, int n_iter, int batch, int k_pad,
+int launch_iter_bound(const uint32_t* cost, int n_iter, int batch, const uint32_t* off, int k_pad,
                       const hyd_scheme* schemes, int n_schemes, uint64_t* bound, cudaStream_t s);
 
 __host__ __device__ constexpr int alg1_sh(int dp) {
@@ -401,7 +401,7 @@ static cudaError_t launch_alg1_dp(const uint32_t* sorted_len, const uint32_t* co
                                   uint64_t* best, uint8_t* pipe, uint64_t* lb,
                                   hyd_pipe_stats* stats, uint32_t* members, uint32_t* status,
                                   cudaStream_t s) {
-  if (launch_iter_bound(cost, n_iter, batch, k_pad, schemes, n_schemes, bound, s) != HYD_OK)
+  if (launch_iter_bound(cost, n_iter, batch, nullptr, k_pad, schemes, n_schemes, bound, s) != HYD_OK)
     return cudaGetLastError();
   cudaError_t e = cudaMemsetAsync(best, 0xFF, (size_t)n_cand * n_iter * 8, s);
   if (e != cudaSuccess) return e;

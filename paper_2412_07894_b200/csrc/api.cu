@@ -7,21 +7,21 @@
 
 namespace hyd {
 
-int launch_sort_cost(const uint32_t*, int, int, const hyd_scheme*, int, int, uint32_t*, uint32_t*,
+int launch_sort_cost(const uint32_t*, int, int, const uint32_t*, const hyd_scheme*, int, int, uint32_t*, uint32_t*,
                      uint32_t*, uint32_t*, cudaStream_t);
 size_t dispatch_workspace(int);
-int launch_dispatch(const uint32_t*, const uint32_t*, int, int, int, const hyd_scheme*, int,
+int launch_dispatch(const uint32_t*, const uint32_t*, int, int, const uint32_t*, size_t, int, const hyd_scheme*, int,
                     const uint8_t*, const uint8_t*, int, int, uint8_t*, uint64_t*, hyd_pipe_stats*,
                     uint32_t*, uint32_t*, void*, cudaStream_t);
 size_t pack_workspace(int, int, int, int);
-int launch_pack(const uint32_t*, const uint32_t*, int, int, int, const hyd_scheme*, int,
+int launch_pack(const uint32_t*, const uint32_t*, int, int, const uint32_t*, size_t, int, const hyd_scheme*, int,
                 const uint8_t*, const uint8_t*, int, int, const uint8_t*, const hyd_pipe_stats*,
                 const uint32_t*, uint16_t*, uint16_t*, uint64_t*, uint64_t*, uint32_t*, void*, size_t,
                 cudaStream_t);
 int launch_select(const uint64_t*, int, int, int, int64_t*, uint32_t*, cudaStream_t);
 int launch_gather(const int64_t*, const uint32_t*, const uint8_t*, const uint16_t*, const uint16_t*,
-                  const uint64_t*, int, int, int, int, uint8_t*, uint16_t*, uint16_t*, uint64_t*,
-                  cudaStream_t);
+                  const uint64_t*, int, int, const uint32_t*, size_t, int, int, uint8_t*, uint16_t*,
+                  uint16_t*, uint64_t*, cudaStream_t);
 
 int launch_alg1_perm(uint64_t, int, int, int, uint16_t*, cudaStream_t);
 size_t alg1_workspace(int);
@@ -53,39 +53,42 @@ static bool cand_ok(int n_cand, int max_np) {
 static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct AssignLayout {
-  size_t len, schemes, cand, cand_np, sorted, perm, cost, pipe, lb, stats, members, mb, v, ptime, makespan, key,
+  size_t off, len, schemes, cand, cand_np, sorted, perm, cost, pipe, lb, stats, members, mb, v, ptime, makespan, key,
       status, win_pipe, win_mb, win_v, win_ptime, disp_ws, pack_ws, pack_bytes, total;
 };
 
-static AssignLayout assign_layout(int n_iter, int batch, int n_schemes, int k_pad, int n_cand,
-                                  int max_np) {
+// n_total: rows of the iteration-indexed arrays (n_iter * batch for uniform batches); batch: the
+// largest batch (member row stride, workspace sizing)
+static AssignLayout assign_layout(int n_iter, size_t n_total, int batch, int n_schemes, int k_pad,
+                                  int n_cand, int max_np) {
   AssignLayout L;
-  const size_t It = (size_t)n_iter, B = (size_t)batch, Cn = (size_t)n_cand;
+  const size_t It = (size_t)n_iter, B = (size_t)batch, Cn = (size_t)n_cand, N = n_total;
   size_t o = 0;
   auto put = [&](size_t bytes) {
     const size_t at = o;
     o += al(bytes);
     return at;
   };
-  L.len = put(It * B * 4);
+  L.off = put((It + 1) * 4);
+  L.len = put(N * 4);
   L.schemes = put((size_t)n_schemes * sizeof(hyd_scheme));
   L.cand = put(Cn * HYD_MAX_PIPES);
   L.cand_np = put(Cn);
-  L.sorted = put(It * B * 4);
-  L.perm = put(It * B * 4);
-  L.cost = put(It * B * (size_t)k_pad * 4);
-  L.pipe = put(Cn * It * B);
+  L.sorted = put(N * 4);
+  L.perm = put(N * 4);
+  L.cost = put(N * (size_t)k_pad * 4);
+  L.pipe = put(Cn * N);
   L.lb = put(Cn * It * 8);
   L.stats = put(Cn * It * (size_t)max_np * sizeof(hyd_pipe_stats));
   L.members = put(Cn * It * (size_t)max_np * ((B + 31) / 32) * 4);
-  L.mb = put(Cn * It * B * 2);
+  L.mb = put(Cn * N * 2);
   L.v = put(Cn * It * HYD_MAX_PIPES * 2);
   L.ptime = put(Cn * It * HYD_MAX_PIPES * 8);
   L.makespan = put(It * Cn * 8);
   L.key = put(It * 8);
   L.status = put(4);
-  L.win_pipe = put(It * B);
-  L.win_mb = put(It * B * 2);
+  L.win_pipe = put(N);
+  L.win_mb = put(N * 2);
   L.win_v = put(It * HYD_MAX_PIPES * 2);
   L.win_ptime = put(It * HYD_MAX_PIPES * 8);
   L.disp_ws = put(dispatch_workspace(n_iter));
@@ -151,8 +154,19 @@ int hyd_cost_table(const uint32_t* len, int n_iter, int batch, const hyd_scheme*
   if (!len || !schemes || !sorted_len || !perm || !cost || !status ||
       !common_ok(n_iter, batch, n_schemes, k_pad))
     return HYD_E_INVALID;
-  return launch_sort_cost(len, n_iter, batch, schemes, n_schemes, k_pad, sorted_len, perm, cost,
-                          status, (cudaStream_t)stream);
+  return launch_sort_cost(len, n_iter, batch, nullptr, schemes, n_schemes, k_pad, sorted_len, perm,
+                          cost, status, (cudaStream_t)stream);
+}
+
+int hyd_cost_table_ragged(const uint32_t* len, int n_iter, const uint32_t* offsets, int n_total,
+                          int batch_max, const hyd_scheme* schemes, int n_schemes, int k_pad,
+                          uint32_t* sorted_len, uint32_t* perm, uint32_t* cost, uint32_t* status,
+                          void* stream) {
+  if (!len || !offsets || !schemes || !sorted_len || !perm || !cost || !status || n_total < 0 ||
+      !common_ok(n_iter, batch_max, n_schemes, k_pad))
+    return HYD_E_INVALID;
+  return launch_sort_cost(len, n_iter, batch_max, offsets, schemes, n_schemes, k_pad, sorted_len,
+                          perm, cost, status, (cudaStream_t)stream);
 }
 
 size_t hyd_dispatch_workspace(int n_iter) {
@@ -169,8 +183,25 @@ int hyd_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, i
       !common_ok(n_iter, batch, n_schemes, k_pad) || !cand_ok(n_cand, max_np))
     return HYD_E_INVALID;
   if (!ws || ws_bytes < dispatch_workspace(n_iter)) return HYD_E_WORKSPACE;
-  return launch_dispatch(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np,
-                         n_cand, max_np, pipe, lb, stats, members, status, ws, (cudaStream_t)stream);
+  return launch_dispatch(sorted_len, cost, n_iter, batch, nullptr, (size_t)n_iter * batch, k_pad,
+                         schemes, n_schemes, cand, cand_np, n_cand, max_np, pipe, lb, stats, members,
+                         status, ws, (cudaStream_t)stream);
+}
+
+int hyd_dispatch_ragged(const uint32_t* sorted_len, const uint32_t* cost, int n_iter,
+                        const uint32_t* offsets, int n_total, int batch_max, int k_pad,
+                        const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
+                        const uint8_t* cand_np, int n_cand, int max_np, uint8_t* pipe, uint64_t* lb,
+                        hyd_pipe_stats* stats, uint32_t* members, uint32_t* status, void* ws,
+                        size_t ws_bytes, void* stream) {
+  if (!sorted_len || !cost || !offsets || !schemes || !cand || !cand_np || !pipe || !lb || !stats ||
+      !members || !status || n_total < 0 || !common_ok(n_iter, batch_max, n_schemes, k_pad) ||
+      !cand_ok(n_cand, max_np))
+    return HYD_E_INVALID;
+  if (!ws || ws_bytes < dispatch_workspace(n_iter)) return HYD_E_WORKSPACE;
+  return launch_dispatch(sorted_len, cost, n_iter, batch_max, offsets, (size_t)n_total, k_pad,
+                         schemes, n_schemes, cand, cand_np, n_cand, max_np, pipe, lb, stats, members,
+                         status, ws, (cudaStream_t)stream);
 }
 
 size_t hyd_alg1_workspace(int n_iter) {
@@ -217,9 +248,26 @@ int hyd_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int b
       !cand_ok(n_cand, max_np))
     return HYD_E_INVALID;
   if (!ws || ws_bytes < pack_workspace(n_iter, batch, n_cand, max_np)) return HYD_E_WORKSPACE;
-  return launch_pack(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np,
-                     n_cand, max_np, pipe, stats, members, mb, v, ptime, makespan, status, ws, ws_bytes,
-                     (cudaStream_t)stream);
+  return launch_pack(sorted_len, cost, n_iter, batch, nullptr, (size_t)n_iter * batch, k_pad,
+                     schemes, n_schemes, cand, cand_np, n_cand, max_np, pipe, stats, members, mb, v,
+                     ptime, makespan, status, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int hyd_pack_ragged(const uint32_t* sorted_len, const uint32_t* cost, int n_iter,
+                    const uint32_t* offsets, int n_total, int batch_max, int k_pad,
+                    const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
+                    const uint8_t* cand_np, int n_cand, int max_np, const uint8_t* pipe,
+                    const hyd_pipe_stats* stats, const uint32_t* members, uint16_t* mb, uint16_t* v,
+                    uint64_t* ptime, uint64_t* makespan, uint32_t* status, void* ws,
+                    size_t ws_bytes, void* stream) {
+  if (!sorted_len || !cost || !offsets || !schemes || !cand || !cand_np || !pipe || !stats ||
+      !members || !mb || !v || !ptime || !makespan || !status || n_total < 0 ||
+      !common_ok(n_iter, batch_max, n_schemes, k_pad) || !cand_ok(n_cand, max_np))
+    return HYD_E_INVALID;
+  if (!ws || ws_bytes < pack_workspace(n_iter, batch_max, n_cand, max_np)) return HYD_E_WORKSPACE;
+  return launch_pack(sorted_len, cost, n_iter, batch_max, offsets, (size_t)n_total, k_pad, schemes,
+                     n_schemes, cand, cand_np, n_cand, max_np, pipe, stats, members, mb, v, ptime,
+                     makespan, status, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 int hyd_select_best(const uint64_t* makespan, int n_iter, int n_cand, int cand_offset,
@@ -238,25 +286,53 @@ int hyd_gather_winners(const int64_t* key, const uint32_t* perm, const uint8_t* 
       !win_ptime || n_iter < 0 || batch < 1 || batch > HYD_MAX_BATCH || n_cand < 0 ||
       cand_offset < 0)
     return HYD_E_INVALID;
-  return launch_gather(key, perm, pipe, mb, v, ptime, n_iter, batch, n_cand, cand_offset, win_pipe,
-                       win_mb, win_v, win_ptime, (cudaStream_t)stream);
+  return launch_gather(key, perm, pipe, mb, v, ptime, n_iter, batch, nullptr, (size_t)n_iter * batch,
+                       n_cand, cand_offset, win_pipe, win_mb, win_v, win_ptime, (cudaStream_t)stream);
+}
+
+int hyd_gather_winners_ragged(const int64_t* key, const uint32_t* perm, const uint8_t* pipe,
+                              const uint16_t* mb, const uint16_t* v, const uint64_t* ptime,
+                              int n_iter, const uint32_t* offsets, int n_total, int batch_max,
+                              int n_cand, int cand_offset, uint8_t* win_pipe, uint16_t* win_mb,
+                              uint16_t* win_v, uint64_t* win_ptime, void* stream) {
+  if (!key || !perm || !pipe || !mb || !v || !ptime || !offsets || !win_pipe || !win_mb ||
+      !win_v || !win_ptime || n_iter < 0 || n_total < 0 || batch_max < 1 ||
+      batch_max > HYD_MAX_BATCH || n_cand < 0 || cand_offset < 0)
+    return HYD_E_INVALID;
+  return launch_gather(key, perm, pipe, mb, v, ptime, n_iter, batch_max, offsets, (size_t)n_total,
+                       n_cand, cand_offset, win_pipe, win_mb, win_v, win_ptime, (cudaStream_t)stream);
 }
 
 size_t hyd_assign_workspace(int n_iter, int batch, int n_schemes, int k_pad, int n_cand, int max_np) {
   if (!common_ok(n_iter, batch, n_schemes, k_pad) || !cand_ok(n_cand, max_np)) return 0;
-  return assign_layout(n_iter, batch, n_schemes, k_pad, n_cand, max_np).total;
+  return assign_layout(n_iter, (size_t)n_iter * batch, batch, n_schemes, k_pad, n_cand, max_np).total;
 }
 
 size_t hyd_assign_key_offset(int n_iter, int batch, int n_schemes, int k_pad, int n_cand, int max_np) {
-  return assign_layout(n_iter, batch, n_schemes, k_pad, n_cand, max_np).key;
+  return assign_layout(n_iter, (size_t)n_iter * batch, batch, n_schemes, k_pad, n_cand, max_np).key;
 }
 
-int hyd_assign_host(const uint32_t* len_host, int n_iter, int batch, const hyd_scheme* schemes_host,
-                    int n_schemes, int k_pad, const uint8_t* cand_host, const uint8_t* cand_np_host,
-                    int n_cand, int cand_offset, int64_t* key_host, uint8_t* win_pipe_host,
-                    uint16_t* win_mb_host, uint16_t* win_v_host, uint64_t* win_ptime_host,
-                    uint32_t* status_host, hyd_reduce_fn reduce, void* reduce_user, void* ws,
-                    size_t ws_bytes, void* stream) {
+size_t hyd_assign_workspace_ragged(int n_iter, int n_total, int batch_max, int n_schemes, int k_pad,
+                                   int n_cand, int max_np) {
+  if (n_total < 0 || !common_ok(n_iter, batch_max, n_schemes, k_pad) || !cand_ok(n_cand, max_np))
+    return 0;
+  return assign_layout(n_iter, (size_t)n_total, batch_max, n_schemes, k_pad, n_cand, max_np).total;
+}
+
+size_t hyd_assign_key_offset_ragged(int n_iter, int n_total, int batch_max, int n_schemes,
+                                    int k_pad, int n_cand, int max_np) {
+  return assign_layout(n_iter, (size_t)n_total, batch_max, n_schemes, k_pad, n_cand, max_np).key;
+}
+
+// e2e host-buffer call; offsets_host == nullptr: uniform batches of `batch`, else CSR offsets
+// [n_iter + 1] of ragged batches whose largest is `batch`
+static int assign_host_impl(const uint32_t* len_host, int n_iter, const uint32_t* offsets_host,
+                            int batch, const hyd_scheme* schemes_host, int n_schemes, int k_pad,
+                            const uint8_t* cand_host, const uint8_t* cand_np_host, int n_cand,
+                            int cand_offset, int64_t* key_host, uint8_t* win_pipe_host,
+                            uint16_t* win_mb_host, uint16_t* win_v_host, uint64_t* win_ptime_host,
+                            uint32_t* status_host, hyd_reduce_fn reduce, void* reduce_user,
+                            void* ws, size_t ws_bytes, void* stream) {
   if (!len_host || !schemes_host || !cand_host || !cand_np_host || !key_host || !win_pipe_host ||
       !win_mb_host || !win_v_host || !win_ptime_host || !status_host ||
       !common_ok(n_iter, batch, n_schemes, k_pad) || cand_offset < 0 ||
@@ -266,12 +342,21 @@ int hyd_assign_host(const uint32_t* len_host, int n_iter, int batch, const hyd_s
   int rc = hyd_check_candidates(cand_host, cand_np_host, n_cand, schemes_host, n_schemes, &max_np);
   if (rc != HYD_OK) return rc;
   if (n_cand == 0) max_np = 1;
-  const AssignLayout L = assign_layout(n_iter, batch, n_schemes, k_pad, n_cand, max_np);
+  size_t n_total = (size_t)n_iter * batch;
+  if (offsets_host) {  // host-side CSR check: 0 = off[0] <= ... , 1 <= B_t <= batch
+    if (offsets_host[0] != 0) return HYD_E_INVALID;
+    for (int t = 0; t < n_iter; ++t) {
+      const uint32_t d = offsets_host[t + 1] - offsets_host[t];
+      if (offsets_host[t + 1] < offsets_host[t] || d < 1 || d > (uint32_t)batch) return HYD_E_INVALID;
+    }
+    n_total = offsets_host[n_iter];
+  }
+  const AssignLayout L = assign_layout(n_iter, n_total, batch, n_schemes, k_pad, n_cand, max_np);
   if (!ws || ws_bytes < L.total) return HYD_E_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
   char* w = static_cast<char*>(ws);
   auto D = [&](size_t off) { return static_cast<void*>(w + off); };
-  const size_t It = (size_t)n_iter, B = (size_t)batch, Cn = (size_t)n_cand;
+  const size_t It = (size_t)n_iter, N = n_total, Cn = (size_t)n_cand;
   cudaError_t e;
 #define HYD_CK(x)                                      \
   do {                                                 \
@@ -279,7 +364,12 @@ int hyd_assign_host(const uint32_t* len_host, int n_iter, int batch, const hyd_s
     if (e != cudaSuccess) return record_cuda_error(e); \
   } while (0)
   HYD_CK(cudaMemsetAsync(D(L.status), 0, 4, s));
-  HYD_CK(cudaMemcpyAsync(D(L.len), len_host, It * B * 4, cudaMemcpyHostToDevice, s));
+  HYD_CK(cudaMemcpyAsync(D(L.len), len_host, N * 4, cudaMemcpyHostToDevice, s));
+  const uint32_t* off = nullptr;
+  if (offsets_host) {
+    HYD_CK(cudaMemcpyAsync(D(L.off), offsets_host, (It + 1) * 4, cudaMemcpyHostToDevice, s));
+    off = static_cast<const uint32_t*>(D(L.off));
+  }
   HYD_CK(cudaMemcpyAsync(D(L.schemes), schemes_host, (size_t)n_schemes * sizeof(hyd_scheme),
                          cudaMemcpyHostToDevice, s));
   if (Cn) {
@@ -299,33 +389,59 @@ int hyd_assign_host(const uint32_t* len_host, int n_iter, int batch, const hyd_s
   auto* pt = static_cast<uint64_t*>(D(L.ptime));
   auto* ms = static_cast<uint64_t*>(D(L.makespan));
   auto* key = static_cast<int64_t*>(D(L.key));
-  rc = launch_sort_cost(static_cast<const uint32_t*>(D(L.len)), n_iter, batch, sch, n_schemes, k_pad,
-                        sorted, perm, cost, st, s);
+  rc = launch_sort_cost(static_cast<const uint32_t*>(D(L.len)), n_iter, batch, off, sch, n_schemes,
+                        k_pad, sorted, perm, cost, st, s);
   if (rc) return rc;
   auto* pst = static_cast<hyd_pipe_stats*>(D(L.stats));
   auto* mem = static_cast<uint32_t*>(D(L.members));
-  rc = launch_dispatch(sorted, cost, n_iter, batch, k_pad, sch, n_schemes, cand, cnp, n_cand, max_np,
+  rc = launch_dispatch(sorted, cost, n_iter, batch, off, N, k_pad, sch, n_schemes, cand, cnp, n_cand, max_np,
                        pipe, static_cast<uint64_t*>(D(L.lb)), pst, mem, st, D(L.disp_ws), s);
   if (rc) return rc;
-  rc = launch_pack(sorted, cost, n_iter, batch, k_pad, sch, n_schemes, cand, cnp, n_cand, max_np,
+  rc = launch_pack(sorted, cost, n_iter, batch, off, N, k_pad, sch, n_schemes, cand, cnp, n_cand, max_np,
                    pipe, pst, mem, mb, vv, pt, ms, st, D(L.pack_ws), L.pack_bytes, s);
   if (rc) return rc;
   rc = launch_select(ms, n_iter, n_cand, cand_offset, key, st, s);
   if (rc) return rc;
   if (reduce && reduce(key, n_iter, reduce_user, stream) != 0) return HYD_E_REDUCE;
-  rc = launch_gather(key, perm, pipe, mb, vv, pt, n_iter, batch, n_cand, cand_offset,
+  rc = launch_gather(key, perm, pipe, mb, vv, pt, n_iter, batch, off, N, n_cand, cand_offset,
                      static_cast<uint8_t*>(D(L.win_pipe)), static_cast<uint16_t*>(D(L.win_mb)),
                      static_cast<uint16_t*>(D(L.win_v)), static_cast<uint64_t*>(D(L.win_ptime)), s);
   if (rc) return rc;
   HYD_CK(cudaMemcpyAsync(key_host, key, It * 8, cudaMemcpyDeviceToHost, s));
-  HYD_CK(cudaMemcpyAsync(win_pipe_host, D(L.win_pipe), It * B, cudaMemcpyDeviceToHost, s));
-  HYD_CK(cudaMemcpyAsync(win_mb_host, D(L.win_mb), It * B * 2, cudaMemcpyDeviceToHost, s));
+  HYD_CK(cudaMemcpyAsync(win_pipe_host, D(L.win_pipe), N, cudaMemcpyDeviceToHost, s));
+  HYD_CK(cudaMemcpyAsync(win_mb_host, D(L.win_mb), N * 2, cudaMemcpyDeviceToHost, s));
   HYD_CK(cudaMemcpyAsync(win_v_host, D(L.win_v), It * HYD_MAX_PIPES * 2, cudaMemcpyDeviceToHost, s));
   HYD_CK(cudaMemcpyAsync(win_ptime_host, D(L.win_ptime), It * HYD_MAX_PIPES * 8, cudaMemcpyDeviceToHost, s));
   HYD_CK(cudaMemcpyAsync(status_host, st, 4, cudaMemcpyDeviceToHost, s));
   HYD_CK(cudaStreamSynchronize(s));
 #undef HYD_CK
   return HYD_OK;
+}
+
+int hyd_assign_host(const uint32_t* len_host, int n_iter, int batch, const hyd_scheme* schemes_host,
+                    int n_schemes, int k_pad, const uint8_t* cand_host, const uint8_t* cand_np_host,
+                    int n_cand, int cand_offset, int64_t* key_host, uint8_t* win_pipe_host,
+                    uint16_t* win_mb_host, uint16_t* win_v_host, uint64_t* win_ptime_host,
+                    uint32_t* status_host, hyd_reduce_fn reduce, void* reduce_user, void* ws,
+                    size_t ws_bytes, void* stream) {
+  return assign_host_impl(len_host, n_iter, nullptr, batch, schemes_host, n_schemes, k_pad,
+                          cand_host, cand_np_host, n_cand, cand_offset, key_host, win_pipe_host,
+                          win_mb_host, win_v_host, win_ptime_host, status_host, reduce, reduce_user,
+                          ws, ws_bytes, stream);
+}
+
+int hyd_assign_host_ragged(const uint32_t* len_host, int n_iter, const uint32_t* offsets_host,
+                           int batch_max, const hyd_scheme* schemes_host, int n_schemes, int k_pad,
+                           const uint8_t* cand_host, const uint8_t* cand_np_host, int n_cand,
+                           int cand_offset, int64_t* key_host, uint8_t* win_pipe_host,
+                           uint16_t* win_mb_host, uint16_t* win_v_host, uint64_t* win_ptime_host,
+                           uint32_t* status_host, hyd_reduce_fn reduce, void* reduce_user, void* ws,
+                           size_t ws_bytes, void* stream) {
+  if (!offsets_host) return HYD_E_INVALID;
+  return assign_host_impl(len_host, n_iter, offsets_host, batch_max, schemes_host, n_schemes, k_pad,
+                          cand_host, cand_np_host, n_cand, cand_offset, key_host, win_pipe_host,
+                          win_mb_host, win_v_host, win_ptime_host, status_host, reduce, reduce_user,
+                          ws, ws_bytes, stream);
 }
 
 }  // extern "C"

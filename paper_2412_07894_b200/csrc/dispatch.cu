@@ -78,7 +78,7 @@ __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
     cf[j] = 0u;
     if (j < np) ml_min = min(ml_min, ml[j]);
   }
-  const bool words = (B & 3) == 0;
+  const bool words = (B & 3) == 0 && ((size_t)prow & 3) == 0;
   uint32_t word = 0u;
   for (int i = 0; i < B; ++i) {
     const uint32_t l = sl[i];
@@ -207,7 +207,7 @@ __device__ __forceinline__ void packed_run(const uint32_t* __restrict__ sl,
     cf[j] = 0u;
     pj[j] = TRANS ? cst + (size_t)kk[j] * stride : cst + kk[j];
   }
-  const bool full_sectors = (B & 31) == 0;
+  const bool full_sectors = (B & 31) == 0 && ((size_t)prow & 15) == 0;
   for (int i0 = 0; i0 < B; i0 += 32) {
     const int n = min(32, B - i0);
     bool empty = false;
@@ -217,8 +217,9 @@ __device__ __forceinline__ void packed_run(const uint32_t* __restrict__ sl,
     uint32_t plane[SH];
 #pragma unroll
     for (int b = 0; b < SH; ++b) plane[b] = 0u;
-    if (TRANS) {  // n % 4 == 0 (staging requires B % 4 == 0)
-      for (int g = 0; g < n; g += 4) {
+    if (TRANS) {  // groups of 4 steps (uniform batches: B % 4 == 0), then the ragged remainder
+      const int n4 = n & ~3;
+      for (int g = 0; g < n4; g += 4) {
         const int i = i0 + g;
         const uint4 l4 = *reinterpret_cast<const uint4*>(sl + i);
         const uint32_t lq[4] = {l4.x, l4.y, l4.z, l4.w};
@@ -232,6 +233,16 @@ __device__ __forceinline__ void packed_run(const uint32_t* __restrict__ sl,
           else
             packed_step<DP, SH, false>(lq[u], tau, key, mults, ml, np, pend, plane, s_sum);
         }
+      }
+      for (int q = n4; q < n; ++q) {
+        const int i = i0 + q;
+        uint32_t tau[DP];
+#pragma unroll
+        for (int j = 0; j < DP; ++j) tau[j] = pj[j][i];
+        if (warp_empty)
+          packed_step<DP, SH, true>(sl[i], tau, key, mults, ml, np, pend, plane, s_sum);
+        else
+          packed_step<DP, SH, false>(sl[i], tau, key, mults, ml, np, pend, plane, s_sum);
       }
     } else {
       for (int q = 0; q < n; ++q) {
@@ -305,15 +316,17 @@ __device__ __forceinline__ void packed_run(const uint32_t* __restrict__ sl,
 // Per-iteration bound[t] = sum_i max_k tau_ik + max_ik tau_ik (PPmax - 1): no C_j + E_j (and no
 // candidate load C_j + tau + e_j) of iteration t can exceed it.  One CTA per iteration.
 __global__ void __launch_bounds__(256)
-    k_iter_bound(const uint32_t* __restrict__ cost, int batch, int k_pad,
-                 const hyd_scheme* __restrict__ schemes, int n_schemes, uint64_t* __restrict__ bound) {
+    k_iter_bound(const uint32_t* __restrict__ cost, int batch, const uint32_t* __restrict__ off,
+                 int k_pad, const hyd_scheme* __restrict__ schemes, int n_schemes,
+                 uint64_t* __restrict__ bound) {
   __shared__ unsigned long long s_part[8];
   __shared__ uint32_t s_top;
   const int t = blockIdx.x, tid = threadIdx.x;
-  const uint32_t* c = cost + (size_t)t * batch * k_pad;
+  const uint32_t* c = cost + geo_base(off, batch, t) * k_pad;
+  const int bt = geo_bt(off, batch, t);
   unsigned long long sum = 0ull;
   uint32_t top = 0u;
-  for (int i = tid; i < batch; i += 256) {
+  for (int i = tid; i < bt; i += 256) {
     uint32_t m = 0u;
     for (int k = 0; k < n_schemes; ++k) m = max(m, __ldg(c + (size_t)i * k_pad + k));
     sum += m;
@@ -339,10 +352,10 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-int launch_iter_bound(const uint32_t* cost, int n_iter, int batch, int k_pad,
+int launch_iter_bound(const uint32_t* cost, int n_iter, int batch, const uint32_t* off, int k_pad,
                       const hyd_scheme* schemes, int n_schemes, uint64_t* bound, cudaStream_t s) {
   if (n_iter == 0) return HYD_OK;
-  k_iter_bound<<<n_iter, 256, 0, s>>>(cost, batch, k_pad, schemes, n_schemes, bound);
+  k_iter_bound<<<n_iter, 256, 0, s>>>(cost, batch, off, k_pad, schemes, n_schemes, bound);
   note_launch();
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? HYD_OK : record_cuda_error(e);
@@ -355,7 +368,8 @@ int launch_iter_bound(const uint32_t* cost, int n_iter, int batch, int k_pad,
 template <int DP, bool STAGED, int MODE>
 __global__ void __launch_bounds__(kDispatchThreads)
     k_dispatch(const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ cost,
-               int n_iter, int batch, int k_pad, const hyd_scheme* __restrict__ schemes,
+               int n_iter, int batch, const uint32_t* __restrict__ off, size_t n_total, int k_pad,
+               const hyd_scheme* __restrict__ schemes,
                int n_schemes, const uint8_t* __restrict__ cand, const uint8_t* __restrict__ cand_np,
                int n_cand, int max_np, int ct, int tt, uint8_t* __restrict__ pipe,
                uint64_t* __restrict__ lb, hyd_pipe_stats* __restrict__ stats,
@@ -365,9 +379,10 @@ __global__ void __launch_bounds__(kDispatchThreads)
   // dynamic smem: [stage if STAGED] [s_sum u64 columns]; stage = [tt][B] lengths, then the
   // costs: MODE 1 as global rows [tt][B][k_pad]; MODE 0 transposed [tt][k_pad][Bp], Bp = B | 1
   constexpr bool TRANS = STAGED && MODE == 0;
-  const int B = batch;
+  // ragged batches (off != nullptr) run with tt = 1: B = this iteration's sequences
+  const int B = off ? geo_bt(off, batch, blockIdx.y) : batch;
   const int Bp = B | 1;
-  const size_t stage_words = STAGED ? dispatch_stage_words(tt, B, k_pad) : 0;
+  const size_t stage_words = STAGED ? dispatch_stage_words(tt, batch, k_pad) : 0;
   unsigned long long* s_sum = reinterpret_cast<unsigned long long*>(sm + ((stage_words + 3) & ~(size_t)3));
   const int tid = threadIdx.x;
   const int c0 = blockIdx.x * ct, t0 = blockIdx.y * tt;
@@ -379,12 +394,21 @@ __global__ void __launch_bounds__(kDispatchThreads)
   constexpr int SHK = DP <= 2 ? 1 : DP <= 4 ? 2 : DP <= 8 ? 3 : DP <= 16 ? 4 : 5;
   const bool packed = bound < (1ull << (31 - SHK));  // keys (load << SHK | j) stay below 2^31
   if ((MODE == 0) != packed) return;  // the other kernel owns this CTA
-  if (STAGED) {
-    const uint4* gl = reinterpret_cast<const uint4*>(sorted_len + (size_t)t0 * B);
+  const size_t base0 = geo_base(off, batch, t0);  // first row of the CTA's iterations
+  if (STAGED && off) {  // ragged: rows need not be 16-byte aligned
+    for (int e = tid; e < B; e += kDispatchThreads) sm[e] = __ldg(sorted_len + base0 + e);
+    uint32_t* st = sm + (size_t)tt * B;
+    const uint32_t* gc = cost + base0 * k_pad;
+    for (int e = tid; e < B * k_pad; e += kDispatchThreads) {
+      const int i = e / k_pad, k = e - i * k_pad;
+      st[TRANS ? (size_t)k * Bp + i : (size_t)e] = __ldg(gc + e);
+    }
+  } else if (STAGED) {
+    const uint4* gl = reinterpret_cast<const uint4*>(sorted_len + base0);
     uint4* sl4 = reinterpret_cast<uint4*>(sm);
     const int nl = ntt * B / 4;
     for (int e = tid; e < nl; e += kDispatchThreads) sl4[e] = __ldg(gl + e);
-    const uint4* gc = reinterpret_cast<const uint4*>(cost + (size_t)t0 * B * k_pad);
+    const uint4* gc = reinterpret_cast<const uint4*>(cost + base0 * k_pad);
     const int nc = ntt * B * k_pad / 4;
     if (TRANS) {
       uint32_t* st = sm + (size_t)tt * B;
@@ -410,13 +434,13 @@ __global__ void __launch_bounds__(kDispatchThreads)
 
   const int lt = tid / ct, lc = tid - lt * ct;
   const int c = c0 + lc, t = t0 + lt;
-  if (lt >= tt || c >= n_cand || t >= n_iter) return;
+  if (lt >= tt || c >= n_cand || t >= n_iter || B == 0) return;
 
-  const uint32_t* sl = STAGED ? sm + (size_t)lt * B : sorted_len + (size_t)t * B;
-  const uint32_t* cs = STAGED ? sm + (size_t)tt * B + (size_t)lt * B * k_pad
-                              : cost + (size_t)t * B * k_pad;
+  const size_t tbase = geo_base(off, batch, t);
+  const uint32_t* sl = STAGED ? sm + (size_t)lt * B : sorted_len + tbase;
+  const uint32_t* cs = STAGED ? sm + (size_t)tt * B + (size_t)lt * B * k_pad : cost + tbase * k_pad;
   const size_t row = (size_t)c * n_iter + t;
-  uint8_t* prow = pipe + row * B;
+  uint8_t* prow = pipe + (size_t)c * n_total + tbase;  // = row * B for uniform batches
 
   // candidate: pipelines in canonical order; unused lanes get MaxLen 0 (never feasible)
   const int np = cand_np[c];
@@ -453,7 +477,7 @@ __global__ void __launch_bounds__(kDispatchThreads)
     stats[srow * max_np].u = 0xFFFFFFFFu;
     return;
   }
-  const int nwords = (B + 31) >> 5;
+  const int nwords = (batch + 31) >> 5;  // row stride: words of the largest batch
   uint32_t* mbits = members + srow * max_np * nwords;  // word w of pipeline j at [w * max_np + j]
   unsigned long long* ssum = s_sum + tid;
   uint64_t lbv = 0ull;
@@ -500,7 +524,8 @@ __global__ void __launch_bounds__(kDispatchThreads)
 
 template <int DP, bool STAGED, int MODE>
 static cudaError_t launch_mode(dim3 grid, size_t smem, cudaStream_t s, const uint32_t* sorted_len,
-                               const uint32_t* cost, int n_iter, int batch, int k_pad,
+                               const uint32_t* cost, int n_iter, int batch, const uint32_t* off,
+                               size_t n_total, int k_pad,
                                const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
                                const uint8_t* cand_np, int n_cand, int max_np, int ct, int tt,
                                uint8_t* pipe, uint64_t* lb, hyd_pipe_stats* stats, uint32_t* members,
@@ -509,7 +534,7 @@ static cudaError_t launch_mode(dim3 grid, size_t smem, cudaStream_t s, const uin
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_dispatch<DP, STAGED, MODE><<<grid, kDispatchThreads, smem, s>>>(
-      sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct,
+      sorted_len, cost, n_iter, batch, off, n_total, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct,
       tt, pipe, lb, stats, members, status, bounds);
   note_launch();
   return cudaGetLastError();
@@ -518,6 +543,7 @@ static cudaError_t launch_mode(dim3 grid, size_t smem, cudaStream_t s, const uin
 template <int DP>
 static cudaError_t launch_dp(bool staged, dim3 grid, size_t smem_stage, cudaStream_t s,
                              const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch,
+                             const uint32_t* off, size_t n_total,
                              int k_pad, const hyd_scheme* schemes, int n_schemes,
                              const uint8_t* cand, const uint8_t* cand_np, int n_cand, int max_np,
                              int ct, int tt, uint8_t* pipe, uint64_t* lb, hyd_pipe_stats* stats,
@@ -526,13 +552,13 @@ static cudaError_t launch_dp(bool staged, dim3 grid, size_t smem_stage, cudaStre
   const size_t smem = staged ? ((smem_stage + 15) & ~(size_t)15) + cols : cols;
   cudaError_t e;
   if (staged) {
-    e = launch_mode<DP, true, 0>(grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds);
+    e = launch_mode<DP, true, 0>(grid, smem, s, sorted_len, cost, n_iter, batch, off, n_total, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds);
     if (e == cudaSuccess)
-      e = launch_mode<DP, true, 1>(grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds);
+      e = launch_mode<DP, true, 1>(grid, smem, s, sorted_len, cost, n_iter, batch, off, n_total, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds);
   } else {
-    e = launch_mode<DP, false, 0>(grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds);
+    e = launch_mode<DP, false, 0>(grid, smem, s, sorted_len, cost, n_iter, batch, off, n_total, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds);
     if (e == cudaSuccess)
-      e = launch_mode<DP, false, 1>(grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds);
+      e = launch_mode<DP, false, 1>(grid, smem, s, sorted_len, cost, n_iter, batch, off, n_total, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds);
   }
   return e;
 }
@@ -540,29 +566,29 @@ static cudaError_t launch_dp(bool staged, dim3 grid, size_t smem_stage, cudaStre
 size_t dispatch_workspace(int n_iter) { return ((size_t)n_iter * 8 + 255) & ~(size_t)255; }
 
 int launch_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch,
-                    int k_pad, const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
+                    const uint32_t* off, size_t n_total, int k_pad, const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
                     const uint8_t* cand_np, int n_cand, int max_np, uint8_t* pipe, uint64_t* lb,
                     hyd_pipe_stats* stats, uint32_t* members, uint32_t* status, void* ws,
                     cudaStream_t s) {
   if (n_iter == 0 || n_cand == 0) return HYD_OK;
   uint64_t* bounds = static_cast<uint64_t*>(ws);
-  const int rb = launch_iter_bound(cost, n_iter, batch, k_pad, schemes, n_schemes, bounds, s);
+  const int rb = launch_iter_bound(cost, n_iter, batch, off, k_pad, schemes, n_schemes, bounds, s);
   if (rb != HYD_OK) return rb;
   const int ct = n_cand < kDispatchThreads ? n_cand : kDispatchThreads;
-  const int tt = kDispatchThreads / ct;
+  const int tt = off ? 1 : kDispatchThreads / ct;  // ragged batches: one iteration per CTA
   const size_t smem = dispatch_stage_words(tt, batch, k_pad) * 4;
   const int dp = max_np <= 2 ? 2 : max_np <= 4 ? 4 : max_np <= 8 ? 8 : max_np <= 16 ? 16 : 32;
   const size_t static_smem = (size_t)dp * kDispatchThreads * 8 + 64;
   // stage when the rows fit comfortably (leaves room for several CTAs per SM)
-  const bool staged = smem + static_smem <= 96 * 1024 && (batch % 4) == 0;
+  const bool staged = smem + static_smem <= 96 * 1024 && (off || (batch % 4) == 0);
   dim3 grid((n_cand + ct - 1) / ct, (n_iter + tt - 1) / tt);
   cudaError_t e;
   switch (dp) {
-    case 2: e = launch_dp<2>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds); break;
-    case 4: e = launch_dp<4>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds); break;
-    case 8: e = launch_dp<8>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds); break;
-    case 16: e = launch_dp<16>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds); break;
-    default: e = launch_dp<32>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds); break;
+    case 2: e = launch_dp<2>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, off, n_total, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds); break;
+    case 4: e = launch_dp<4>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, off, n_total, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds); break;
+    case 8: e = launch_dp<8>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, off, n_total, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds); break;
+    case 16: e = launch_dp<16>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, off, n_total, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds); break;
+    default: e = launch_dp<32>(staged, grid, smem, s, sorted_len, cost, n_iter, batch, off, n_total, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds); break;
   }
   return e == cudaSuccess ? HYD_OK : record_cuda_error(e);
 }

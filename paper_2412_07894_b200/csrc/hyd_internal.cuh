@@ -36,6 +36,22 @@ __device__ __forceinline__ bool gt128(uint64_t ahi, uint64_t alo, uint64_t bhi, 
   return ahi > bhi || (ahi == bhi && alo > blo);
 }
 
+// Batch geometry (NEXT-2, token-budget batches): iteration t holds geo_bt(t) sequences whose rows
+// start at geo_base(t) in every iteration-indexed array ([N_total] lengths, [C][N_total] pipe/mb,
+// ...).  off = nullptr: the uniform case, B sequences per iteration; otherwise off[0..It] are CSR
+// offsets and B is the largest batch (bt is clamped to [0, B]; sort_cost flags violations).
+__device__ __forceinline__ int geo_bt(const uint32_t* off, int B, int t) {
+  if (!off) return B;
+  const int d = (int)(__ldg(off + t + 1) - __ldg(off + t));
+  return d < 0 ? 0 : (d > B ? B : d);
+}
+__device__ __forceinline__ size_t geo_base(const uint32_t* off, int B, int t) {
+  return off ? (size_t)__ldg(off + t) : (size_t)t * B;
+}
+__device__ __forceinline__ size_t geo_total(const uint32_t* off, int B, int n_iter) {
+  return off ? (size_t)__ldg(off + n_iter) : (size_t)n_iter * B;
+}
+
 __device__ __forceinline__ int next_pow2_ge(int x) {
   int p = 1;
   while (p < x) p <<= 1;

@@ -46,7 +46,9 @@ constexpr int kBigWarps = 3584;   // persistent warps of k_pack_big (scratch slo
 struct PackArgs {
   const uint32_t* sorted_len;
   const uint32_t* cost;
-  int n_iter, batch, k_pad;
+  int n_iter, batch, k_pad;  // batch: the largest batch (row stride of members, scratch)
+  const uint32_t* off;       // ragged CSR offsets [n_iter + 1] or nullptr (uniform)
+  size_t n_total;            // rows of iteration-indexed arrays (n_iter * batch if uniform)
   const hyd_scheme* schemes;
   int n_schemes;
   const uint8_t* cand;
@@ -181,8 +183,9 @@ __device__ __forceinline__ void search_take(Search& s, uint32_t V, uint64_t maxb
 // makespan = 0 (feasible) or UINT64_MAX (infeasible); v/ptime rows zeroed; infeasible
 // pairs get mb = 0xFFFF.  Tasks then write their v/ptime slot and atomicMax the makespan.
 __global__ void __launch_bounds__(256) k_pack_init(const hyd_pipe_stats* __restrict__ stats,
-                                                   int mnp, int n_iter, int batch, int n_cand,
-                                                   uint16_t* __restrict__ mb,
+                                                   int mnp, int n_iter, int batch,
+                                                   const uint32_t* __restrict__ off, size_t n_total,
+                                                   int n_cand, uint16_t* __restrict__ mb,
                                                    uint16_t* __restrict__ v,
                                                    uint64_t* __restrict__ ptime,
                                                    uint64_t* __restrict__ makespan) {
@@ -200,12 +203,13 @@ __global__ void __launch_bounds__(256) k_pack_init(const hyd_pipe_stats* __restr
 #pragma unroll
   for (int q = 0; q < 16; ++q) p4[q] = z;
   if (!feasible) {
-    uint16_t* mrow = mb + row * batch;
-    if ((batch & 7) == 0) {
+    const int bt = geo_bt(off, batch, t);
+    uint16_t* mrow = mb + (size_t)c * n_total + geo_base(off, batch, t);
+    if ((bt & 7) == 0 && ((size_t)mrow & 15) == 0) {
       const uint4 f = make_uint4(~0u, ~0u, ~0u, ~0u);
-      for (int q = 0; q < batch / 8; ++q) reinterpret_cast<uint4*>(mrow)[q] = f;
+      for (int q = 0; q < bt / 8; ++q) reinterpret_cast<uint4*>(mrow)[q] = f;
     } else {
-      for (int i = 0; i < batch; ++i) mrow[i] = 0xFFFF;
+      for (int i = 0; i < bt; ++i) mrow[i] = 0xFFFF;
     }
   }
 }
@@ -356,12 +360,15 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
   __shared__ int s_next, s_nrec, s_n2a, s_n2b;
   __shared__ int s_hist[NB];
   __shared__ uint32_t s_ml[HYD_MAX_SCHEMES], s_pp[HYD_MAX_SCHEMES], s_ul[HYD_MAX_SCHEMES];
-  const int B = a.batch, kp = a.k_pad;
+  const int kp = a.k_pad;
   const int t = blockIdx.y, c0 = blockIdx.x * tc;
+  const int B = geo_bt(a.off, a.batch, t);  // this iteration's sequences
+  const size_t tbase = geo_base(a.off, a.batch, t);
   const int tid = threadIdx.x, lane = tid & 31;
   const int ncl = min(tc, a.n_cand - c0);
   const int ntile = ncl * mnp;  // task ids of the tile
-  const uint32_t nwords = (uint32_t)a.nwords;
+  const uint32_t nwords = (uint32_t)a.nwords;           // member row stride (largest batch)
+  const uint32_t nwords_t = (uint32_t)((B + 31) >> 5);  // words of this iteration
   const size_t fbase = ((size_t)t * a.n_cand + c0) * mnp;  // first task bit / stats row of the tile
   if (tid == 0 && VM == 16) {  // this CTA's stats and membership rows are contiguous: pull them into L2
     const size_t total_rows = (size_t)a.n_iter * a.n_cand * mnp;
@@ -371,7 +378,7 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
   }
   // dynamic smem: [stage B*(1+kp) u32] [key u64] [sum_t, tau_max, eid, list2 u32]
   //               [u, vlo, vhi, va, perm, ncand u16] [k, state, cbucket u8]   (ncap slots each)
-  uint32_t* recbase = sm + (STAGED ? (size_t)B * (1 + kp) : 0);
+  uint32_t* recbase = sm + (STAGED ? (((size_t)a.batch * (1 + kp) + 3) & ~(size_t)3) : 0);  // 16 B
   TaskRecs R;
   R.key = reinterpret_cast<unsigned long long*>(recbase);
   R.sum_t = reinterpret_cast<uint32_t*>(R.key + ncap);
@@ -503,29 +510,31 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
     __syncthreads();
     for (int q = tid; q < nrec; q += kLaneThreads) R.perm[q] = (uint16_t)R.list2[q];
   }
-  if (STAGED) {
-    const uint4* gl = reinterpret_cast<const uint4*>(a.sorted_len + (size_t)t * B);
+  if (STAGED && a.off) {  // ragged rows need not be 16-byte aligned
+    for (int e = tid; e < B; e += kLaneThreads) sm[e] = __ldg(a.sorted_len + tbase + e);
+    for (int e = tid; e < B * kp; e += kLaneThreads) sm[B + e] = __ldg(a.cost + tbase * kp + e);
+  } else if (STAGED) {
+    const uint4* gl = reinterpret_cast<const uint4*>(a.sorted_len + tbase);
     uint4* s4 = reinterpret_cast<uint4*>(sm);
     for (int e = tid; e < B / 4; e += kLaneThreads) s4[e] = __ldg(gl + e);
-    const uint4* gc = reinterpret_cast<const uint4*>(a.cost + (size_t)t * B * kp);
+    const uint4* gc = reinterpret_cast<const uint4*>(a.cost + tbase * kp);
     uint4* c4 = reinterpret_cast<uint4*>(sm + B);
     for (int e = tid; e < B * kp / 4; e += kLaneThreads) c4[e] = __ldg(gc + e);
   }
   __syncthreads();
-  const uint32_t* slen = STAGED ? sm : a.sorted_len + (size_t)t * B;
-  const uint32_t* cst = STAGED ? sm + B : a.cost + (size_t)t * B * kp;
+  const uint32_t* slen = STAGED ? sm : a.sorted_len + tbase;
+  const uint32_t* cst = STAGED ? sm + B : a.cost + tbase * kp;
 
   LaneUnit<VM> u;
   uint32_t ev = 0;
   auto load_unit = [&](int r, uint32_t V, uint32_t thr, bool write) {
     const int e = (int)R.eid[r];
     const int c = c0 + e / mnp;
-    const size_t row = (size_t)c * a.n_iter + t;
     u.e = r;
     u.k = R.k[r];
     u.M = s_ml[u.k];
     u.mw = a.members + (fbase + e - e % mnp) * nwords + e % mnp;  // word-major rows of (t, c)
-    u.mrow = a.mb + row * B;
+    u.mrow = a.mb + (size_t)c * a.n_total + tbase;
     u.write = write;
     unit_start<VM>(u, V, thr);
   };
@@ -549,8 +558,8 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
         int st = 0;
 #pragma unroll 1
         for (int e = 0; e < kLaneEpoch && st == 0; ++e) {
-          if (VM == 16 && narrow) st = unit_step<8, VM, STAGED>(u, nwords, mnp, B, slen, cst, kp, ev);
-          else st = unit_step<VM, VM, STAGED>(u, nwords, mnp, B, slen, cst, kp, ev);
+          if (VM == 16 && narrow) st = unit_step<8, VM, STAGED>(u, nwords_t, mnp, B, slen, cst, kp, ev);
+          else st = unit_step<VM, VM, STAGED>(u, nwords_t, mnp, B, slen, cst, kp, ev);
         }
         if (st) have = finish(st);  // finish may load a follow-up unit into this lane
       }
@@ -995,8 +1004,10 @@ __global__ void __launch_bounds__(256) k_pack_big(PackArgs a) {
     const int c = (int)(e >> 37), t = (int)((e >> 5) & 0xFFFFFFFFull), j = (int)(e & 31);
     const size_t row = (size_t)c * a.n_iter + t;
     const size_t srow = ((size_t)t * a.n_cand + c) * a.mnp + j;
-    const uint32_t* sl = a.sorted_len + (size_t)t * B;
-    const uint32_t* cs = a.cost + (size_t)t * B * kp;
+    const size_t tbase = geo_base(a.off, a.batch, t);
+    const uint32_t nwords_t = (uint32_t)((geo_bt(a.off, a.batch, t) + 31) >> 5);
+    const uint32_t* sl = a.sorted_len + tbase;
+    const uint32_t* cs = a.cost + tbase * kp;
     const uint32_t* mw = a.members + (srow - j) * a.nwords + j;  // word-major rows of (t, c)
     const uint32_t k = a.cand[(size_t)c * HYD_MAX_PIPES + j];
     const hyd_pipe_stats st = a.stats[srow];
@@ -1008,7 +1019,7 @@ __global__ void __launch_bounds__(256) k_pack_big(PackArgs a) {
     s.S = st.s;
     s.sumT = st.sum_t;
     s.tau_max = st.tau_max;
-    uint16_t* mrow = a.mb + row * B;
+    uint16_t* mrow = a.mb + (size_t)c * a.n_total + tbase;
     if (s.U) {
       search_init(s);
       const bool narrow = s.sumT < 0xFFFFFFFFull;
@@ -1017,16 +1028,16 @@ __global__ void __launch_bounds__(256) k_pack_big(PackArgs a) {
       while ((V = search_next(s)) != 0) {
         const uint64_t thr = first ? ~0ull : search_thr_approx(s, V);
         uint64_t mx = 0;
-        const bool ok = narrow ? lpt_warp_dispatch<uint32_t>(mw, a.nwords, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, scr_t, scr_k, ev)
-                               : lpt_warp_dispatch<uint64_t>(mw, a.nwords, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, scr_t, scr_k, ev);
+        const bool ok = narrow ? lpt_warp_dispatch<uint32_t>(mw, nwords_t, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, scr_t, scr_k, ev)
+                               : lpt_warp_dispatch<uint64_t>(mw, nwords_t, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, scr_t, scr_k, ev);
         if (ok && first) wV = V;
         first = false;
         if (ok && search_improves(s, V, mx)) search_take(s, V, mx);
       }
       if (s.have && s.vbest != wV) {  // the winner's mb was not written by the first run
         uint64_t mx = 0;
-        if (narrow) lpt_warp_dispatch<uint32_t>(mw, a.nwords, (uint32_t)a.mnp, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, scr_t, scr_k, ev);
-        else lpt_warp_dispatch<uint64_t>(mw, a.nwords, (uint32_t)a.mnp, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, scr_t, scr_k, ev);
+        if (narrow) lpt_warp_dispatch<uint32_t>(mw, nwords_t, (uint32_t)a.mnp, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, scr_t, scr_k, ev);
+        else lpt_warp_dispatch<uint64_t>(mw, nwords_t, (uint32_t)a.mnp, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, scr_t, scr_k, ev);
       }
     } else {
       s.best = 0;
@@ -1069,7 +1080,8 @@ static cudaError_t launch_lanes(dim3 grid, size_t smem, cudaStream_t s, const Pa
   return cudaGetLastError();
 }
 
-int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch, int k_pad,
+int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch,
+                const uint32_t* off, size_t n_total, int k_pad,
                 const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
                 const uint8_t* cand_np, int n_cand, int max_np, const uint8_t* pipe,
                 const hyd_pipe_stats* stats, const uint32_t* members, uint16_t* mb, uint16_t* v,
@@ -1083,6 +1095,8 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
   a.cost = cost;
   a.n_iter = n_iter;
   a.batch = batch;
+  a.off = off;
+  a.n_total = n_total;
   a.k_pad = k_pad;
   a.schemes = schemes;
   a.n_schemes = n_schemes;
@@ -1119,7 +1133,7 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
   e = cudaMemsetAsync(a.flags, 0, flag_bytes(n_iter, n_cand, max_np), s);
   if (e != cudaSuccess) return record_cuda_error(e);
   const size_t pairs = (size_t)n_iter * n_cand;
-  k_pack_init<<<(unsigned)((pairs + 255) / 256), 256, 0, s>>>(stats, max_np, n_iter, batch, n_cand,
+  k_pack_init<<<(unsigned)((pairs + 255) / 256), 256, 0, s>>>(stats, max_np, n_iter, batch, off, n_total, n_cand,
                                                               mb, v, ptime, makespan);
   note_launch();
   e = cudaGetLastError();
@@ -1128,9 +1142,9 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
   // persistent lanes: pass 1 (VMAX 16) CTA = one iteration x tc candidates (~2048 tasks);
   // pass 2 (VMAX 32, flagged tasks, compacted records) CTA = one whole iteration
   // two CTAs per SM: ~110 KB of dynamic smem each for the staged iteration + task records
-  const size_t stage = (size_t)batch * 4 * (1 + (size_t)k_pad);
+  const size_t stage = ((size_t)batch * 4 * (1 + (size_t)k_pad) + 15) & ~(size_t)15;
   auto plan = [&](size_t budget, bool& staged, int& ncap, size_t& smem) {
-    staged = (batch % 4) == 0 && stage + 512 * 39 <= budget;
+    staged = (off || (batch % 4) == 0) && stage + 512 * 39 <= budget;
     ncap = (int)(((staged ? budget - stage : budget) / 39) & ~(size_t)31);
     ncap = ncap > 2048 ? 2048 : ncap;
     smem = (size_t)ncap * 39 + (staged ? stage : 0);  // task records + staged iteration

@@ -46,7 +46,8 @@ __global__ void __launch_bounds__(256) k_gather(const int64_t* __restrict__ key,
                                                 const uint16_t* __restrict__ mb,
                                                 const uint16_t* __restrict__ v,
                                                 const uint64_t* __restrict__ ptime, int n_iter,
-                                                int batch, int n_cand, int cand_offset,
+                                                int batch, const uint32_t* __restrict__ off,
+                                                size_t n_total, int n_cand, int cand_offset,
                                                 uint8_t* __restrict__ win_pipe,
                                                 uint16_t* __restrict__ win_mb,
                                                 uint16_t* __restrict__ win_v,
@@ -57,11 +58,14 @@ __global__ void __launch_bounds__(256) k_gather(const int64_t* __restrict__ key,
   const int c = (int)(k & ((1ll << HYD_KEY_SHIFT) - 1)) - cand_offset;
   if (c < 0 || c >= n_cand) return;  // another rank owns the winner
   const size_t row = (size_t)c * n_iter + t;
-  const uint32_t* pr = perm + (size_t)t * batch;
-  for (int i = threadIdx.x; i < batch; i += blockDim.x) {
+  const size_t base = geo_base(off, batch, t);
+  const int bt = geo_bt(off, batch, t);
+  const uint32_t* pr = perm + base;
+  const size_t src = (size_t)c * n_total + base;
+  for (int i = threadIdx.x; i < bt; i += blockDim.x) {
     const uint32_t o = pr[i];
-    win_pipe[(size_t)t * batch + o] = pipe[row * batch + i];
-    win_mb[(size_t)t * batch + o] = mb[row * batch + i];
+    win_pipe[base + o] = pipe[src + i];
+    win_mb[base + o] = mb[src + i];
   }
   if (threadIdx.x < HYD_MAX_PIPES) {
     win_v[(size_t)t * HYD_MAX_PIPES + threadIdx.x] = v[row * HYD_MAX_PIPES + threadIdx.x];
@@ -80,11 +84,11 @@ int launch_select(const uint64_t* makespan, int n_iter, int n_cand, int cand_off
 }
 
 int launch_gather(const int64_t* key, const uint32_t* perm, const uint8_t* pipe, const uint16_t* mb,
-                  const uint16_t* v, const uint64_t* ptime, int n_iter, int batch, int n_cand,
-                  int cand_offset, uint8_t* win_pipe, uint16_t* win_mb, uint16_t* win_v,
+                  const uint16_t* v, const uint64_t* ptime, int n_iter, int batch,
+                  const uint32_t* off, size_t n_total, int n_cand, int cand_offset, uint8_t* win_pipe, uint16_t* win_mb, uint16_t* win_v,
                   uint64_t* win_ptime, cudaStream_t s) {
   if (n_iter == 0) return HYD_OK;
-  k_gather<<<n_iter, 256, 0, s>>>(key, perm, pipe, mb, v, ptime, n_iter, batch, n_cand, cand_offset,
+  k_gather<<<n_iter, 256, 0, s>>>(key, perm, pipe, mb, v, ptime, n_iter, batch, off, n_total, n_cand, cand_offset,
                                   win_pipe, win_mb, win_v, win_ptime);
   note_launch();
   const cudaError_t e = cudaGetLastError();

@@ -38,6 +38,7 @@ __device__ __forceinline__ uint32_t eval_cost(uint64_t a, uint64_t b, uint64_t c
 
 template <int NT>
 __global__ void __launch_bounds__(NT) k_sort_cost(const uint32_t* __restrict__ len, int batch,
+                                                  const uint32_t* __restrict__ off,
                                                   const hyd_scheme* __restrict__ schemes,
                                                   int n_schemes, int k_pad,
                                                   uint32_t* __restrict__ sorted_len,
@@ -45,19 +46,24 @@ __global__ void __launch_bounds__(NT) k_sort_cost(const uint32_t* __restrict__ l
                                                   uint32_t* __restrict__ cost,
                                                   uint32_t* __restrict__ status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int B = batch;
   const int t = blockIdx.x;
   const int tid = threadIdx.x;
-  // layout: lens[B] u32 | hist[16*NT] u32 | idxA[B] u16 | idxB[B] u16 | coef[3*K] u64
+  const int B = geo_bt(off, batch, t);  // this iteration's sequences (<= batch)
+  const size_t base = geo_base(off, batch, t);
+  if (off && tid == 0) {  // ragged batches: 1 <= B_t <= batch
+    const int d = (int)(__ldg(off + t + 1) - __ldg(off + t));
+    if (d < 1 || d > batch) atomicOr(status, HYD_F_BAD_LENGTH);
+  }
+  // layout (sized for `batch`): lens[B] u32 | hist[16*NT] u32 | idxA[B] u16 | idxB[B] u16 | coef
   uint32_t* lens = reinterpret_cast<uint32_t*>(smem_raw);
-  uint32_t* hist = lens + B;
+  uint32_t* hist = lens + batch;
   uint16_t* idxA = reinterpret_cast<uint16_t*>(hist + 16 * NT);
-  uint16_t* idxB = idxA + B;
-  uint64_t* coef = reinterpret_cast<uint64_t*>(smem_raw + (((size_t)B * 4 + 16 * NT * 4 + (size_t)B * 4 + 15) & ~(size_t)15));
+  uint16_t* idxB = idxA + batch;
+  uint64_t* coef = reinterpret_cast<uint64_t*>(smem_raw + (((size_t)batch * 4 + 16 * NT * 4 + (size_t)batch * 4 + 15) & ~(size_t)15));
   __shared__ uint32_t s_or[NT / 32];
   __shared__ uint32_t s_wsum[NT / 32];
 
-  const uint32_t* lrow = len + (size_t)t * B;
+  const uint32_t* lrow = len + base;
   uint32_t orv = 0;
   for (int i = tid; i < B; i += NT) {
     const uint32_t l = __ldg(lrow + i);
@@ -140,8 +146,8 @@ __global__ void __launch_bounds__(NT) k_sort_cost(const uint32_t* __restrict__ l
     dst = tmp;
   }
 
-  uint32_t* srow = sorted_len + (size_t)t * B;
-  uint32_t* prow = perm + (size_t)t * B;
+  uint32_t* srow = sorted_len + base;
+  uint32_t* prow = perm + base;
   for (int i = tid; i < B; i += NT) {
     const uint32_t ix = src[i];
     srow[i] = lens[ix];
@@ -150,7 +156,7 @@ __global__ void __launch_bounds__(NT) k_sort_cost(const uint32_t* __restrict__ l
   // cost rows: thread handles (i, quad) pairs, consecutive threads -> consecutive 16 B
   uint32_t st = 0;
   const int quads = k_pad >> 2;
-  uint4* crow = reinterpret_cast<uint4*>(cost + (size_t)t * B * k_pad);
+  uint4* crow = reinterpret_cast<uint4*>(cost + base * k_pad);
   for (int e = tid; e < B * quads; e += NT) {
     const int i = e / quads, q = e - i * quads;
     const uint32_t l = lens[src[i]];
@@ -171,22 +177,22 @@ size_t sort_cost_smem(int batch, int nt, int n_schemes) {
          (size_t)n_schemes * 24;
 }
 
-int launch_sort_cost(const uint32_t* len, int n_iter, int batch, const hyd_scheme* schemes,
-                     int n_schemes, int k_pad, uint32_t* sorted_len, uint32_t* perm, uint32_t* cost,
-                     uint32_t* status, cudaStream_t s) {
+int launch_sort_cost(const uint32_t* len, int n_iter, int batch, const uint32_t* off,
+                     const hyd_scheme* schemes, int n_schemes, int k_pad, uint32_t* sorted_len,
+                     uint32_t* perm, uint32_t* cost, uint32_t* status, cudaStream_t s) {
   if (n_iter == 0) return HYD_OK;
   cudaError_t e;
   if (batch <= 2048) {
     const size_t sm = sort_cost_smem(batch, 256, n_schemes);
     e = cudaFuncSetAttribute(k_sort_cost<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return record_cuda_error(e);
-    k_sort_cost<256><<<n_iter, 256, sm, s>>>(len, batch, schemes, n_schemes, k_pad, sorted_len,
+    k_sort_cost<256><<<n_iter, 256, sm, s>>>(len, batch, off, schemes, n_schemes, k_pad, sorted_len,
                                               perm, cost, status);
   } else {
     const size_t sm = sort_cost_smem(batch, 1024, n_schemes);
     e = cudaFuncSetAttribute(k_sort_cost<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return record_cuda_error(e);
-    k_sort_cost<1024><<<n_iter, 1024, sm, s>>>(len, batch, schemes, n_schemes, k_pad, sorted_len,
+    k_sort_cost<1024><<<n_iter, 1024, sm, s>>>(len, batch, off, schemes, n_schemes, k_pad, sorted_len,
                                                 perm, cost, status);
   }
   note_launch();

@@ -36,6 +36,13 @@ EXPORTS = (
     "hyd_status_string",
     "hyd_last_cuda_error",
     "hyd_kernel_launches",
+    "hyd_cost_table_ragged",
+    "hyd_dispatch_ragged",
+    "hyd_pack_ragged",
+    "hyd_gather_winners_ragged",
+    "hyd_assign_workspace_ragged",
+    "hyd_assign_key_offset_ragged",
+    "hyd_assign_host_ragged",
     "hyd_alg1_workspace",
     "hyd_alg1_permutations",
     "hyd_dispatch_alg1",
@@ -74,6 +81,13 @@ def lib():
         "hyd_status_string": ([I], C.c_char_p),
         "hyd_last_cuda_error": ([], C.c_char_p),
         "hyd_kernel_launches": ([], I),
+        "hyd_cost_table_ragged": ([P, I, P, I, I, P, I, I, P, P, P, P, P], I),
+        "hyd_dispatch_ragged": ([P, P, I, P, I, I, I, P, I, P, P, I, I, P, P, P, P, P, P, Z, P], I),
+        "hyd_pack_ragged": ([P, P, I, P, I, I, I, P, I, P, P, I, I, P, P, P, P, P, P, P, P, P, Z, P], I),
+        "hyd_gather_winners_ragged": ([P, P, P, P, P, P, I, P, I, I, I, I, P, P, P, P, P], I),
+        "hyd_assign_workspace_ragged": ([I, I, I, I, I, I, I], Z),
+        "hyd_assign_key_offset_ragged": ([I, I, I, I, I, I, I], Z),
+        "hyd_assign_host_ragged": ([P, I, P, I, P, I, I, P, P, I, I, P, P, P, P, P, P, REDUCE_FN, P, P, Z, P], I),
         "hyd_alg1_workspace": ([I], Z),
         "hyd_alg1_permutations": ([U64, I, I, I, P, P], I),
         "hyd_dispatch_alg1": ([P, P, I, I, I, P, I, P, P, I, I, I, P, P, P, P, P, P, P, P, Z, P], I),
@@ -161,6 +175,50 @@ def pack(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_
                           _dev(ptime),
                           _dev(makespan), _dev(status), _dev(ws), ws.numel() * ws.element_size(),
                           _stream(stream)), "hyd_pack")
+
+
+# ---- NEXT-2: ragged (token-budget) batches; ``off`` is the device CSR offsets tensor [It + 1]
+def cost_table_ragged(len_, n_iter, off, n_total, batch_max, schemes, n_schemes, k_pad, sorted_len, perm, cost,
+                      status, stream=None):
+    _check(lib().hyd_cost_table_ragged(_dev(len_), n_iter, _dev(off), n_total, batch_max, _dev(schemes), n_schemes,
+                                       k_pad, _dev(sorted_len), _dev(perm), _dev(cost), _dev(status),
+                                       _stream(stream)), "hyd_cost_table_ragged")
+
+
+def dispatch_ragged(sorted_len, cost, n_iter, off, n_total, batch_max, k_pad, schemes, n_schemes, cand, cand_np,
+                    n_cand, max_np, pipe, lb, stats, members, status, ws, stream=None):
+    _check(lib().hyd_dispatch_ragged(_dev(sorted_len), _dev(cost), n_iter, _dev(off), n_total, batch_max, k_pad,
+                                     _dev(schemes), n_schemes, _dev(cand), _dev(cand_np), n_cand, max_np, _dev(pipe),
+                                     _dev(lb), _dev(stats), _dev(members), _dev(status), _dev(ws),
+                                     ws.numel() * ws.element_size(), _stream(stream)), "hyd_dispatch_ragged")
+
+
+def pack_ragged(sorted_len, cost, n_iter, off, n_total, batch_max, k_pad, schemes, n_schemes, cand, cand_np, n_cand,
+                max_np, pipe, stats, members, mb, v, ptime, makespan, status, ws, stream=None):
+    _check(lib().hyd_pack_ragged(_dev(sorted_len), _dev(cost), n_iter, _dev(off), n_total, batch_max, k_pad,
+                                 _dev(schemes), n_schemes, _dev(cand), _dev(cand_np), n_cand, max_np, _dev(pipe),
+                                 _dev(stats), _dev(members), _dev(mb), _dev(v), _dev(ptime), _dev(makespan),
+                                 _dev(status), _dev(ws), ws.numel() * ws.element_size(), _stream(stream)),
+           "hyd_pack_ragged")
+
+
+def assign_workspace_ragged(n_iter, n_total, batch_max, n_schemes, k_pad, n_cand, max_np) -> int:
+    return int(lib().hyd_assign_workspace_ragged(n_iter, n_total, batch_max, n_schemes, k_pad, n_cand, max_np))
+
+
+def assign_key_offset_ragged(n_iter, n_total, batch_max, n_schemes, k_pad, n_cand, max_np) -> int:
+    return int(lib().hyd_assign_key_offset_ragged(n_iter, n_total, batch_max, n_schemes, k_pad, n_cand, max_np))
+
+
+def assign_host_ragged(len_host_ptr, n_iter, off_host_ptr, batch_max, schemes_host_ptr, n_schemes, k_pad,
+                       cand_host_ptr, cand_np_host_ptr, n_cand, cand_offset, key_host_ptr, win_pipe_ptr, win_mb_ptr,
+                       win_v_ptr, win_ptime_ptr, status_ptr, reduce_cb, ws, stream=None):
+    cb = reduce_cb if reduce_cb is not None else REDUCE_FN(0)
+    _check(lib().hyd_assign_host_ragged(len_host_ptr, n_iter, off_host_ptr, batch_max, schemes_host_ptr, n_schemes,
+                                        k_pad, cand_host_ptr, cand_np_host_ptr, n_cand, cand_offset, key_host_ptr,
+                                        win_pipe_ptr, win_mb_ptr, win_v_ptr, win_ptime_ptr, status_ptr, cb, None,
+                                        _dev(ws), ws.numel() * ws.element_size(), _stream(stream)),
+           "hyd_assign_host_ragged")
 
 
 def alg1_workspace(n_iter) -> int:

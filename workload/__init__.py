@@ -190,6 +190,25 @@ def lengths_lognormal(rng, n, mu=6.9, sigma=1.2, lo=1, hi=32768):
     return np.clip(x, lo, hi).astype(np.uint32)
 
 
+def sample_minibatches(rng, corpus, n_iter, token_budget, context):
+    """Token-budget mini-batches: per iteration, draw lengths
+    uniformly with replacement from ``corpus``, truncate each draw to ``context`` (the budget counts
+    truncated tokens), stop at the first draw that brings the total to >= ``token_budget``.
+    Returns (lengths u32 [N_total], offsets u32 [n_iter + 1])."""
+    corpus = np.asarray(corpus, dtype=np.int64)
+    out, offs, tot = [], [0], 0
+    for _ in range(n_iter):
+        got, acc = [], 0
+        while acc < token_budget:
+            x = min(int(corpus[int(rng.integers(0, corpus.size))]), context)
+            got.append(x)
+            acc += x
+        out.extend(got)
+        tot += len(got)
+        offs.append(tot)
+    return np.asarray(out, dtype=np.uint32), np.asarray(offs, dtype=np.uint32)
+
+
 def lengths_pareto(rng, n, alpha=1.1, xmin=256, lo=1, hi=131072):
     x = np.floor(xmin * (1.0 + rng.pareto(alpha, n)))
     return np.clip(x, lo, hi).astype(np.uint32)
@@ -277,20 +296,34 @@ def candidate_table(rng, schemes, n_cand, n_pipes, gpu_budget, safety, cover_len
 class Workload:
     cfg: int
     name: str
-    lengths: np.ndarray  # u32 [It][B]
+    lengths: np.ndarray  # u32 [It][B], or [N_total] for ragged batches
     schemes: np.ndarray  # SCHEME_DTYPE [K]
     cand: np.ndarray  # u8 [C][32]
     cand_np: np.ndarray  # u8 [C]
     k_pad: int
     meta: dict = field(default_factory=dict)
+    offsets: np.ndarray | None = None  # NEXT-2: u32 CSR [It + 1] of ragged (token-budget) batches
+
+    @property
+    def ragged(self):
+        return self.offsets is not None
 
     @property
     def n_iter(self):
-        return int(self.lengths.shape[0])
+        return int(self.offsets.size - 1) if self.ragged else int(self.lengths.shape[0])
 
     @property
     def batch(self):
-        return int(self.lengths.shape[1])
+        """Sequences per iteration (the largest one for ragged batches)."""
+        return int(np.diff(self.offsets.astype(np.int64)).max()) if self.ragged else int(self.lengths.shape[1])
+
+    @property
+    def n_total(self):
+        return int(self.offsets[-1]) if self.ragged else self.n_iter * self.batch
+
+    def iteration(self, t):
+        """Lengths of iteration t (a view)."""
+        return self.lengths[self.offsets[t]:self.offsets[t + 1]] if self.ragged else self.lengths[t]
 
     @property
     def n_cand(self):
@@ -308,6 +341,9 @@ CONFIGS = {
     3: dict(name="cfg3-gh128k-512seq-8pipe-1024cand", B=512, D=8, C=1024, It=256, budget=64, seed=303),
     4: dict(name="cfg4-70b-512seq-8pipe-4096cand", B=512, D=8, C=4096, It=1024, budget=64, seed=404),
     5: dict(name="cfg5-stress-8192seq-16pipe-16384cand", B=8192, D=16, C=16384, It=16, budget=256, seed=505),
+    # NEXT-2: the paper's workload shape -- 100K-token mini-batches, 32K context, ragged B
+    6: dict(name="cfg6-70b-100ktok-32kctx-8pipe-4096cand", B=None, D=8, C=4096, It=1024, budget=64, seed=606,
+            tokens=100_000, context=32768),
 }
 
 _SHAPES = {
@@ -335,6 +371,8 @@ def _kpad(K):
 def make_workload(cfg: int, n_cand: int | None = None, n_iter: int | None = None) -> Workload:
     """Config ``cfg`` (1-5).  ``n_cand``/``n_iter`` take a prefix (parity-test sizes)."""
     p = CONFIGS[cfg]
+    if cfg == 6:
+        return _make_ragged_workload(cfg, n_cand, n_iter)
     B, D, C, It = p["B"], p["D"], p["C"], p["It"]
     C = C if n_cand is None else n_cand
     It = It if n_iter is None else n_iter
@@ -383,6 +421,40 @@ def make_workload(cfg: int, n_cand: int | None = None, n_iter: int | None = None
         cand_np=cand_np,
         k_pad=_kpad(len(schemes)),
         meta=dict(model=model.name, hw=hw.name, gpu_budget=p["budget"], seed=p["seed"], D=D),
+    )
+
+
+def _make_ragged_workload(cfg, n_cand, n_iter):
+    """Config 6 (NEXT-2): config 4's model, hardware, schemes and candidate recipe with
+    token-budget batches drawn from a CommonCrawl-like corpus (lognormal mu 6.9, sigma 1.2)."""
+    p = CONFIGS[cfg]
+    D, C, It = p["D"], p["C"], p["It"]
+    C = C if n_cand is None else n_cand
+    It = It if n_iter is None else n_iter
+    rng_len = np.random.Generator(np.random.PCG64(p["seed"]))
+    rng_cand = np.random.Generator(np.random.PCG64(p["seed"] + 1))
+    corpus = np.maximum(np.floor(rng_len.lognormal(6.9, 1.2, 1_000_000)), 1).astype(np.int64)
+    lens, offs = sample_minibatches(rng_len, corpus, It, p["tokens"], p["context"])
+    schemes = scheme_table(LLAMA_70B, B200, _SHAPES[4], p["budget"])
+    maxlen_cap = p["context"]
+    g = [gpus(int(s["tp"]), int(s["pp"]), int(s["cp"])) for s in schemes]
+    ml = schemes["max_len"].astype(np.int64)
+    longest = [k for k in range(len(schemes)) if ml[k] >= maxlen_cap]
+    k_long = min(longest, key=lambda k: (g[k], k))
+    k_small = min(range(len(schemes)), key=lambda k: (g[k], -ml[k], k))
+    safety = [k_long] + [k_small] * (D - 1)
+    cand, cand_np = candidate_table(rng_cand, schemes, C, D, p["budget"], safety=safety, cover_len=maxlen_cap)
+    return Workload(
+        cfg=cfg,
+        name=p["name"],
+        lengths=lens,
+        schemes=schemes,
+        cand=cand,
+        cand_np=cand_np,
+        k_pad=_kpad(len(schemes)),
+        meta=dict(model=LLAMA_70B.name, hw=B200.name, gpu_budget=p["budget"], seed=p["seed"], D=D,
+                  tokens_per_iteration=p["tokens"], context=p["context"]),
+        offsets=offs,
     )
 
 
