@@ -17,7 +17,7 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SRCS = [os.path.join(_HERE, "hydref.c"), os.path.join(_HERE, "alg1ref.c")]
+_SRCS = [os.path.join(_HERE, "hydref.c"), os.path.join(_HERE, "alg1ref.c"), os.path.join(_HERE, "dpref.c")]
 _HDR = os.path.join(_HERE, "hydref.h")
 _LIB = os.path.join(_HERE, "libhydref.so")
 
@@ -94,6 +94,12 @@ def lib():
             _u32p, _u32p, I, I, I, _voidp, _u8p, _u8p, _i32p, _i32p, I, I, U64,
             _u8p, _u64p, _u16p, _u16p, _u64p, _u64p, _i32p, U32P, I,
         ]
+        # NEXT-3 (dpref.c)
+        L.hydref_dp_prefix.argtypes = [_u32p, I, _voidp, I, I, I, _u64p, U32P]
+        L.hydref_dp_solve.argtypes = [_u64p, _voidp, I, I, I, I, I, _u64p, _u64p, _i32p]
+        L.hydref_dp_solve.restype = I
+        L.hydref_dp_strategy.argtypes = [_i32p, _u64p, _voidp, I, I, I, I, I, _u32p, U32P]
+        L.hydref_dp_strategy.restype = I
         _lib = L
     return _lib
 
@@ -338,3 +344,70 @@ def assign_pairs_ragged(W, pairs_c, pairs_t, n_threads=0):
         for q, i in enumerate(idx):
             out[i] = {k: r[k][q] for k in ("pipe", "lb", "mb", "v", "ptime", "makespan")}
     return out
+
+
+# ------------------------------------------------------------------ NEXT-3 (dpref.c)
+def dp_prefix(lengths, schemes, step, J):
+    x = np.ascontiguousarray(lengths, np.uint32)
+    K = len(schemes)
+    pre = np.empty((K, J + 1), np.uint64)
+    st = C.c_uint32(0)
+    lib().hydref_dp_prefix(x, x.size, _sch_ptr(schemes), K, int(step), int(J), pre.reshape(-1), C.byref(st))
+    return pre, int(st.value)
+
+
+def dp_solve(pre, schemes, step, J, n_gpus, scale):
+    """The DP table: (t_num, t_den, choice), each [(n_gpus * scale + 1)][J + 1]."""
+    NV = n_gpus * scale
+    shape = (NV + 1, J + 1)
+    tn, td = np.empty(shape, np.uint64), np.empty(shape, np.uint64)
+    ch = np.empty(shape, np.int32)
+    lib().hydref_dp_solve(np.ascontiguousarray(pre, np.uint64).reshape(-1), _sch_ptr(schemes), len(schemes),
+                          int(step), int(J), int(n_gpus), int(scale), tn.reshape(-1), td.reshape(-1),
+                          ch.reshape(-1))
+    return tn, td, ch
+
+
+def dp_strategy(choice, t_den, schemes, J, n_gpus, scale, j):
+    """S[N][j step]: (feasible, per-scheme d in 1/scale units, scheme of the longest interval)."""
+    K = len(schemes)
+    counts = np.zeros(K, np.uint32)
+    top = C.c_uint32(0)
+    ok = lib().hydref_dp_strategy(np.ascontiguousarray(choice, np.int32).reshape(-1),
+                                  np.ascontiguousarray(t_den, np.uint64).reshape(-1), _sch_ptr(schemes), K, int(J),
+                                  int(n_gpus), int(scale), int(j), counts, C.byref(top))
+    return bool(ok), counts, int(top.value)
+
+
+def dp_round(counts, top_k, schemes, n_gpus, scale):
+    """Integer candidates near a relaxed strategy (reading 27): every scheme
+    with d_k > 0 takes floor or ceil of d_k; keep combinations within N GPUs whose scheme of the
+    longest interval keeps >= 1 pipeline.  Returns a list of tuples of per-scheme pipeline counts."""
+    ks = [k for k in range(len(counts)) if counts[k] > 0]
+    g = [int(schemes[k]["tp"]) * int(schemes[k]["pp"]) * int(schemes[k]["cp"]) for k in range(len(counts))]
+    opts = [sorted({int(counts[k]) // scale, -(-int(counts[k]) // scale)}) for k in ks]
+    out = []
+    import itertools
+
+    for combo in itertools.product(*opts):
+        n = [0] * len(counts)
+        for k, c in zip(ks, combo):
+            n[k] = c
+        if sum(n[k] * g[k] for k in range(len(n))) > n_gpus or n[top_k] < 1:
+            continue
+        out.append(tuple(n))
+    return out
+
+
+def dp_propose(lengths, schemes, step, J, n_gpus, scale):
+    """The proposed subset: the union over l = step..J step of the roundings of S[N][l]."""
+    pre, st = dp_prefix(lengths, schemes, step, J)
+    tn, td, ch = dp_solve(pre, schemes, step, J, n_gpus, scale)
+    rows = []
+    for j in range(1, J + 1):
+        ok, counts, top = dp_strategy(ch, td, schemes, J, n_gpus, scale, j)
+        if ok:
+            for r in dp_round(counts, top, schemes, n_gpus, scale):
+                if r not in rows:
+                    rows.append(r)
+    return rows, (pre, tn, td, ch), st

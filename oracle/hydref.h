@@ -146,6 +146,20 @@ void hydref_assign_pairs_ex(const uint32_t* sorted, const uint32_t* cost, int n_
                             uint16_t* mb, uint16_t* v, uint64_t* ptime, uint64_t* makespan,
                             int32_t* best_trial, uint32_t* status, int n_threads);
 
+/* ------------------------------------------------------------------ NEXT-3 (dpref.c)
+ * Strategy-proposal DP.  pre [K][J+1]: pre[k][j] = sum of T(x, P_k) over dataset
+ * lengths x (truncated to J step) with x <= j step.  t_num/t_den/choice [(N scale + 1)][J + 1]:
+ * t[nu][j] = t_num/t_den for n = nu/scale GPUs and l = j step (den 0 = infinity); choice = -1
+ * (carry t[nu-1][j]), -2 (base), else k << 24 | mu << 12 | j' (d = mu/scale pipelines of P_k on
+ * the interval (l - j' step, l]). */
+void hydref_dp_prefix(const uint32_t* lengths, int n_seq, const hydref_scheme* schemes, int K,
+                      int step, int J, uint64_t* pre, uint32_t* status);
+int hydref_dp_solve(const uint64_t* pre, const hydref_scheme* schemes, int K, int step, int J,
+                    int n_gpus, int scale, uint64_t* t_num, uint64_t* t_den, int32_t* choice);
+int hydref_dp_strategy(const int32_t* choice, const uint64_t* t_den, const hydref_scheme* schemes,
+                       int K, int J, int n_gpus, int scale, int j, uint32_t* counts,
+                       uint32_t* top_k);
+
 #ifdef __cplusplus
 }
 #endif
