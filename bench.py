@@ -47,6 +47,9 @@ def parse():
                     help="NEXT-1: stage 1 = Alg. 1 with this many random trials per (c,t) (0: HYD-H1 dispatch)")
     ap.add_argument("--seed", type=int, default=2024, help="Alg. 1 permutation seed")
     ap.add_argument("--candidates", type=int, default=0, help="diagnostics: first N candidates only (0: all)")
+    ap.add_argument("--dp", action="store_true",
+                    help="NEXT-3: time the strategy-proposal DP on the paper's grid (64 GPUs, 0.1 steps, 128-token "
+                         "buckets to 32K) instead of the assignment path")
     return ap.parse_args()
 
 
@@ -217,10 +220,92 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- GPU leg
+def dp_transitions(schemes, step, J, n_gpus, scale):
+    """Algorithmic (k, d, l') transitions the DP evaluates: sum over states (n, l)."""
+    g = [int(s["tp"]) * int(s["pp"]) * int(s["cp"]) for s in schemes]
+    ml = [int(s["max_len"]) for s in schemes]
+    NV = n_gpus * scale
+    tot = 0
+    for j in range(1, J + 1):
+        ks = [k for k in range(len(schemes)) if ml[k] >= j * step]
+        per_nu = sum(sum(nu // g[k] for k in ks) for nu in range(1, NV + 1))
+        tot += per_nu * j
+    return tot
+
+
+def run_dp(args):
+    """NEXT-3 bench line: one proposal = histogram + DP over the whole grid + strategies + rounding."""
+    import torch
+
+    from paper_2412_07894_b200 import assign, hyd
+
+    W = wl.make_workload(6, n_cand=2, n_iter=1024)  # 100K-token iterations: a 1024-iteration length sample
+    lens = np.ascontiguousarray(W.lengths)
+    step, J, N, scale = 128, 256, 64, 10
+    P = assign.Proposer(W.schemes, step, J, N, scale)
+    L = assign.lengths_to_device(lens)
+    for _ in range(args.warmup):
+        P.run(L)
+    torch.cuda.synchronize()
+    clk = ClockSampler(0)
+    clk.start()
+    time.sleep(0.3)
+    l0 = hyd.kernel_launches()
+    evs = []
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        P.run(L)
+        b.record()
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    launches = hyd.kernel_launches() - l0
+    clocks = clk.stop()
+    ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    trans = dp_transitions(W.schemes, step, J, N, scale)
+    sel, cand, cnp = P.candidates()
+    # oracle on a coarser grid (CPU minutes otherwise): same code, 1-GPU steps
+    cpu = None
+    if not args.no_cpu:
+        import oracle
+
+        oracle.build()
+        t0 = time.perf_counter()
+        oracle.dp_propose(lens, W.schemes, step, J, N, 1)
+        dt = time.perf_counter() - t0
+        ct = dp_transitions(W.schemes, step, J, N, 1)
+        cpu = {"value": ct / dt, "unit": "transitions/s", "cores": 1, "kind": "oracle",
+               "sample": f"integer DP (scale 1) on the same lengths and length grid, {ct} transitions in {dt:.1f} s"}
+    pk, how = peaks()
+    sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
+    alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e9
+    ops = 24.0 * trans  # DESIGN.md §5.5: ~24 int ops per transition (two 64x64->128 products, compares)
+    achieved = ops / (ms / 1000.0) / 1e9
+    line = {
+        "metric": "strategy-proposal DP transitions/sec", "value": trans / (ms / 1000.0), "unit": "transitions/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int64 (exact rationals, 128-bit products)",
+        "data": "synthetic",
+        "config": {"workload": "NEXT-3 proposal DP, cfg6 length sample", "n_sequences": int(lens.size),
+                   "length_step": step, "buckets": J, "gpus": N, "gpu_step": 1 / scale, "transitions": trans,
+                   "proposed_candidates": int(len(sel))},
+        "roofline": {"kernel": "k_dp_solve", "bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Gop/s",
+                     "frac": achieved / alu_peak, "traffic": None,
+                     "peak_source": f"148 SM x 128 INT32 lanes x {sm_mhz:.0f} MHz ({how} clock)"},
+        "gpu_launches": int(launches), "clocks": clocks,
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.dp:
+        return run_dp(args)
     import torch
     import torch.distributed as dist
 

@@ -255,6 +255,35 @@ int hyd_assign_host_ragged(const uint32_t* len_host, int n_iter, const uint32_t*
                            uint32_t* status_host, hyd_reduce_fn reduce, void* reduce_user, void* ws,
                            size_t ws_bytes, void* stream);
 
+/* ---- NEXT-3: strategy-proposal dynamic programme (§5) -------------------------
+ * lengths [n_seq] u32 (device): a sample of the dataset's sequence lengths, truncated to the
+ * context J * step.  Length grid l = j * step (j = 0..J), GPU grid n = nu / scale
+ * (nu = 0..n_gpus * scale; scale 1 = the integer DP, 10 = the 0.1-step continuous relaxation).
+ *   t[n][l] = min(t[n-1][l], min over (k, d, l') of max(t[n - d N(P_k)][l - l'],
+ *             (1/d) sum_{x in (l - l', l]} T(x, P_k))),  MaxLen(P_k) >= l, d N(P_k) <= n,
+ *   t[n][0] = 0, t[0][l > 0] = infinity; N(P_k) = tp * pp * cp.
+ * Outputs (caller-owned device buffers):
+ *   t_num, t_den [(n_gpus*scale + 1)][J + 1] u64: t = t_num / t_den exactly (t_den 0 = infinity;
+ *     t_num = scale * (sum of T) of the binding interval, t_den = scale * d);
+ *   choice [(n_gpus*scale + 1)][J + 1] i32: -1 = t[n-1][l] (carry), -2 = base state, else
+ *     k << 24 | (d * scale) << 12 | l'/step (ties: carry, then k, d, l' ascending);
+ *   counts [J + 1][n_schemes] u16: S[N][l]'s pipelines per scheme in units of 1/scale;
+ *   rows [J + 1][HYD_DP_MAX_ROUND][n_schemes] u8, valid [J + 1][HYD_DP_MAX_ROUND] u8: the integer
+ *     candidates near S[N][l] (every non-integer d_k rounded down or up; combination m takes the
+ *     ceiling for the q-th non-integer scheme, ascending k, iff bit q of m is set; valid iff
+ *     within n_gpus GPUs and the scheme of the longest interval keeps a pipeline);
+ *   keep [J + 1][HYD_DP_MAX_ROUND] u8: 1 for the first occurrence of each valid candidate in
+ *     (l, m) order -- the proposed subset is the rows with keep = 1.
+ * Limits: 1 <= n_schemes <= HYD_MAX_SCHEMES, 1 <= J, n_gpus * scale <= 4095, step >= 1,
+ * J * step <= HYD_LEN_LIMIT.  More than log2(HYD_DP_MAX_ROUND) non-integer d_k set HYD_F_OVERFLOW
+ * (that l proposes nothing).  ws: hyd_dp_workspace(n_schemes, J) bytes. */
+#define HYD_DP_MAX_ROUND 64
+size_t hyd_dp_workspace(int n_schemes, int J);
+int hyd_dp_propose(const uint32_t* lengths, int n_seq, const hyd_scheme* schemes, int n_schemes,
+                   int step, int J, int n_gpus, int scale, uint64_t* t_num, uint64_t* t_den,
+                   int32_t* choice, uint16_t* counts, uint8_t* rows, uint8_t* valid, uint8_t* keep,
+                   uint32_t* status, void* ws, size_t ws_bytes, void* stream);
+
 /* ---- host utilities --------------------------------------------------------------------
  * hyd_check_candidates: HOST tables; HYD_OK, HYD_E_INVALID or HYD_E_NOT_CANONICAL; writes
  * max over c of cand_np to *max_np_out (if non-null). */

@@ -379,35 +379,43 @@ def dp_strategy(choice, t_den, schemes, J, n_gpus, scale, j):
     return bool(ok), counts, int(top.value)
 
 
-def dp_round(counts, top_k, schemes, n_gpus, scale):
-    """Integer candidates near a relaxed strategy (reading 27): every scheme
-    with d_k > 0 takes floor or ceil of d_k; keep combinations within N GPUs whose scheme of the
-    longest interval keeps >= 1 pipeline.  Returns a list of tuples of per-scheme pipeline counts."""
-    ks = [k for k in range(len(counts)) if counts[k] > 0]
-    g = [int(schemes[k]["tp"]) * int(schemes[k]["pp"]) * int(schemes[k]["cp"]) for k in range(len(counts))]
-    opts = [sorted({int(counts[k]) // scale, -(-int(counts[k]) // scale)}) for k in ks]
+def dp_round(counts, top_k, schemes, n_gpus, scale, max_round=64):
+    """Integer candidates near a relaxed strategy (reading 27): each scheme
+    whose d_k (= counts[k] / scale) is not an integer takes floor or ceil -- combination m takes
+    the ceiling for the q-th such scheme (ascending k) iff bit q of m is set, m = 0 .. 2^f - 1;
+    a combination is kept if it fits in N GPUs and the scheme of the longest interval keeps a
+    pipeline.  More than log2(max_round) non-integer schemes: nothing (flagged).  Returns a list
+    of (m, per-scheme pipeline counts) for the kept combinations."""
+    K = len(counts)
+    g = [int(schemes[k]["tp"]) * int(schemes[k]["pp"]) * int(schemes[k]["cp"]) for k in range(K)]
+    fr = [k for k in range(K) if int(counts[k]) % scale != 0]
+    if 2 ** len(fr) > max_round:
+        return None
     out = []
-    import itertools
-
-    for combo in itertools.product(*opts):
-        n = [0] * len(counts)
-        for k, c in zip(ks, combo):
-            n[k] = c
-        if sum(n[k] * g[k] for k in range(len(n))) > n_gpus or n[top_k] < 1:
-            continue
-        out.append(tuple(n))
+    for m in range(2 ** len(fr)):
+        n = [int(counts[k]) // scale for k in range(K)]
+        for q, k in enumerate(fr):
+            n[k] += (m >> q) & 1
+        if sum(n[k] * g[k] for k in range(K)) <= n_gpus and n[top_k] >= 1:
+            out.append((m, tuple(n)))
     return out
 
 
 def dp_propose(lengths, schemes, step, J, n_gpus, scale):
-    """The proposed subset: the union over l = step..J step of the roundings of S[N][l]."""
+    """The proposed subset: the union over l = step .. J step of the roundings of S[N][l],
+    in first-occurrence order over (l, m).  Returns (rows, tables, status)."""
     pre, st = dp_prefix(lengths, schemes, step, J)
     tn, td, ch = dp_solve(pre, schemes, step, J, n_gpus, scale)
     rows = []
     for j in range(1, J + 1):
         ok, counts, top = dp_strategy(ch, td, schemes, J, n_gpus, scale, j)
-        if ok:
-            for r in dp_round(counts, top, schemes, n_gpus, scale):
-                if r not in rows:
-                    rows.append(r)
+        if not ok:
+            continue
+        r = dp_round(counts, top, schemes, n_gpus, scale)
+        if r is None:
+            st |= 1  # HYDREF_F_OVERFLOW
+            continue
+        for _, row in r:
+            if row not in rows:
+                rows.append(row)
     return rows, (pre, tn, td, ch), st

@@ -318,3 +318,55 @@ class HostAssigner:
             self._cb, self.ws, stream,
         )
         return self.key
+
+
+class Proposer:
+    """NEXT-3: the strategy-proposal DP (§5) on the device (include/hyd.h hyd_dp_propose).
+
+    ``lengths``: a sample of the dataset's sequence lengths; ``step``/``J``: length grid
+    (l = j step, context J step); ``scale``: 1 (integer DP) or 10 (0.1-step relaxation)."""
+
+    def __init__(self, schemes, step, J, n_gpus, scale=10, device=None):
+        import torch
+
+        self.torch = torch
+        self.dev = torch.device(device if device is not None else "cuda")
+        self.schemes_np = np.ascontiguousarray(schemes)
+        self.K, self.step, self.J, self.N, self.scale = len(schemes), int(step), int(J), int(n_gpus), int(scale)
+        dev, K, J = self.dev, self.K, self.J
+        NV = self.N * self.scale
+        self.schemes = torch.from_numpy(schemes_bytes(self.schemes_np).copy()).to(dev)
+        self.t_num = torch.empty((NV + 1, J + 1), dtype=torch.int64, device=dev)
+        self.t_den = torch.empty((NV + 1, J + 1), dtype=torch.int64, device=dev)
+        self.choice = torch.empty((NV + 1, J + 1), dtype=torch.int32, device=dev)
+        self.counts = torch.empty((J + 1, K), dtype=torch.int16, device=dev)
+        self.rows = torch.empty((J + 1, hyd.DP_MAX_ROUND, K), dtype=torch.uint8, device=dev)
+        self.valid = torch.empty((J + 1, hyd.DP_MAX_ROUND), dtype=torch.uint8, device=dev)
+        self.keep = torch.empty((J + 1, hyd.DP_MAX_ROUND), dtype=torch.uint8, device=dev)
+        self.status = torch.zeros((1,), dtype=torch.int32, device=dev)
+        self.ws = torch.empty((max(hyd.dp_workspace(K, J), 1),), dtype=torch.uint8, device=dev)
+
+    def run(self, len_dev, stream=None):
+        self.status.zero_()
+        hyd.dp_propose(len_dev, int(len_dev.numel()), self.schemes, self.K, self.step, self.J, self.N, self.scale,
+                       self.t_num, self.t_den, self.choice, self.counts, self.rows, self.valid, self.keep,
+                       self.status, self.ws, stream)
+
+    def candidates(self):
+        """Proposed subset as per-scheme pipeline counts [M][K] (first-occurrence order) and as
+        candidate tables (cand [M][32] u8 in canonical order, cand_np [M] u8)."""
+        self.torch.cuda.synchronize(self.dev)
+        rows = self.rows.cpu().numpy().reshape(-1, self.K)
+        keep = self.keep.cpu().numpy().reshape(-1).astype(bool)
+        sel = rows[keep]
+        ml = self.schemes_np["max_len"].astype(np.int64)
+        order = sorted(range(self.K), key=lambda k: (-ml[k], k))  # canonical pipelines (P:623)
+        cand = np.full((sel.shape[0], hyd.MAX_PIPES), 0xFF, np.uint8)
+        cnp = np.zeros(sel.shape[0], np.uint8)
+        for m, r in enumerate(sel):
+            ks = [k for k in order for _ in range(int(r[k]))]
+            if len(ks) > hyd.MAX_PIPES:
+                raise hyd.HydError(f"proposed candidate with {len(ks)} pipelines > {hyd.MAX_PIPES}")
+            cand[m, : len(ks)] = ks
+            cnp[m] = len(ks)
+        return sel, cand, cnp

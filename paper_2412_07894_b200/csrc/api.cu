@@ -29,6 +29,10 @@ int launch_alg1(const uint32_t*, const uint32_t*, int, int, int, const hyd_schem
                 const uint8_t*, const uint8_t*, int, int, int, const uint16_t*, uint64_t*, uint8_t*,
                 uint64_t*, hyd_pipe_stats*, uint32_t*, uint32_t*, void*, cudaStream_t);
 
+size_t dp_workspace(int, int);
+int launch_dp(const uint32_t*, int, const hyd_scheme*, int, int, int, int, int, uint64_t*, uint64_t*,
+              int32_t*, uint16_t*, uint8_t*, uint8_t*, uint8_t*, uint32_t*, void*, cudaStream_t);
+
 static std::atomic<int> g_launches{0};
 static thread_local char g_err[256] = "no CUDA error";
 
@@ -231,6 +235,25 @@ int hyd_dispatch_alg1(const uint32_t* sorted_len, const uint32_t* cost, int n_it
   return launch_alg1(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np,
                      n_cand, max_np, trials, order, best, pipe, lb, stats, members, status, ws,
                      (cudaStream_t)stream);
+}
+
+size_t hyd_dp_workspace(int n_schemes, int J) {
+  if (n_schemes < 1 || J < 1) return 0;
+  return dp_workspace(n_schemes, J);
+}
+
+int hyd_dp_propose(const uint32_t* lengths, int n_seq, const hyd_scheme* schemes, int n_schemes,
+                   int step, int J, int n_gpus, int scale, uint64_t* t_num, uint64_t* t_den,
+                   int32_t* choice, uint16_t* counts, uint8_t* rows, uint8_t* valid, uint8_t* keep,
+                   uint32_t* status, void* ws, size_t ws_bytes, void* stream) {
+  if (!lengths || !schemes || !t_num || !t_den || !choice || !counts || !rows || !valid || !keep ||
+      !status || n_seq < 0 || n_schemes < 1 || n_schemes > HYD_MAX_SCHEMES || step < 1 || J < 1 ||
+      J > 4095 || n_gpus < 1 || scale < 1 || (long long)n_gpus * scale > 4095 ||
+      (long long)J * step > HYD_LEN_LIMIT)
+    return HYD_E_INVALID;
+  if (!ws || ws_bytes < dp_workspace(n_schemes, J)) return HYD_E_WORKSPACE;
+  return launch_dp(lengths, n_seq, schemes, n_schemes, step, J, n_gpus, scale, t_num, t_den, choice,
+                   counts, rows, valid, keep, status, ws, (cudaStream_t)stream);
 }
 
 size_t hyd_pack_workspace(int n_iter, int batch, int n_cand, int max_np) {

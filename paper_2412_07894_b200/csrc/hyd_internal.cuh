@@ -52,6 +52,31 @@ __device__ __forceinline__ size_t geo_total(const uint32_t* off, int B, int n_it
   return off ? (size_t)__ldg(off + n_iter) : (size_t)n_iter * B;
 }
 
+// T(l) with a 128-bit intermediate; status bits per include/hyd.h.
+__device__ __forceinline__ uint32_t eval_cost(uint64_t a, uint64_t b, uint64_t c, uint32_t l,
+                                              uint32_t& st) {
+  if (l == 0u || l > HYD_LEN_LIMIT) {
+    st |= HYD_F_BAD_LENGTH;
+    return 0xFFFFFFFFu;
+  }
+  const uint64_t l2 = (uint64_t)l * (uint64_t)l;  // < 2^49
+  uint64_t hi1, lo1, hi2, lo2;
+  mul128(a, l2, hi1, lo1);
+  mul128(b, (uint64_t)l, hi2, lo2);
+  uint64_t lo = lo1 + lo2;
+  uint64_t hi = hi1 + hi2 + (lo < lo1 ? 1ull : 0ull);
+  const uint64_t lo3 = lo + c;
+  hi += (lo3 < lo) ? 1ull : 0ull;
+  // T = (hi:lo3) >> 32 = hi * 2^32 + (lo3 >> 32): fits u32 iff hi == 0
+  if (hi != 0ull) {
+    st |= HYD_F_OVERFLOW;
+    return 0xFFFFFFFFu;
+  }
+  const uint32_t t = (uint32_t)(lo3 >> 32);
+  if (t == 0u) st |= HYD_F_ZERO_COST;
+  return t;
+}
+
 __device__ __forceinline__ int next_pow2_ge(int x) {
   int p = 1;
   while (p < x) p <<= 1;

@@ -43,6 +43,8 @@ EXPORTS = (
     "hyd_assign_workspace_ragged",
     "hyd_assign_key_offset_ragged",
     "hyd_assign_host_ragged",
+    "hyd_dp_workspace",
+    "hyd_dp_propose",
     "hyd_alg1_workspace",
     "hyd_alg1_permutations",
     "hyd_dispatch_alg1",
@@ -88,6 +90,8 @@ def lib():
         "hyd_assign_workspace_ragged": ([I, I, I, I, I, I, I], Z),
         "hyd_assign_key_offset_ragged": ([I, I, I, I, I, I, I], Z),
         "hyd_assign_host_ragged": ([P, I, P, I, P, I, I, P, P, I, I, P, P, P, P, P, P, REDUCE_FN, P, P, Z, P], I),
+        "hyd_dp_workspace": ([I, I], Z),
+        "hyd_dp_propose": ([P, I, P, I, I, I, I, I, P, P, P, P, P, P, P, P, P, Z, P], I),
         "hyd_alg1_workspace": ([I], Z),
         "hyd_alg1_permutations": ([U64, I, I, I, P, P], I),
         "hyd_dispatch_alg1": ([P, P, I, I, I, P, I, P, P, I, I, I, P, P, P, P, P, P, P, P, Z, P], I),
@@ -219,6 +223,21 @@ def assign_host_ragged(len_host_ptr, n_iter, off_host_ptr, batch_max, schemes_ho
                                         win_pipe_ptr, win_mb_ptr, win_v_ptr, win_ptime_ptr, status_ptr, cb, None,
                                         _dev(ws), ws.numel() * ws.element_size(), _stream(stream)),
            "hyd_assign_host_ragged")
+
+
+DP_MAX_ROUND = 64
+
+
+def dp_workspace(n_schemes, J) -> int:
+    return int(lib().hyd_dp_workspace(n_schemes, J))
+
+
+def dp_propose(lengths, n_seq, schemes, n_schemes, step, J, n_gpus, scale, t_num, t_den, choice, counts, rows, valid,
+               keep, status, ws, stream=None):
+    _check(lib().hyd_dp_propose(_dev(lengths), n_seq, _dev(schemes), n_schemes, step, J, n_gpus, scale, _dev(t_num),
+                                _dev(t_den), _dev(choice), _dev(counts), _dev(rows), _dev(valid), _dev(keep),
+                                _dev(status), _dev(ws), ws.numel() * ws.element_size(), _stream(stream)),
+           "hyd_dp_propose")
 
 
 def alg1_workspace(n_iter) -> int:
