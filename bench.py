@@ -47,6 +47,8 @@ def parse():
                     help="NEXT-1: stage 1 = Alg. 1 with this many random trials per (c,t) (0: HYD-H1 dispatch)")
     ap.add_argument("--seed", type=int, default=2024, help="Alg. 1 permutation seed")
     ap.add_argument("--candidates", type=int, default=0, help="diagnostics: first N candidates only (0: all)")
+    ap.add_argument("--gap", action="store_true",
+                    help="NEXT-4: exact Eq. 3 optimum (branch-and-bound) vs the heuristics on 20-sequence iterations")
     ap.add_argument("--dp", action="store_true",
                     help="NEXT-3: time the strategy-proposal DP on the paper's grid (64 GPUs, 0.1 steps, 128-token "
                          "buckets to 32K) instead of the assignment path")
@@ -233,6 +235,59 @@ def dp_transitions(schemes, step, J, n_gpus, scale):
     return tot
 
 
+def run_gap(args):
+    """NEXT-4 bench line: exact Eq. 3 optima at scale and the heuristics' gap."""
+    import torch
+
+    from paper_2412_07894_b200 import assign, hyd
+
+    B, It, Cn, node_limit = 20, 64, 4096, 1 << 22
+    base = wl.make_workload(4, n_cand=Cn, n_iter=1)
+    rng = np.random.default_rng(2024)
+    L = wl.lengths_lognormal(rng, It * B, hi=32768).reshape(It, B)
+    W = wl.Workload(0, "gap-20seq", L, base.schemes, base.cand, base.cand_np, base.k_pad)
+    Ld = assign.lengths_to_device(L)
+    A = assign.Assigner(W.schemes, W.cand, W.cand_np, It, B, W.k_pad)
+    A1 = assign.Assigner(W.schemes, W.cand, W.cand_np, It, B, W.k_pad, trials=100, seed=args.seed)
+    pc = np.repeat(np.arange(Cn), It).astype(np.int32)
+    pt = np.tile(np.arange(It), Cn).astype(np.int32)
+    for _ in range(max(1, args.warmup)):
+        A.eq3_exact(Ld, pc[:4096], pt[:4096], node_limit)
+    torch.cuda.synchronize()
+    l0 = hyd.kernel_launches()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    val, pipe, nodes, proved = A.eq3_exact(Ld, pc, pt, node_limit)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    launches = hyd.kernel_launches() - l0
+    A.run(Ld)
+    A1.run(Ld)
+    lb = A.numpy()["lb"][pc, pt]
+    lb1 = A1.numpy()["lb"][pc, pt]
+    feas = (val != np.uint64(2**64 - 1)) & proved
+    opt = val[feas].astype(np.float64)
+    r_h1 = lb[feas].astype(np.float64) / opt
+    r_a1 = lb1[feas].astype(np.float64) / opt
+    line = {
+        "metric": "exact Eq. 3 instances/sec", "value": pc.size / (ms / 1000.0), "unit": "instances/s", "n_gpus": 1,
+        "steps": 1, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": "NEXT-4 gap study: config-4 schemes and candidates (8 pipelines), 20-sequence "
+                               "lognormal iterations", "instances": int(pc.size), "node_limit": node_limit},
+        "gap": {"proved_fraction": float(proved[val != np.uint64(2**64 - 1)].mean()),
+                "hyd_h1_within_10pct": float((r_h1 <= 1.10).mean()), "hyd_h1_mean_ratio": float(r_h1.mean()),
+                "hyd_h1_max_ratio": float(r_h1.max()),
+                "alg1_T100_within_10pct": float((r_a1 <= 1.10).mean()), "alg1_T100_mean_ratio": float(r_a1.mean()),
+                "alg1_T100_max_ratio": float(r_a1.max()),
+                "nodes_mean": float(nodes.astype(np.float64).mean()), "nodes_max": int(nodes.max())},
+        "gpu_launches": int(launches),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_dp(args):
     """NEXT-3 bench line: one proposal = histogram + DP over the whole grid + strategies + rounding."""
     import torch
@@ -306,6 +361,8 @@ def main():
         return run_reference(args)
     if args.dp:
         return run_dp(args)
+    if args.gap:
+        return run_gap(args)
     import torch
     import torch.distributed as dist
 

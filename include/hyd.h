@@ -284,6 +284,23 @@ int hyd_dp_propose(const uint32_t* lengths, int n_seq, const hyd_scheme* schemes
                    int32_t* choice, uint16_t* counts, uint8_t* rows, uint8_t* valid, uint8_t* keep,
                    uint32_t* status, void* ws, size_t ws_bytes, void* stream);
 
+/* ---- NEXT-4: exact Eq. 3 optimum for small batches (gap study P:654) --------------
+ * For each listed (pair_c[p], pair_t[p]): the minimum over every dispatch (each sequence on a
+ * pipeline with MaxLen >= l) of max_j LB_j, LB_j = sum T(l, P_j) + T(max l, P_j)(PP_j - 1)
+ * (Eq. 2), by branch-and-bound (exact pruning only), started from the HYD-H1 greedy dispatch.
+ * Inputs as hyd_dispatch (uniform batches, sorted_len / cost from hyd_cost_table).
+ * Outputs: value [n_pairs] u64 (the optimum; UINT64_MAX for an infeasible pair), pipe
+ * [n_pairs][batch] u8 (an optimal assignment by sorted position; ties between optima are not
+ * specified), nodes [n_pairs] u64 (search nodes), proved [n_pairs] u8 (0: the node budget
+ * ran out; value / pipe are then the best found).
+ * Limits: batch <= HYD_BB_MAX_BATCH, max_np <= 8. */
+#define HYD_BB_MAX_BATCH 64
+int hyd_eq3_exact(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch, int k_pad,
+                  const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
+                  const uint8_t* cand_np, int n_cand, const int32_t* pair_c, const int32_t* pair_t,
+                  int n_pairs, uint64_t node_limit, uint64_t* value, uint8_t* pipe, uint64_t* nodes,
+                  uint8_t* proved, uint32_t* status, void* stream);
+
 /* ---- host utilities --------------------------------------------------------------------
  * hyd_check_candidates: HOST tables; HYD_OK, HYD_E_INVALID or HYD_E_NOT_CANONICAL; writes
  * max over c of cand_np to *max_np_out (if non-null). */

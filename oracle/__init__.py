@@ -17,7 +17,8 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SRCS = [os.path.join(_HERE, "hydref.c"), os.path.join(_HERE, "alg1ref.c"), os.path.join(_HERE, "dpref.c")]
+_SRCS = [os.path.join(_HERE, "hydref.c"), os.path.join(_HERE, "alg1ref.c"), os.path.join(_HERE, "dpref.c"),
+         os.path.join(_HERE, "bbref.c")]
 _HDR = os.path.join(_HERE, "hydref.h")
 _LIB = os.path.join(_HERE, "libhydref.so")
 
@@ -94,6 +95,10 @@ def lib():
             _u32p, _u32p, I, I, I, _voidp, _u8p, _u8p, _i32p, _i32p, I, I, U64,
             _u8p, _u64p, _u16p, _u16p, _u64p, _u64p, _i32p, U32P, I,
         ]
+        # NEXT-4 (bbref.c)
+        L.hydref_eq3_exact.argtypes = [_u32p, _u32p, I, I, _voidp, _u8p, I, C.c_uint64, _u8p,
+                                       C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.hydref_eq3_exact.restype = I
         # NEXT-3 (dpref.c)
         L.hydref_dp_prefix.argtypes = [_u32p, I, _voidp, I, I, I, _u64p, U32P]
         L.hydref_dp_solve.argtypes = [_u64p, _voidp, I, I, I, I, I, _u64p, _u64p, _i32p]
@@ -419,3 +424,17 @@ def dp_propose(lengths, schemes, step, J, n_gpus, scale):
             if row not in rows:
                 rows.append(row)
     return rows, (pre, tn, td, ch), st
+
+
+# ------------------------------------------------------------------ NEXT-4 (bbref.c)
+def eq3_exact(sorted_len, cost_tab, schemes, cand_row, node_limit=1 << 40):
+    """Exact Eq. 3 optimum: (proved, value, pipe, nodes)."""
+    B, k_pad = cost_tab.shape
+    row = np.full(32, 0xFF, np.uint8)
+    row[: len(cand_row)] = cand_row
+    pipe = np.zeros(max(B, 1), np.uint8)
+    v, n = C.c_uint64(0), C.c_uint64(0)
+    ok = lib().hydref_eq3_exact(np.ascontiguousarray(sorted_len, np.uint32),
+                                np.ascontiguousarray(cost_tab, np.uint32).ravel(), B, k_pad, _sch_ptr(schemes), row,
+                                len(cand_row), int(node_limit), pipe, C.byref(v), C.byref(n))
+    return bool(ok), int(v.value), pipe[:B], int(n.value)

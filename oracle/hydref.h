@@ -160,6 +160,13 @@ int hydref_dp_strategy(const int32_t* choice, const uint64_t* t_den, const hydre
                        int K, int J, int n_gpus, int scale, int j, uint32_t* counts,
                        uint32_t* top_k);
 
+/* ------------------------------------------------------------------ NEXT-4 (bbref.c)
+ * Exact Eq. 3 optimum by plain depth-first enumeration (pruned by the incumbent only).
+ * Returns 1 if proved optimal within node_limit. */
+int hydref_eq3_exact(const uint32_t* sorted, const uint32_t* cost, int batch, int k_pad,
+                     const hydref_scheme* schemes, const uint8_t* cand_row, int np,
+                     uint64_t node_limit, uint8_t* pipe, uint64_t* value, uint64_t* nodes);
+
 #ifdef __cplusplus
 }
 #endif

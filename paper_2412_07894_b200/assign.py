@@ -171,6 +171,25 @@ class Assigner:
         hyd.select_best(self.makespan, It, Cn, self.cand_offset, self.key, self.status, stream)
         return self.key
 
+    def eq3_exact(self, len_dev, pair_c, pair_t, node_limit=1 << 24, stream=None):
+        """NEXT-4: exact Eq. 3 optimum of the listed (c, t) pairs (include/hyd.h hyd_eq3_exact),
+        on this workload's sorted lengths / cost table.  Returns numpy (value, pipe, nodes, proved)."""
+        torch = self.torch
+        It, B, K, kp, Cn = self.n_iter, self.batch, self.n_schemes, self.k_pad, self.n_cand
+        hyd.cost_table(len_dev, It, B, self.schemes, K, kp, self.sorted_len, self.perm, self.cost, self.status, stream)
+        pc = torch.as_tensor(np.asarray(pair_c, np.int32), device=self.dev)
+        pt = torch.as_tensor(np.asarray(pair_t, np.int32), device=self.dev)
+        n = int(pc.numel())
+        value = torch.empty((n,), dtype=torch.int64, device=self.dev)
+        pipe = torch.empty((n, B), dtype=torch.uint8, device=self.dev)
+        nodes = torch.empty((n,), dtype=torch.int64, device=self.dev)
+        proved = torch.empty((n,), dtype=torch.uint8, device=self.dev)
+        hyd.eq3_exact(self.sorted_len, self.cost, It, B, kp, self.schemes, K, self.cand, self.cand_np, Cn, pc, pt,
+                      node_limit, value, pipe, nodes, proved, self.status, stream)
+        torch.cuda.synchronize(self.dev)
+        return (value.cpu().numpy().view(np.uint64), pipe.cpu().numpy(), nodes.cpu().numpy().view(np.uint64),
+                proved.cpu().numpy().astype(bool))
+
     def pack_counters(self) -> dict:
         """Work counter written by the last hyd_pack (include/hyd.h: u64 at ws offset 16)."""
         self.torch.cuda.synchronize(self.dev)

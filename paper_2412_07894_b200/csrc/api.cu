@@ -29,6 +29,10 @@ int launch_alg1(const uint32_t*, const uint32_t*, int, int, int, const hyd_schem
                 const uint8_t*, const uint8_t*, int, int, int, const uint16_t*, uint64_t*, uint8_t*,
                 uint64_t*, hyd_pipe_stats*, uint32_t*, uint32_t*, void*, cudaStream_t);
 
+int launch_eq3_exact(const uint32_t*, const uint32_t*, int, int, int, const hyd_scheme*, int,
+                     const uint8_t*, const uint8_t*, int, const int32_t*, const int32_t*, int,
+                     unsigned long long, uint64_t*, uint8_t*, uint64_t*, uint8_t*, uint32_t*,
+                     cudaStream_t);
 size_t dp_workspace(int, int);
 int launch_dp(const uint32_t*, int, const hyd_scheme*, int, int, int, int, int, uint64_t*, uint64_t*,
               int32_t*, uint16_t*, uint8_t*, uint8_t*, uint8_t*, uint32_t*, void*, cudaStream_t);
@@ -235,6 +239,20 @@ int hyd_dispatch_alg1(const uint32_t* sorted_len, const uint32_t* cost, int n_it
   return launch_alg1(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np,
                      n_cand, max_np, trials, order, best, pipe, lb, stats, members, status, ws,
                      (cudaStream_t)stream);
+}
+
+int hyd_eq3_exact(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch, int k_pad,
+                  const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
+                  const uint8_t* cand_np, int n_cand, const int32_t* pair_c, const int32_t* pair_t,
+                  int n_pairs, uint64_t node_limit, uint64_t* value, uint8_t* pipe, uint64_t* nodes,
+                  uint8_t* proved, uint32_t* status, void* stream) {
+  if (!sorted_len || !cost || !schemes || !cand || !cand_np || !pair_c || !pair_t || !value ||
+      !pipe || !nodes || !proved || !status || n_pairs < 0 || batch > HYD_BB_MAX_BATCH ||
+      !common_ok(n_iter, batch, n_schemes, k_pad) || n_cand < 0)
+    return HYD_E_INVALID;
+  return launch_eq3_exact(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np,
+                          n_cand, pair_c, pair_t, n_pairs, node_limit, value, pipe, nodes, proved,
+                          status, (cudaStream_t)stream);
 }
 
 size_t hyd_dp_workspace(int n_schemes, int J) {

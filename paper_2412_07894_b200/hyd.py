@@ -43,6 +43,7 @@ EXPORTS = (
     "hyd_assign_workspace_ragged",
     "hyd_assign_key_offset_ragged",
     "hyd_assign_host_ragged",
+    "hyd_eq3_exact",
     "hyd_dp_workspace",
     "hyd_dp_propose",
     "hyd_alg1_workspace",
@@ -90,6 +91,7 @@ def lib():
         "hyd_assign_workspace_ragged": ([I, I, I, I, I, I, I], Z),
         "hyd_assign_key_offset_ragged": ([I, I, I, I, I, I, I], Z),
         "hyd_assign_host_ragged": ([P, I, P, I, P, I, I, P, P, I, I, P, P, P, P, P, P, REDUCE_FN, P, P, Z, P], I),
+        "hyd_eq3_exact": ([P, P, I, I, I, P, I, P, P, I, P, P, I, C.c_uint64, P, P, P, P, P, P], I),
         "hyd_dp_workspace": ([I, I], Z),
         "hyd_dp_propose": ([P, I, P, I, I, I, I, I, P, P, P, P, P, P, P, P, P, Z, P], I),
         "hyd_alg1_workspace": ([I], Z),
@@ -223,6 +225,17 @@ def assign_host_ragged(len_host_ptr, n_iter, off_host_ptr, batch_max, schemes_ho
                                         win_pipe_ptr, win_mb_ptr, win_v_ptr, win_ptime_ptr, status_ptr, cb, None,
                                         _dev(ws), ws.numel() * ws.element_size(), _stream(stream)),
            "hyd_assign_host_ragged")
+
+
+BB_MAX_BATCH = 64
+
+
+def eq3_exact(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, pair_c, pair_t,
+              node_limit, value, pipe, nodes, proved, status, stream=None):
+    _check(lib().hyd_eq3_exact(_dev(sorted_len), _dev(cost), n_iter, batch, k_pad, _dev(schemes), n_schemes,
+                               _dev(cand), _dev(cand_np), n_cand, _dev(pair_c), _dev(pair_t), int(pair_c.numel()),
+                               int(node_limit), _dev(value), _dev(pipe), _dev(nodes), _dev(proved), _dev(status),
+                               _stream(stream)), "hyd_eq3_exact")
 
 
 DP_MAX_ROUND = 64
