@@ -366,7 +366,7 @@ int launch_iter_bound(const uint32_t* cost, int n_iter, int batch, const uint32_
 // alone (before staging anything), so the common packed case runs with the packed kernel's
 // smaller register footprint.
 template <int DP, bool STAGED, int MODE>
-__global__ void __launch_bounds__(kDispatchThreads)
+__global__ void __launch_bounds__(kDispatchThreads, (MODE == 0 && DP == 8) ? 5 : 1)
     k_dispatch(const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ cost,
                int n_iter, int batch, const uint32_t* __restrict__ off, size_t n_total, int k_pad,
                const hyd_scheme* __restrict__ schemes,
