@@ -579,7 +579,7 @@ def roofline(name, ms, W, A, pk, how, local_ci):
         ops = 6.0 * cnt["bin_evals"]  # ~6 int32 ops per (item, bin) evaluation
         achieved = ops / (ms / 1000.0) / 1e9
         traffic, src = ncu_traffic(W.cfg, ("k_pack_",))
-        return {"kernel": "pack (k_pack_init + k_pack_lanes + k_pack_big)", "bound": "alu", "achieved": achieved,
+        return {"kernel": "pack (k_pack_lanes + k_pack_big)", "bound": "alu", "achieved": achieved,
                 "peak": alu_peak, "unit": "Gop/s", "frac": achieved / alu_peak, "traffic": traffic,
                 "traffic_unit": "bytes/launch (dram read+write, ncu --set full)", "traffic_source": src,
                 "algorithmic_bytes_per_launch": local_ci * (3 * B + 10 * D + 8),

@@ -19,7 +19,8 @@
 //   are then copied to mb.
 //
 // Three kernels (all stream-ordered after hyd_dispatch, which supplies U, S, sumT, tau_max):
-//   k_pack_init: per (c,t) makespan = 0 / UINT64_MAX, v/ptime rows zeroed, infeasible mb rows.
+//   (the VMAX-16 pass also writes every (c,t) row of v / ptime / makespan and the mb rows of
+//    infeasible pairs, so no separate initialisation kernel runs)
 //   k_pack_lanes: one LANE per pipeline task, persistent inside a CTA that owns one iteration
 //     (its lengths + cost rows staged in smem) and ~2048 (c,j) tasks sorted into VMAX classes
 //     8 / 16 by V_a.  Each loop iteration advances one sequence of the lane's current LPT run
@@ -182,38 +183,6 @@ __device__ __forceinline__ void search_take(Search& s, uint32_t V, uint64_t maxb
 // ------------------------------------------------------------------ pair-level init
 // makespan = 0 (feasible) or UINT64_MAX (infeasible); v/ptime rows zeroed; infeasible
 // pairs get mb = 0xFFFF.  Tasks then write their v/ptime slot and atomicMax the makespan.
-__global__ void __launch_bounds__(256) k_pack_init(const hyd_pipe_stats* __restrict__ stats,
-                                                   int mnp, int n_iter, int batch,
-                                                   const uint32_t* __restrict__ off, size_t n_total,
-                                                   int n_cand, uint16_t* __restrict__ mb,
-                                                   uint16_t* __restrict__ v,
-                                                   uint64_t* __restrict__ ptime,
-                                                   uint64_t* __restrict__ makespan) {
-  const size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (e >= (size_t)n_iter * n_cand) return;
-  const int t = (int)(e / n_cand), c = (int)(e - (size_t)t * n_cand);
-  const size_t row = (size_t)c * n_iter + t;
-  const bool feasible = stats[e * mnp].u != 0xFFFFFFFFu;  // e = t * n_cand + c
-  makespan[(size_t)t * n_cand + c] = feasible ? 0ull : ~0ull;
-  uint4* v4 = reinterpret_cast<uint4*>(v + row * HYD_MAX_PIPES);
-  uint4* p4 = reinterpret_cast<uint4*>(ptime + row * HYD_MAX_PIPES);
-  const uint4 z = make_uint4(0, 0, 0, 0);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) v4[q] = z;
-#pragma unroll
-  for (int q = 0; q < 16; ++q) p4[q] = z;
-  if (!feasible) {
-    const int bt = geo_bt(off, batch, t);
-    uint16_t* mrow = mb + (size_t)c * n_total + geo_base(off, batch, t);
-    if ((bt & 7) == 0 && ((size_t)mrow & 15) == 0) {
-      const uint4 f = make_uint4(~0u, ~0u, ~0u, ~0u);
-      for (int q = 0; q < bt / 8; ++q) reinterpret_cast<uint4*>(mrow)[q] = f;
-    } else {
-      for (int i = 0; i < bt; ++i) mrow[i] = 0xFFFF;
-    }
-  }
-}
-
 // ------------------------------------------------------------------ persistent lanes (V <= 32)
 // bins as packed u32 keys: key_b = time_b << SH | b, tokens tok_b.  SH = 4 for VMAX 16
 // (sumT < 2^27), 5 for VMAX 32 (sumT < 2^26).  masked_b = key_b | ((cap - tok_b) & 2^31) is
@@ -440,9 +409,9 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
       if (!((a.flags[bit >> 5] >> (bit & 31)) & 1u)) continue;
     }
     const hyd_pipe_stats* sp = a.stats + (fbase + e - j);
-    if (VM == 16 && sp[0].u == 0xFFFFFFFFu) continue;  // infeasible pair: k_pack_init wrote it
+    if (VM == 16 && sp[0].u == 0xFFFFFFFFu) continue;  // infeasible pair: rows written below
     const hyd_pipe_stats st = sp[j];
-    if (st.u == 0) continue;  // empty pipeline: V = ptime = 0 (k_pack_init)
+    if (st.u == 0) continue;  // empty pipeline: V = ptime = 0 (row writes)
     const uint32_t k = a.cand[(size_t)c * HYD_MAX_PIPES + j];
     Search s;
     s.M = s_ml[k];
@@ -485,7 +454,54 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
   }
   __syncthreads();
   const int nrec = min(s_nrec, ncap);
-  if (nrec == 0) return;
+  // VMAX-16 pass: this CTA owns the (c, t) rows of its tile and writes them whole -- v and ptime
+  // (32 slots: its tasks' results, 0 elsewhere; tasks handed to later passes overwrite their
+  // slot), makespan (max over its tasks; later passes atomicMax into it) and, for an infeasible
+  // pair, UINT64_MAX and a 0xFFFF mb row -- one warp per candidate, full-sector row stores.
+  auto write_rows = [&](int nr) {
+    uint16_t* map = R.perm;  // free after phase 1: tile task id -> record slot
+    for (int e = tid; e < ntile; e += kLaneThreads) map[e] = 0xFFFFu;
+    __syncthreads();
+    for (int r = tid; r < nr; r += kLaneThreads)
+      if (R.state[r] != 1) map[R.eid[r]] = (uint16_t)r;
+    __syncthreads();
+    const int warp = tid >> 5;
+    for (int cc = warp; cc < ncl; cc += kLaneThreads / 32) {
+      const int c = c0 + cc;
+      const size_t row = (size_t)c * a.n_iter + t;
+      const bool feasible = a.stats[(fbase + (size_t)cc * mnp)].u != 0xFFFFFFFFu;
+      auto slot_key = [&](int j) -> unsigned long long {
+        if (j >= mnp || !feasible) return 0ull;
+        const uint16_t r = map[cc * mnp + j];
+        return r == 0xFFFFu ? 0ull : R.key[r];
+      };
+      unsigned long long mx = 0ull;
+      if (lane < 4) {  // v: 8 slots per 16-byte chunk
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          w[q] = (uint32_t)(slot_key(8 * lane + 2 * q) & 0xFFFFu) |
+                 ((uint32_t)(slot_key(8 * lane + 2 * q + 1) & 0xFFFFu) << 16);
+        reinterpret_cast<uint4*>(a.v + row * HYD_MAX_PIPES)[lane] = make_uint4(w[0], w[1], w[2], w[3]);
+      } else if (lane < 20) {  // ptime: 2 slots per 16-byte chunk
+        const int j = 2 * (lane - 4);
+        const unsigned long long p0 = slot_key(j) >> 16, p1 = slot_key(j + 1) >> 16;
+        mx = max(p0, p1);
+        reinterpret_cast<ulonglong2*>(a.ptime + row * HYD_MAX_PIPES)[lane - 4] = make_ulonglong2(p0, p1);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(HYD_FULL, mx, o));
+      if (lane == 0) a.makespan[(size_t)t * a.n_cand + c] = feasible ? (uint64_t)mx : ~0ull;
+      if (!feasible) {
+        uint16_t* mrow = a.mb + (size_t)c * a.n_total + tbase;
+        for (int i = lane; i < B; i += 32) mrow[i] = 0xFFFF;
+      }
+    }
+  };
+  if (nrec == 0) {
+    if (VM == 16) write_rows(0);
+    return;
+  }
   if (tid == 0) {  // exclusive scan over the 64 buckets in descending order
     int run = 0;
     for (int b = NB - 1; b >= 0; --b) {
@@ -788,8 +804,13 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
   phase_clock(4);
   phase_clock(5);
   if (VM == 16 && tid == 0) atomicAdd(a.why + 15, (unsigned long long)nrec);
-  // ---- outputs (parallel over tasks)
-  for (int r = tid; r < nrec; r += kLaneThreads) {
+  // ---- outputs
+  if (VM == 16) {
+    write_rows(nrec);
+    if (ev) atomicAdd(a.evals, (unsigned long long)ev);
+    return;
+  }
+  for (int r = tid; r < nrec; r += kLaneThreads) {  // VMAX-32 pass: its tasks' slots only
     if (R.state[r] == 1) continue;
     const int e = (int)R.eid[r];
     const int c = c0 + e / mnp, j = e % mnp;
@@ -1132,12 +1153,7 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
   if (e != cudaSuccess) return record_cuda_error(e);
   e = cudaMemsetAsync(a.flags, 0, flag_bytes(n_iter, n_cand, max_np), s);
   if (e != cudaSuccess) return record_cuda_error(e);
-  const size_t pairs = (size_t)n_iter * n_cand;
-  k_pack_init<<<(unsigned)((pairs + 255) / 256), 256, 0, s>>>(stats, max_np, n_iter, batch, off, n_total, n_cand,
-                                                              mb, v, ptime, makespan);
-  note_launch();
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return record_cuda_error(e);
+  // (v / ptime / makespan rows and infeasible mb rows are written whole by the VMAX-16 pass)
 
   // persistent lanes: pass 1 (VMAX 16) CTA = one iteration x tc candidates (~2048 tasks);
   // pass 2 (VMAX 32, flagged tasks, compacted records) CTA = one whole iteration
