@@ -184,10 +184,11 @@ __device__ __forceinline__ void search_take(Search& s, uint32_t V, uint64_t maxb
 // makespan = 0 (feasible) or UINT64_MAX (infeasible); v/ptime rows zeroed; infeasible
 // pairs get mb = 0xFFFF.  Tasks then write their v/ptime slot and atomicMax the makespan.
 // ------------------------------------------------------------------ persistent lanes (V <= 32)
-// bins as packed u32 keys: key_b = time_b << SH | b, tokens tok_b.  SH = 4 for VMAX 16
-// (sumT < 2^27), 5 for VMAX 32 (sumT < 2^26).  masked_b = key_b | ((cap - tok_b) & 2^31) is
-// >= 2^31 iff tok_b + l > MaxLen, so the minimum masked key is the least-time fitting bin with
-// the smallest index.
+// bins as packed u32 keys: key_b = time_b << SH | b, and rem_b = MaxLen - tokens of bin b.
+// SH = 4 for VMAX 16 (sumT < 2^27), 5 for VMAX 32 (sumT < 2^26).  masked_b = key_b |
+// ((rem_b - l) & 2^31) is >= 2^31 iff tok_b + l > MaxLen, so the minimum masked key is the
+// least-time fitting bin with the smallest index; the chosen bin's new rem is rem_b - l, the
+// difference the mask already formed.
 template <int VM>
 struct LaneCfg {
   static constexpr int SH = VM <= 16 ? 4 : 5;
@@ -196,10 +197,10 @@ struct LaneCfg {
 
 template <int N, int VM>
 __device__ __forceinline__ uint32_t argmin_keys(const uint32_t (&keys)[VM],
-                                                const uint32_t (&toks)[VM], uint32_t cap) {
+                                                const uint32_t (&rem)[VM], uint32_t l) {
   uint32_t m[N];
 #pragma unroll
-  for (int b = 0; b < N; ++b) m[b] = keys[b] | ((cap - toks[b]) & 0x80000000u);
+  for (int b = 0; b < N; ++b) m[b] = keys[b] | ((rem[b] - l) & 0x80000000u);
 #pragma unroll
   for (int w = N / 2; w > 0; w >>= 1)
 #pragma unroll
@@ -207,18 +208,18 @@ __device__ __forceinline__ uint32_t argmin_keys(const uint32_t (&keys)[VM],
   return m[0];
 }
 
-// place the item in the bin whose key is mk: one compare and two predicated adds per bin
-// (the C++ form compiles to compare + 2 SEL + 2 IADD)
+// place the item in the bin whose key is mk (no bin when mk = 0xFFFFFFFF): one compare and two
+// predicated updates per bin (the C++ form compiles to compare + 2 SEL + 2 IADD)
 template <int N, int VM>
-__device__ __forceinline__ void place_key(uint32_t (&keys)[VM], uint32_t (&toks)[VM], uint32_t mk,
+__device__ __forceinline__ void place_key(uint32_t (&keys)[VM], uint32_t (&rem)[VM], uint32_t mk,
                                           uint32_t tau_sh, uint32_t l) {
 #pragma unroll
   for (int b = 0; b < N; ++b)
     asm("{\n\t.reg .pred p;\n\t"
         "setp.eq.u32 p, %0, %2;\n\t"
         "@p add.u32 %0, %0, %3;\n\t"
-        "@p add.u32 %1, %1, %4;\n\t}"
-        : "+r"(keys[b]), "+r"(toks[b])
+        "@p sub.u32 %1, %1, %4;\n\t}"
+        : "+r"(keys[b]), "+r"(rem[b])
         : "r"(mk), "r"(tau_sh), "r"(l));
 }
 
@@ -258,7 +259,7 @@ __device__ __forceinline__ void prefetch_l2_block(const void* base, size_t off, 
 // One LPT run as a lane's unit of work (state carried across loop iterations).
 template <int VM>
 struct LaneUnit {
-  uint32_t keys[VM], toks[VM];
+  uint32_t keys[VM], rem[VM];  // rem_b = MaxLen - tokens of bin b
   const uint32_t* mw;
   uint16_t* mrow;
   uint32_t qw, cur, wbase, nxtw;
@@ -275,7 +276,7 @@ __device__ __forceinline__ void unit_start(LaneUnit<VM>& u, uint32_t V, uint32_t
 #pragma unroll
   for (int b = 0; b < VM; ++b) {
     u.keys[b] = (uint32_t)b < V ? (uint32_t)b : 0xFFFFFFFEu;  // unused: never fits, never 'mk'
-    u.toks[b] = 0u;
+    u.rem[b] = u.M;
   }
   u.qw = 0;
   u.cur = 0;
@@ -305,10 +306,10 @@ __device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, uint3
   u.cur &= u.cur - 1u;
   const uint32_t l = STAGED ? sm[i] : slen[i];
   const uint32_t tau = STAGED ? sm[B + i * kp + u.k] : cst[(size_t)i * kp + u.k];
-  const uint32_t m0 = argmin_keys<N, VM>(u.keys, u.toks, u.M - l);
+  const uint32_t m0 = argmin_keys<N, VM>(u.keys, u.rem, l);
   const bool ok = valid && (m0 >> 31) == 0u;
   const uint32_t mk = ok ? m0 : 0xFFFFFFFFu;  // matches no bin key: placement is a no-op
-  place_key<N, VM>(u.keys, u.toks, mk, tau << SH, l);
+  place_key<N, VM>(u.keys, u.rem, mk, tau << SH, l);
   u.mx = ok ? max(u.mx, (mk >> SH) + tau) : u.mx;
   if (u.write && ok) u.mrow[i] = (uint16_t)(mk & ((1u << SH) - 1u));
   ev += valid ? u.V : 0u;
