@@ -288,6 +288,21 @@ def run_gap(args):
     return 0
 
 
+def dp_probes(schemes, step, J, n_gpus, scale):
+    """(k, d) pairs the GPU evaluates, each by two binary searches over l' (~2 log2 j + 2 probes)."""
+    import math
+
+    g = [int(s["tp"]) * int(s["pp"]) * int(s["cp"]) for s in schemes]
+    ml = [int(s["max_len"]) for s in schemes]
+    NV = n_gpus * scale
+    tot = 0
+    for j in range(1, J + 1):
+        ks = [k for k in range(len(schemes)) if ml[k] >= j * step]
+        pairs = sum(sum(nu // g[k] for k in ks) for nu in range(1, NV + 1))
+        tot += pairs * (2 * math.ceil(math.log2(j + 1)) + 2)
+    return tot
+
+
 def run_dp(args):
     """NEXT-3 bench line: one proposal = histogram + DP over the whole grid + strategies + rounding."""
     import torch
@@ -334,7 +349,8 @@ def run_dp(args):
     pk, how = peaks()
     sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
     alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e9
-    ops = 24.0 * trans  # ~24 int ops per transition (two 64x64->128 products, compares)
+    probes = dp_probes(W.schemes, step, J, N, scale)
+    ops = 24.0 * probes  # ~24 int ops per probe (two 64x64->128 products, compares)
     achieved = ops / (ms / 1000.0) / 1e9
     line = {
         "metric": "strategy-proposal DP transitions/sec", "value": trans / (ms / 1000.0), "unit": "transitions/s",
@@ -343,6 +359,7 @@ def run_dp(args):
         "data": "synthetic",
         "config": {"workload": "NEXT-3 proposal DP, cfg6 length sample", "n_sequences": int(lens.size),
                    "length_step": step, "buckets": J, "gpus": N, "gpu_step": 1 / scale, "transitions": trans,
+                   "probes_evaluated": probes,
                    "proposed_candidates": int(len(sel))},
         "roofline": {"kernel": "k_dp_solve", "bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Gop/s",
                      "frac": achieved / alu_peak, "traffic": None,

@@ -10,8 +10,8 @@
 // Kernels: k_dp_hist (per-CTA shared histograms of sum T per (scheme, length bucket), one
 // pass over the lengths), k_dp_scan (prefix sums per scheme), k_dp_solve (cooperative: one CTA
 // per l, all levels n in order with a grid barrier between them -- level n reads only levels
-// < n; the CTA's threads split the (k, d, l') transitions and reduce the lexicographic
-// (value, choice) minimum), k_dp_strategy (thread per l: follow the recorded choices from
+// < n; the CTA's threads split the (k, d) pairs, each finds its best l' by binary search on the
+// monotone halves of max(t, W/d), and the CTA reduces the lexicographic (value, choice) minimum), k_dp_strategy (thread per l: follow the recorded choices from
 // (N, l), per-scheme d totals), k_dp_round (thread per l: floor/ceil of every d, within N GPUs),
 // k_dp_unique (first occurrence of each rounded candidate).
 #include <cooperative_groups.h>
@@ -122,29 +122,72 @@ __global__ void __launch_bounds__(kDpThreads)
     // candidate: carry t[nu - 1][j] (choice -1), then every (k, mu, j')
     uint64_t bn = t_num[(size_t)(nu - 1) * W1 + j], bd = t_den[(size_t)(nu - 1) * W1 + j];
     int32_t bc = -1;
+    // (k, mu) pairs split over the threads; for each pair the best l' by binary search:
+    // f(j') = t[nu - mu N_k][j - j'] is non-increasing in j' (t is non-decreasing in l) and
+    // g(j') = scale W_k(j - j', j) / mu non-decreasing, so max(f, g) falls then rises -- its
+    // minimum is at the first j' with g >= f (value g) or just before it (value f, taken at the
+    // first j' of f's plateau); the smaller (value, j') of the two is the exact argmin the
+    // enumeration of every j' would return (ties: smaller j', as the choice code orders them).
+    const unsigned long long* ppre = s_pre;
+    int pair = 0;
     for (int k = 0; k < K; ++k) {
       if (!s_ok[k]) continue;
       const int mumax = nu / (int)s_g[k];
-      const int cnt = mumax * j;  // (mu, j') pairs
-      const unsigned long long* pk = s_pre + (size_t)k * W1;
+      const unsigned long long* pk = ppre + (size_t)k * W1;
       const unsigned long long pj = pk[j];
-      for (int e = tid; e < cnt; e += kDpThreads) {
-        const int mu = 1 + e / j, jp = 1 + (e - (mu - 1) * j);
-        const int nrest = nu - mu * (int)s_g[k];
-        const size_t r = (size_t)nrest * W1 + (j - jp);
-        uint64_t vn = (uint64_t)scale * (pj - pk[j - jp]), vd = (uint64_t)mu;
-        const uint64_t rn = t_num[r], rd = t_den[r];
-        if (q_less(vn, vd, rn, rd)) {  // max(t[rest], W / d)
-          vn = rn;
-          vd = rd;
+      for (int mu = 1 + ((tid - pair) % kDpThreads + kDpThreads) % kDpThreads; mu <= mumax;
+           mu += kDpThreads) {
+        const size_t rbase = (size_t)(nu - mu * (int)s_g[k]) * W1 + j;  // f(j') = t[rbase - j']
+        auto f_at = [&](int jp, uint64_t& fn, uint64_t& fd) {
+          fn = t_num[rbase - jp];
+          fd = t_den[rbase - jp];
+        };
+        auto g_at = [&](int jp, uint64_t& gn, uint64_t& gd) {
+          gn = (uint64_t)scale * (pj - pk[j - jp]);
+          gd = (uint64_t)mu;
+        };
+        // c = first j' in [1, j] with g >= f (j + 1 if none)
+        int lo = 1, hi = j + 1;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          uint64_t fn, fd, gn, gd;
+          f_at(mid, fn, fd);
+          g_at(mid, gn, gd);
+          if (!q_less(gn, gd, fn, fd)) hi = mid;
+          else lo = mid + 1;
         }
-        const int32_t code = (int32_t)(((uint32_t)k << 24) | ((uint32_t)mu << 12) | (uint32_t)jp);
-        if (key_less(vn, vd, code, bn, bd, bc)) {
-          bn = vn;
-          bd = vd;
-          bc = code;
+        const int c = lo;
+        const uint32_t codebase = ((uint32_t)k << 24) | ((uint32_t)mu << 12);
+        if (c <= j) {  // candidate A: j' = c, value g(c)
+          uint64_t gn, gd;
+          g_at(c, gn, gd);
+          const int32_t code = (int32_t)(codebase | (uint32_t)c);
+          if (key_less(gn, gd, code, bn, bd, bc)) {
+            bn = gn;
+            bd = gd;
+            bc = code;
+          }
+        }
+        if (c > 1) {  // candidate B: value f(c - 1), at the first j' of its plateau
+          uint64_t vn, vd;
+          f_at(c - 1, vn, vd);
+          int l2 = 1, h2 = c - 1;  // first j' in [1, c - 1] with f(j') <= f(c - 1)
+          while (l2 < h2) {
+            const int mid = (l2 + h2) >> 1;
+            uint64_t fn, fd;
+            f_at(mid, fn, fd);
+            if (!q_less(vn, vd, fn, fd)) h2 = mid;  // f(mid) <= v
+            else l2 = mid + 1;
+          }
+          const int32_t code = (int32_t)(codebase | (uint32_t)l2);
+          if (key_less(vn, vd, code, bn, bd, bc)) {
+            bn = vn;
+            bd = vd;
+            bc = code;
+          }
         }
       }
+      pair += mumax;
     }
     // block-wide lexicographic minimum
 #pragma unroll
