@@ -301,6 +301,19 @@ int hyd_eq3_exact(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, 
                   int n_pairs, uint64_t node_limit, uint64_t* value, uint8_t* pipe, uint64_t* nodes,
                   uint8_t* proved, uint32_t* status, void* stream);
 
+/* Exact Eq. 1 per listed pipeline (pair_c, pair_t, pair_j) of a dispatched batch
+ * (members / sorted_len / cost from hyd_dispatch and hyd_cost_table): min over V in App. D's
+ * range (extended upward while none is feasible) and every split of the pipeline's sequences
+ * into V non-empty micro-batches within MaxLen of (max micro-batch time)(PP - 1 + V), ties to
+ * the smaller V, by branch-and-bound from the LPT(V) incumbent.  Outputs v [n] u32 (0 if the
+ * pipeline is empty or nothing was proved), obj [n] u64, nodes [n] u64, proved [n] u8.
+ * Limits: at most 32 sequences per pipeline (larger ones report proved = 0). */
+int hyd_eq1_exact(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch, int k_pad,
+                  const hyd_scheme* schemes, int n_schemes, const uint8_t* cand, int n_cand,
+                  int max_np, const uint32_t* members, const int32_t* pair_c, const int32_t* pair_t,
+                  const int32_t* pair_j, int n_pairs, uint64_t node_limit, uint32_t* v,
+                  uint64_t* obj, uint64_t* nodes, uint8_t* proved, uint32_t* status, void* stream);
+
 /* ---- host utilities --------------------------------------------------------------------
  * hyd_check_candidates: HOST tables; HYD_OK, HYD_E_INVALID or HYD_E_NOT_CANONICAL; writes
  * max over c of cand_np to *max_np_out (if non-null). */

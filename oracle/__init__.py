@@ -99,6 +99,9 @@ def lib():
         L.hydref_eq3_exact.argtypes = [_u32p, _u32p, I, I, _voidp, _u8p, I, C.c_uint64, _u8p,
                                        C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.hydref_eq3_exact.restype = I
+        L.hydref_eq1_exact.argtypes = [_u32p, _u32p, I, _voidp, C.c_uint64, C.POINTER(C.c_uint32),
+                                       C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.hydref_eq1_exact.restype = I
         # NEXT-3 (dpref.c)
         L.hydref_dp_prefix.argtypes = [_u32p, I, _voidp, I, I, I, _u64p, U32P]
         L.hydref_dp_solve.argtypes = [_u64p, _voidp, I, I, I, I, I, _u64p, _u64p, _i32p]
@@ -438,3 +441,13 @@ def eq3_exact(sorted_len, cost_tab, schemes, cand_row, node_limit=1 << 40):
                                 np.ascontiguousarray(cost_tab, np.uint32).ravel(), B, k_pad, _sch_ptr(schemes), row,
                                 len(cand_row), int(node_limit), pipe, C.byref(v), C.byref(n))
     return bool(ok), int(v.value), pipe[:B], int(n.value)
+
+
+def eq1_exact(ell, tau, scheme_row, node_limit=1 << 40):
+    """Exact Eq. 1 optimum of one pipeline: (proved, V, obj, nodes)."""
+    ell = np.ascontiguousarray(ell, np.uint32)
+    tau = np.ascontiguousarray(tau, np.uint32)
+    sch = np.ascontiguousarray(np.atleast_1d(scheme_row))
+    v, o, n = C.c_uint32(0), C.c_uint64(0), C.c_uint64(0)
+    ok = lib().hydref_eq1_exact(ell, tau, ell.size, _sch_ptr(sch), int(node_limit), C.byref(v), C.byref(o), C.byref(n))
+    return bool(ok), int(v.value), int(o.value), int(n.value)

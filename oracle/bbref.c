@@ -93,3 +93,98 @@ int hydref_eq3_exact(const uint32_t* sorted, const uint32_t* cost, int batch, in
   free(s);
   return proved; /* 1: value is the exact optimum; 0: infeasible, too large or node limit hit */
 }
+
+/* ---------------------------------------------------------------- Eq. 1 exact
+ * Eq. 1 for one pipeline: min over V in App. D's range (reading 5, extended upward
+ * while no V is feasible) and over every split of the items into V micro-batches with
+ * sum l <= MaxLen of (max micro-batch time) (PP - 1 + V); ties to the smaller V.  Plain
+ * depth-first enumeration: item by item (given order), every bin, pruned only by "the partial
+ * maximum already reaches the best for this V" (bin times never decrease). */
+typedef struct {
+  const uint32_t* ell;
+  const uint32_t* tau;
+  int u, v;
+  uint32_t M;
+  uint64_t t[64];
+  uint32_t tok[64];
+  uint64_t best;
+  uint64_t nodes, limit;
+  int exhausted;
+} pk_t;
+
+static void pk_dfs(pk_t* s, int i, uint64_t pmax) {
+  if (s->exhausted) return;
+  if (++s->nodes > s->limit) {
+    s->exhausted = 1;
+    return;
+  }
+  if (i == s->u) {
+    int empty = 0;
+    for (int b = 0; b < s->v; ++b) empty |= s->tok[b] == 0; /* V non-empty micro-batches */
+    if (!empty && pmax < s->best) s->best = pmax;
+    return;
+  }
+  for (int b = 0; b < s->v; ++b) {
+    if (s->tok[b] + s->ell[i] > s->M) continue;
+    const uint64_t nt = s->t[b] + s->tau[i];
+    const uint64_t nm = nt > pmax ? nt : pmax;
+    if (nm >= s->best) continue;
+    s->t[b] = nt;
+    s->tok[b] += s->ell[i];
+    pk_dfs(s, i + 1, nm);
+    s->t[b] -= s->tau[i];
+    s->tok[b] -= s->ell[i];
+  }
+}
+
+int hydref_eq1_exact(const uint32_t* ell, const uint32_t* tau, int u, const hydref_scheme* sch,
+                     uint64_t node_limit, uint32_t* v_out, uint64_t* obj_out, uint64_t* nodes) {
+  *v_out = 0;
+  *obj_out = 0;
+  *nodes = 0;
+  if (u == 0) return 1;
+  if (u > 64) return 0;
+  uint64_t S = 0;
+  for (int i = 0; i < u; ++i) S += ell[i];
+  const uint32_t M = sch->max_len, P = sch->pp;
+  uint32_t vlo = (uint32_t)((S + M - 1) / M);
+  if (vlo < 1) vlo = 1;
+  uint32_t vhi = (uint32_t)u;
+  if (sch->util_len) {
+    const uint64_t q = S / sch->util_len;
+    vhi = q < (uint64_t)u ? (uint32_t)q : (uint32_t)u;
+  }
+  if (vhi < vlo) vhi = vlo;
+  pk_t* s = (pk_t*)calloc(1, sizeof(pk_t));
+  s->ell = ell;
+  s->tau = tau;
+  s->u = u;
+  s->M = M;
+  s->limit = node_limit;
+  uint64_t best = UINT64_MAX;
+  uint32_t vbest = 0;
+  int proved = 1;
+  for (uint32_t V = vlo; V <= (uint32_t)u; ++V) {
+    if (V > vhi && vbest != 0) break; /* extension only while nothing in range is feasible */
+    if (V > 64) break;
+    s->v = (int)V;
+    memset(s->t, 0, sizeof(s->t));
+    memset(s->tok, 0, sizeof(s->tok));
+    s->best = UINT64_MAX;
+    s->exhausted = 0;
+    pk_dfs(s, 0, 0);
+    if (s->exhausted) proved = 0;
+    if (s->best != UINT64_MAX) {
+      const uint64_t obj = s->best * (uint64_t)(P - 1u + V);
+      if (obj < best) {
+        best = obj;
+        vbest = V;
+      }
+    }
+  }
+  *nodes = s->nodes;
+  free(s);
+  *v_out = vbest;
+  *obj_out = best;
+  return proved && vbest != 0;
+}

@@ -166,6 +166,11 @@ int hydref_dp_strategy(const int32_t* choice, const uint64_t* t_den, const hydre
 int hydref_eq3_exact(const uint32_t* sorted, const uint32_t* cost, int batch, int k_pad,
                      const hydref_scheme* schemes, const uint8_t* cand_row, int np,
                      uint64_t node_limit, uint8_t* pipe, uint64_t* value, uint64_t* nodes);
+/* Exact Eq. 1 for one pipeline's items (ell/tau in sorted order): min over App. D's V range
+ * (extended upward while none is feasible) and every capacity-feasible split of
+ * max-bin-time (PP-1+V), ties to the smaller V.  Returns 1 if proved within node_limit. */
+int hydref_eq1_exact(const uint32_t* ell, const uint32_t* tau, int u, const hydref_scheme* sch,
+                     uint64_t node_limit, uint32_t* v_out, uint64_t* obj_out, uint64_t* nodes);
 
 #ifdef __cplusplus
 }

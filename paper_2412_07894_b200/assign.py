@@ -190,6 +190,24 @@ class Assigner:
         return (value.cpu().numpy().view(np.uint64), pipe.cpu().numpy(), nodes.cpu().numpy().view(np.uint64),
                 proved.cpu().numpy().astype(bool))
 
+    def eq1_exact(self, pair_c, pair_t, pair_j, node_limit=1 << 24, stream=None):
+        """NEXT-4: exact Eq. 1 optimum of the listed pipelines of the LAST run() (its dispatch);
+        include/hyd.h hyd_eq1_exact.  Returns numpy (v, obj, nodes, proved)."""
+        torch = self.torch
+        It, B, K, kp, Cn = self.n_iter, self.batch, self.n_schemes, self.k_pad, self.n_cand
+        mk = lambda x: torch.as_tensor(np.asarray(x, np.int32), device=self.dev)
+        pc, pt, pj = mk(pair_c), mk(pair_t), mk(pair_j)
+        n = int(pc.numel())
+        v = torch.empty((n,), dtype=torch.int32, device=self.dev)
+        obj = torch.empty((n,), dtype=torch.int64, device=self.dev)
+        nodes = torch.empty((n,), dtype=torch.int64, device=self.dev)
+        proved = torch.empty((n,), dtype=torch.uint8, device=self.dev)
+        hyd.eq1_exact(self.sorted_len, self.cost, It, B, kp, self.schemes, K, self.cand, Cn, self.max_np, self.members,
+                      pc, pt, pj, node_limit, v, obj, nodes, proved, self.status, stream)
+        torch.cuda.synchronize(self.dev)
+        return (v.cpu().numpy().view(np.uint32), obj.cpu().numpy().view(np.uint64),
+                nodes.cpu().numpy().view(np.uint64), proved.cpu().numpy().astype(bool))
+
     def pack_counters(self) -> dict:
         """Work counter written by the last hyd_pack (include/hyd.h: u64 at ws offset 16)."""
         self.torch.cuda.synchronize(self.dev)

@@ -33,6 +33,10 @@ int launch_eq3_exact(const uint32_t*, const uint32_t*, int, int, int, const hyd_
                      const uint8_t*, const uint8_t*, int, const int32_t*, const int32_t*, int,
                      unsigned long long, uint64_t*, uint8_t*, uint64_t*, uint8_t*, uint32_t*,
                      cudaStream_t);
+int launch_eq1_exact(const uint32_t*, const uint32_t*, int, int, int, const hyd_scheme*, int,
+                     const uint8_t*, int, int, const uint32_t*, const int32_t*, const int32_t*,
+                     const int32_t*, int, unsigned long long, uint32_t*, uint64_t*, uint64_t*,
+                     uint8_t*, uint32_t*, cudaStream_t);
 size_t dp_workspace(int, int);
 int launch_dp(const uint32_t*, int, const hyd_scheme*, int, int, int, int, int, uint64_t*, uint64_t*,
               int32_t*, uint16_t*, uint8_t*, uint8_t*, uint8_t*, uint32_t*, void*, cudaStream_t);
@@ -253,6 +257,20 @@ int hyd_eq3_exact(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, 
   return launch_eq3_exact(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np,
                           n_cand, pair_c, pair_t, n_pairs, node_limit, value, pipe, nodes, proved,
                           status, (cudaStream_t)stream);
+}
+
+int hyd_eq1_exact(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch, int k_pad,
+                  const hyd_scheme* schemes, int n_schemes, const uint8_t* cand, int n_cand,
+                  int max_np, const uint32_t* members, const int32_t* pair_c, const int32_t* pair_t,
+                  const int32_t* pair_j, int n_pairs, uint64_t node_limit, uint32_t* v,
+                  uint64_t* obj, uint64_t* nodes, uint8_t* proved, uint32_t* status, void* stream) {
+  if (!sorted_len || !cost || !schemes || !cand || !members || !pair_c || !pair_t || !pair_j ||
+      !v || !obj || !nodes || !proved || !status || n_pairs < 0 ||
+      !common_ok(n_iter, batch, n_schemes, k_pad) || !cand_ok(n_cand, max_np))
+    return HYD_E_INVALID;
+  return launch_eq1_exact(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, n_cand,
+                          max_np, members, pair_c, pair_t, pair_j, n_pairs, node_limit, v, obj,
+                          nodes, proved, status, (cudaStream_t)stream);
 }
 
 size_t hyd_dp_workspace(int n_schemes, int J) {

@@ -195,3 +195,197 @@ int launch_eq3_exact(const uint32_t* sorted_len, const uint32_t* cost, int n_ite
 }
 
 }  // namespace hyd
+
+namespace hyd {
+
+// Exact Eq. 1 for one pipeline per thread: the items (the pipeline's sequences in
+// sorted order, from the membership words) split into V micro-batches within MaxLen, min over V
+// of (max micro-batch time)(PP - 1 + V) over App. D's range (upward extension while none is
+// feasible), ties to the smaller V.  Per V: iterative depth-first search item by item over the
+// bins, started from the LPT(V) packing as incumbent; pruned by the partial maximum, by LB(V) =
+// max(ceil(sum T / V), tau_max)(PP-1+V) against the best objective so far, and by symmetry (an
+// item goes to the first empty bin only); leaves must fill all V bins.
+constexpr int kE1Max = 32;  // items and micro-batches per instance
+
+__global__ void __launch_bounds__(128)
+    k_eq1_exact(const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ cost,
+                int n_iter, int batch, int k_pad, const hyd_scheme* __restrict__ schemes,
+                int n_schemes, const uint8_t* __restrict__ cand, int n_cand, int max_np,
+                const uint32_t* __restrict__ members, const int32_t* __restrict__ pair_c,
+                const int32_t* __restrict__ pair_t, const int32_t* __restrict__ pair_j, int n_pairs,
+                unsigned long long node_limit, uint32_t* __restrict__ v_out,
+                uint64_t* __restrict__ obj_out, uint64_t* __restrict__ nodes_out,
+                uint8_t* __restrict__ proved, uint32_t* __restrict__ status) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_pairs) return;
+  const int c = pair_c[p], t = pair_t[p], j = pair_j[p];
+  const int B = batch;
+  const uint32_t k = cand[(size_t)c * HYD_MAX_PIPES + j];
+  const uint32_t* sl = sorted_len + (size_t)t * B;
+  const uint32_t* cs = cost + (size_t)t * B * k_pad;
+  const int nwords = (B + 31) >> 5;
+  const uint32_t* mw = members + ((size_t)t * n_cand + c) * nwords * max_np + j;  // word-major
+  uint32_t ell[kE1Max], tau[kE1Max];
+  int U = 0;
+  uint64_t S = 0, sumT = 0;
+  uint32_t tmax = 0;
+  bool too_big = false;
+  for (int w = 0; w < nwords; ++w) {
+    uint32_t bits = mw[(size_t)w * max_np];
+    while (bits) {
+      const int i = w * 32 + __ffs(bits) - 1;
+      bits &= bits - 1u;
+      if (U == kE1Max) {
+        too_big = true;
+        break;
+      }
+      ell[U] = sl[i];
+      tau[U] = cs[(size_t)i * k_pad + k];
+      S += ell[U];
+      sumT += tau[U];
+      tmax = max(tmax, tau[U]);
+      ++U;
+    }
+  }
+  v_out[p] = 0;
+  obj_out[p] = 0;
+  nodes_out[p] = 0;
+  proved[p] = 0;
+  if (too_big || k >= (uint32_t)n_schemes) {
+    flag(status, too_big ? 0u : HYD_F_NOT_CANONICAL);
+    return;
+  }
+  if (U == 0) {
+    proved[p] = 1;
+    return;
+  }
+  const uint32_t M = schemes[k].max_len, P = schemes[k].pp, UL = schemes[k].util_len;
+  uint32_t vlo = (uint32_t)((S + M - 1) / M);
+  if (vlo < 1) vlo = 1;
+  uint32_t vhi = (uint32_t)U;
+  if (UL) vhi = (uint32_t)min((uint64_t)U, S / UL);
+  if (vhi < vlo) vhi = vlo;
+  uint64_t best = ~0ull;
+  uint32_t vbest = 0;
+  unsigned long long nodes = 0;
+  bool exhausted = false;
+  uint64_t bt[kE1Max];
+  uint32_t bk[kE1Max];
+  uint8_t nxt[kE1Max];
+  for (uint32_t V = vlo; V <= (uint32_t)U && !exhausted; ++V) {
+    if (V > vhi && vbest != 0) break;  // extension only while nothing in range is feasible
+    const uint64_t m = (uint64_t)(P - 1u + V);
+    const uint64_t lbv = max((sumT + V - 1) / V, (uint64_t)tmax);
+    if (vbest != 0 && lbv * m >= best) continue;  // cannot beat (or tie at smaller V) the best
+    // incumbent: LPT(V) with capacity (least-time fitting bin, smallest index)
+    for (uint32_t b = 0; b < V; ++b) {
+      bt[b] = 0;
+      bk[b] = 0;
+    }
+    uint64_t inc = 0;
+    bool lpt_ok = true;
+    for (int i = 0; i < U && lpt_ok; ++i) {
+      int bb = -1;
+      for (uint32_t b = 0; b < V; ++b)
+        if (bk[b] + ell[i] <= M && (bb < 0 || bt[b] < bt[bb])) bb = (int)b;
+      if (bb < 0) {
+        lpt_ok = false;
+        break;
+      }
+      bt[bb] += tau[i];
+      bk[bb] += ell[i];
+      inc = max(inc, bt[bb]);
+    }
+    uint64_t bestV = lpt_ok ? inc : ~0ull;  // best max micro-batch time for this V
+    // depth-first search for a strictly better split
+    for (uint32_t b = 0; b < V; ++b) {
+      bt[b] = 0;
+      bk[b] = 0;
+    }
+    int i = 0;
+    nxt[0] = 0;
+    uint64_t pm[kE1Max + 1];
+    pm[0] = 0;
+    uint32_t empty = V;  // bins still empty
+    uint8_t cur[kE1Max];
+    while (i >= 0) {
+      if (i == U) {
+        if (empty == 0 && pm[U] < bestV) bestV = pm[U];
+        --i;
+        if (i >= 0) {
+          const int b = cur[i];
+          bt[b] -= tau[i];
+          bk[b] -= ell[i];
+          if (bk[b] == 0) ++empty;
+          nxt[i] = (uint8_t)(b + 1);
+        }
+        continue;
+      }
+      if (++nodes > node_limit) {
+        exhausted = true;
+        break;
+      }
+      int taken = -1;
+      for (int b = nxt[i]; b < (int)V; ++b) {
+        if (bk[b] + ell[i] > M) continue;
+        if (bk[b] == 0) {  // the first empty bin only
+          bool earlier = false;
+          for (int q = 0; q < b; ++q) earlier |= bk[q] == 0;
+          if (earlier) continue;
+        }
+        if ((uint32_t)(U - i - 1) < empty - (bk[b] == 0 ? 1u : 0u)) continue;  // bins left unfillable
+        const uint64_t nm = max(pm[i], bt[b] + tau[i]);
+        if (nm >= bestV) continue;
+        taken = b;
+        break;
+      }
+      if (taken < 0) {
+        --i;
+        if (i >= 0) {
+          const int b = cur[i];
+          bt[b] -= tau[i];
+          bk[b] -= ell[i];
+          if (bk[b] == 0) ++empty;
+          nxt[i] = (uint8_t)(b + 1);
+        }
+        continue;
+      }
+      if (bk[taken] == 0) --empty;
+      bt[taken] += tau[i];
+      bk[taken] += ell[i];
+      pm[i + 1] = max(pm[i], bt[taken]);
+      cur[i] = (uint8_t)taken;
+      ++i;
+      if (i < U) nxt[i] = 0;
+    }
+    if (bestV != ~0ull) {
+      const uint64_t obj = bestV * m;
+      if (obj < best) {
+        best = obj;
+        vbest = V;
+      }
+    }
+  }
+  v_out[p] = vbest;
+  obj_out[p] = vbest ? best : ~0ull;
+  nodes_out[p] = nodes;
+  proved[p] = !exhausted && vbest != 0;
+}
+
+int launch_eq1_exact(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch,
+                     int k_pad, const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
+                     int n_cand, int max_np, const uint32_t* members, const int32_t* pair_c,
+                     const int32_t* pair_t, const int32_t* pair_j, int n_pairs,
+                     unsigned long long node_limit, uint32_t* v, uint64_t* obj, uint64_t* nodes,
+                     uint8_t* proved, uint32_t* status, cudaStream_t s) {
+  if (n_pairs == 0) return HYD_OK;
+  k_eq1_exact<<<(n_pairs + 127) / 128, 128, 0, s>>>(sorted_len, cost, n_iter, batch, k_pad, schemes,
+                                                    n_schemes, cand, n_cand, max_np, members, pair_c,
+                                                    pair_t, pair_j, n_pairs, node_limit, v, obj,
+                                                    nodes, proved, status);
+  note_launch();
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? HYD_OK : record_cuda_error(e);
+}
+
+}  // namespace hyd

@@ -44,6 +44,7 @@ EXPORTS = (
     "hyd_assign_key_offset_ragged",
     "hyd_assign_host_ragged",
     "hyd_eq3_exact",
+    "hyd_eq1_exact",
     "hyd_dp_workspace",
     "hyd_dp_propose",
     "hyd_alg1_workspace",
@@ -92,6 +93,7 @@ def lib():
         "hyd_assign_key_offset_ragged": ([I, I, I, I, I, I, I], Z),
         "hyd_assign_host_ragged": ([P, I, P, I, P, I, I, P, P, I, I, P, P, P, P, P, P, REDUCE_FN, P, P, Z, P], I),
         "hyd_eq3_exact": ([P, P, I, I, I, P, I, P, P, I, P, P, I, C.c_uint64, P, P, P, P, P, P], I),
+        "hyd_eq1_exact": ([P, P, I, I, I, P, I, P, I, I, P, P, P, P, I, C.c_uint64, P, P, P, P, P, P], I),
         "hyd_dp_workspace": ([I, I], Z),
         "hyd_dp_propose": ([P, I, P, I, I, I, I, I, P, P, P, P, P, P, P, P, P, Z, P], I),
         "hyd_alg1_workspace": ([I], Z),
@@ -236,6 +238,14 @@ def eq3_exact(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, 
                                _dev(cand), _dev(cand_np), n_cand, _dev(pair_c), _dev(pair_t), int(pair_c.numel()),
                                int(node_limit), _dev(value), _dev(pipe), _dev(nodes), _dev(proved), _dev(status),
                                _stream(stream)), "hyd_eq3_exact")
+
+
+def eq1_exact(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, n_cand, max_np, members, pair_c,
+              pair_t, pair_j, node_limit, v, obj, nodes, proved, status, stream=None):
+    _check(lib().hyd_eq1_exact(_dev(sorted_len), _dev(cost), n_iter, batch, k_pad, _dev(schemes), n_schemes,
+                               _dev(cand), n_cand, max_np, _dev(members), _dev(pair_c), _dev(pair_t), _dev(pair_j),
+                               int(pair_c.numel()), int(node_limit), _dev(v), _dev(obj), _dev(nodes), _dev(proved),
+                               _dev(status), _stream(stream)), "hyd_eq1_exact")
 
 
 DP_MAX_ROUND = 64

@@ -72,3 +72,32 @@ def test_eq3_exact_at_scale_runs(env):
     feas = val != np.uint64(2**64 - 1)
     assert proved[feas].mean() > 0.9
     assert (val[feas] <= lb[pc[feas], pt[feas]]).all()
+
+
+@pytest.mark.parametrize("B,D", [(10, 2), (16, 4)])
+def test_eq1_exact_parity(env, B, D):
+    """Exact Eq. 1 per pipeline of the GPU's own dispatch equals the oracle's (unique optimum);
+    never above the heuristic's ptime."""
+    O, assign = env["oracle"], env["assign"]
+    W = small_workload(B, D, 30, 2, 100 + B)
+    A = assign.Assigner(W.schemes, W.cand, W.cand_np, W.n_iter, W.batch, W.k_pad)
+    A.run(assign.lengths_to_device(W.lengths))
+    g = A.numpy()
+    pc, pt, pj = [], [], []
+    for c in range(W.n_cand):
+        for t in range(W.n_iter):
+            if g["makespan"][t, c] == np.uint64(2**64 - 1):
+                continue
+            for j in range(int(W.cand_np[c])):
+                pc.append(c), pt.append(t), pj.append(j)
+    v, obj, nodes, proved = A.eq1_exact(pc, pt, pj)
+    for q, (c, t, j) in enumerate(zip(pc, pt, pj)):
+        s, _, cst, _ = O.cost_table(W.lengths[t], W.schemes, W.k_pad)
+        k = int(W.cand[c, j])
+        idx = np.nonzero(g["pipe"][c, t] == j)[0]
+        ok, V, o, _ = O.eq1_exact(s[idx], cst[idx, k], W.schemes[k:k + 1])
+        if idx.size == 0:
+            assert proved[q] and v[q] == 0
+            continue
+        assert proved[q] == ok and int(obj[q]) == o and int(v[q]) == V, (c, t, j)
+        assert o <= int(g["ptime"][c, t, j])

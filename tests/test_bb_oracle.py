@@ -41,3 +41,34 @@ def test_bounds_the_heuristics_and_node_limit():
             assert okA and v <= lbA
             ok2, v2, _, n2 = oracle.eq3_exact(s, cst, W.schemes, row, node_limit=3)
             assert not ok2 and n2 > 3 and v2 >= v  # budget exhausted: not proved
+
+
+def first_feasible_above(lengths, scheme, lo, hi):
+    for v in range(hi + 1, len(lengths) + 1):
+        r = bf.pack_opt(lengths, scheme, [v])
+        if r is not None:
+            return r
+    return None
+
+
+def test_eq1_equals_exhaustive_partitions_and_bounds_lpt():
+    """Eq. 1 exact (oracle/bbref.c) against the set-partition enumeration of tests/bruteforce.py
+    over App. D's range (first feasible V above it when none is, reading 5); LPT never beats it."""
+    rng = np.random.default_rng(21)
+    n = 0
+    for _ in range(150):
+        W = w.random_small_instance(rng, int(rng.integers(1, 9)), 1)
+        k = int(W.cand[0, 0])
+        sch = W.schemes[k:k + 1]
+        s, _, cst, _ = oracle.cost_table(W.lengths[0], W.schemes, W.k_pad)
+        L = [int(x) for x in s]
+        ok, V, obj, nodes = oracle.eq1_exact(s, cst[:, k], sch)
+        lo, hi = bf.v_range(L, sch)
+        ref = bf.pack_opt(L, sch, range(lo, hi + 1))
+        if ref is None:
+            ref = first_feasible_above(L, sch, lo, hi)
+        assert ok and obj == ref
+        hv, hp, _, _ = oracle.pack_pipeline(s, cst[:, k], sch)
+        assert hp >= obj  # the LPT heuristic (HYD-H1) never beats the optimum
+        n += 1
+    assert n == 150
