@@ -33,6 +33,8 @@
 //     bins b = lane + 32 r (r < R <= 8 in registers, or global scratch beyond 256 bins); per
 //     item a redux.sync min over times, then over bin ids, picks the bin.
 //   makespan[t][c] = max_j ptime via atomicMax from the tasks.
+#include <type_traits>
+
 #include "hyd_internal.cuh"
 
 namespace hyd {
@@ -223,6 +225,37 @@ __device__ __forceinline__ void place_key(uint32_t (&keys)[VM], uint32_t (&rem)[
         : "r"(mk), "r"(tau_sh), "r"(l));
 }
 
+// Capacity-free runs (an exact shortcut): with alpha = min_i tau_i / l_i over
+// the iteration's sequences that scheme k can hold, every bin satisfies alpha * tokens <= time.
+// A run whose abort threshold thr satisfies thr <= cap_k = floor(alpha MaxLen_k) can never place
+// a sequence into a bin it overflows without that bin's time exceeding thr (which aborts the run
+// under either rule, and the capacity rule would pick a bin of no smaller time), so LPT with and
+// without the capacity mask agree step for step.  Such runs skip the mask and the token updates;
+// a warp whose units are all capacity-free takes this path (bin tokens of those units go stale,
+// which can only let a later masked step see a bin as fitting -- and every bin fits for them).
+template <int N, int VM>
+__device__ __forceinline__ uint32_t min_keys(const uint32_t (&keys)[VM]) {
+  uint32_t m[N];
+#pragma unroll
+  for (int b = 0; b < N; ++b) m[b] = keys[b];
+#pragma unroll
+  for (int w = N / 2; w > 0; w >>= 1)
+#pragma unroll
+    for (int b = 0; b < w; ++b) m[b] = min(m[b], m[b + w]);
+  return m[0];
+}
+
+template <int N, int VM>
+__device__ __forceinline__ void add_key(uint32_t (&keys)[VM], uint32_t mk, uint32_t tau_sh) {
+#pragma unroll
+  for (int b = 0; b < N; ++b)
+    asm("{\n\t.reg .pred p;\n\t"
+        "setp.eq.u32 p, %0, %1;\n\t"
+        "@p add.u32 %0, %0, %2;\n\t}"
+        : "+r"(keys[b])
+        : "r"(mk), "r"(tau_sh));
+}
+
 // per-CTA task records (compacted slots), built in parallel before the lane phases
 struct TaskRecs {
   unsigned long long* key;  // best (obj << 16 | V) found so far
@@ -266,6 +299,7 @@ struct LaneUnit {
   uint32_t V, thr, mx, k, M;
   int e;
   bool write;
+  bool F;  // capacity-free: no placement of this run can exceed MaxLen before it completes or aborts
 };
 
 template <int VM>
@@ -289,7 +323,7 @@ __device__ __forceinline__ void unit_start(LaneUnit<VM>& u, uint32_t V, uint32_t
 // takes the next one (an all-zero word costs it one idle step), and the step's placement is
 // predicated on having a member, so the warp never splits inside the bin arithmetic.
 // STAGED: lengths at sm[0, B), costs at sm[B + i * kp + k] (shared window, 32-bit addressing).
-template <int N, int VM, bool STAGED>
+template <int N, int VM, bool STAGED, bool FREE>
 __device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, uint32_t mnp, int B,
                                          const uint32_t* __restrict__ slen,
                                          const uint32_t* __restrict__ cst, int kp, uint32_t& ev) {
@@ -306,10 +340,19 @@ __device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, uint3
   u.cur &= u.cur - 1u;
   const uint32_t l = STAGED ? sm[i] : slen[i];
   const uint32_t tau = STAGED ? sm[B + i * kp + u.k] : cst[(size_t)i * kp + u.k];
-  const uint32_t m0 = argmin_keys<N, VM>(u.keys, u.rem, l);
+  uint32_t m0;
+  if constexpr (FREE) {  // capacity cannot bind: plain least-time bin, bin tokens not tracked
+    m0 = min_keys<N, VM>(u.keys);
+  } else {
+    m0 = argmin_keys<N, VM>(u.keys, u.rem, l);
+  }
   const bool ok = valid && (m0 >> 31) == 0u;
   const uint32_t mk = ok ? m0 : 0xFFFFFFFFu;  // matches no bin key: placement is a no-op
-  place_key<N, VM>(u.keys, u.rem, mk, tau << SH, l);
+  if constexpr (FREE) {
+    add_key<N, VM>(u.keys, mk, tau << SH);
+  } else {
+    place_key<N, VM>(u.keys, u.rem, mk, tau << SH, l);
+  }
   u.mx = ok ? max(u.mx, (mk >> SH) + tau) : u.mx;
   if (u.write && ok) u.mrow[i] = (uint16_t)(mk & ((1u << SH) - 1u));
   ev += valid ? u.V : 0u;
@@ -324,12 +367,13 @@ __device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, uint3
 //          exact search.
 template <bool STAGED, int VM>
 __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(PackArgs a, int tc, int mnp, int ncap) {
-  constexpr int NB = 64;  // LPT-order buckets: (class, U) descending
+  constexpr int NB = 128;  // LPT-order buckets: (class, mode, U) descending (phase 1: 64 used)
   constexpr unsigned long long kBottom = ~0ull;
   extern __shared__ __align__(16) uint32_t sm[];
   __shared__ int s_next, s_nrec, s_n2a, s_n2b;
   __shared__ int s_hist[NB];
   __shared__ uint32_t s_ml[HYD_MAX_SCHEMES], s_pp[HYD_MAX_SCHEMES], s_ul[HYD_MAX_SCHEMES];
+  __shared__ uint32_t s_cap[HYD_MAX_SCHEMES];  // floor(alpha_k MaxLen_k), see min_keys
   const int kp = a.k_pad;
   const int t = blockIdx.y, c0 = blockIdx.x * tc;
   const int B = geo_bt(a.off, a.batch, t);  // this iteration's sequences
@@ -541,10 +585,37 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
   __syncthreads();
   const uint32_t* slen = STAGED ? sm : a.sorted_len + tbase;
   const uint32_t* cst = STAGED ? sm + B : a.cost + tbase * kp;
+  // alpha_k = min tau_ik / l_i over the iteration's sequences with l_i <= MaxLen_k (warp per scheme)
+  for (int k = tid >> 5; k < a.n_schemes; k += kLaneThreads / 32) {
+    const uint32_t ml = s_ml[k];
+    uint32_t tn = 1u, td = 0u;  // running minimum tn / td (td = 0: none yet, +infinity)
+    for (int i = lane; i < B; i += 32) {
+      const uint32_t l = slen[i];
+      if (l > ml) continue;
+      const uint32_t tau = cst[(size_t)i * kp + k];
+      if (td == 0u || (uint64_t)tau * td < (uint64_t)tn * l) {
+        tn = tau;
+        td = l;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint32_t on = __shfl_xor_sync(HYD_FULL, tn, o), od = __shfl_xor_sync(HYD_FULL, td, o);
+      if (od != 0u && (td == 0u || (uint64_t)on * td < (uint64_t)tn * od)) {
+        tn = on;
+        td = od;
+      }
+    }
+    if (lane == 0) {
+      const uint64_t cap = td ? (uint64_t)tn * ml / td : 0xFFFFFFFFull;
+      s_cap[k] = cap > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)cap;
+    }
+  }
+  __syncthreads();
 
   LaneUnit<VM> u;
   uint32_t ev = 0;
-  auto load_unit = [&](int r, uint32_t V, uint32_t thr, bool write) {
+  auto load_unit = [&](int r, uint32_t V, uint32_t thr, bool write, bool F) {
     const int e = (int)R.eid[r];
     const int c = c0 + e / mnp;
     u.e = r;
@@ -553,13 +624,15 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
     u.mw = a.members + (fbase + e - e % mnp) * nwords + e % mnp;  // word-major rows of (t, c)
     u.mrow = a.mb + (size_t)c * a.n_total + tbase;
     u.write = write;
+    u.F = F;
     unit_start<VM>(u, V, thr);
   };
   // Lanes pull consecutive units of a list sorted by (class, U) -- so the units a warp holds at
   // any time have the same class and similar U -- and refill as soon as their unit ends.
   // Between epochs of kLaneEpoch sequences, all lanes whose unit ended record it and pull the
   // next one together (converged); the VMAX code path is chosen per epoch for the whole warp.
-  auto run_units = [&](int n_units, auto&& pull, auto&& finish) {
+  auto run_units = [&](auto allow_free, int n_units, auto&& pull, auto&& finish) {
+    constexpr bool AF = decltype(allow_free)::value;
     if (tid == 0) s_next = 0;
     __syncthreads();
     bool have = false, done = false;
@@ -571,12 +644,18 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
       }
       if (__all_sync(HYD_FULL, !have)) break;
       const bool narrow = __all_sync(HYD_FULL, !have || u.V <= 8u);
+      const bool fr = AF && __all_sync(HYD_FULL, !have || u.F);
       if (have) {
         int st = 0;
 #pragma unroll 1
         for (int e = 0; e < kLaneEpoch && st == 0; ++e) {
-          if (VM == 16 && narrow) st = unit_step<8, VM, STAGED>(u, nwords_t, mnp, B, slen, cst, kp, ev);
-          else st = unit_step<VM, VM, STAGED>(u, nwords_t, mnp, B, slen, cst, kp, ev);
+          if (AF && fr) {
+            if (VM == 16 && narrow) st = unit_step<8, VM, STAGED, AF>(u, nwords_t, mnp, B, slen, cst, kp, ev);
+            else st = unit_step<VM, VM, STAGED, AF>(u, nwords_t, mnp, B, slen, cst, kp, ev);
+          } else {
+            if (VM == 16 && narrow) st = unit_step<8, VM, STAGED, false>(u, nwords_t, mnp, B, slen, cst, kp, ev);
+            else st = unit_step<VM, VM, STAGED, false>(u, nwords_t, mnp, B, slen, cst, kp, ev);
+          }
         }
         if (st) have = finish(st);  // finish may load a follow-up unit into this lane
       }
@@ -610,10 +689,10 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
   //      (capacity), the same lane goes on with V_a + 1, which then takes V_a's place as the
   //      reference run of the exact tests below
   run_units(
-      nrec,
+      std::false_type{}, nrec,
       [&](int q) {
         const int r = R.perm[q];
-        load_unit(r, R.va[r], 0xFFFFFFFFu, true);
+        load_unit(r, R.va[r], 0xFFFFFFFFu, true, false);
         return true;
       },
       [&](int st) -> bool {
@@ -626,7 +705,7 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
         const uint32_t V = u.V + 1u;
         if (V > (uint32_t)R.vhi[r] || V > (uint32_t)VM || V != (uint32_t)R.va[r] + 1u) return false;
         R.va[r] = (uint16_t)V;
-        load_unit(r, V, 0xFFFFFFFFu, true);
+        load_unit(r, V, 0xFFFFFFFFu, true, false);
         return true;  // keep the lane on this task
       });
   phase_clock(1);
@@ -659,7 +738,17 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
       }
     }
   };
-  // pass A (thread per task): candidate counts (class <= 8 / > 8) and bucket of every task
+  // thr of a phase-2 unit against best (the run's abort threshold, search_thr_approx clamped)
+  auto unit_thr = [&](int r, uint32_t V, uint64_t best) -> uint32_t {
+    Search s;
+    s.P = s_pp[R.k[r]];
+    s.have = true;
+    s.best = best;
+    const uint64_t th = search_thr_approx(s, V);
+    return th > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)th;
+  };
+  // pass A (thread per task): candidate counts (class <= 8 / > 8), bucket and mode of every task
+  // (mode: every candidate's run is capacity-free against the reference, bit 5 of cbucket)
   if (tid == 0) s_n2a = 0;
   __syncthreads();
   for (int r = tid; r < nrec; r += kLaneThreads) {
@@ -675,10 +764,13 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
     walk(r, s);
     int n_lo = 0, n_hi = 0;  // candidates with V <= 8 / V > 8 (VM = 32: all counted high)
     uint32_t vmax = 0, V;
+    bool all_free = true;
+    const uint32_t cap = s_cap[R.k[r]];
     while ((V = search_next(s)) != 0) {
       vmax = max(vmax, V);
       if (VM == 16 && V <= 8) ++n_lo;
       else ++n_hi;
+      all_free = all_free && unit_thr(r, V, R.key[r] >> 16) <= cap;
     }
     if (vmax > (uint32_t)VM) {
       atomicAdd(a.why + (VM == 16 ? 3 : 6), 1ull);
@@ -688,16 +780,32 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
     }
     if (n_lo + n_hi == 0) continue;
     R.ncand[r] = (uint16_t)(n_lo | (n_hi << 8));
-    R.cbucket[r] = (uint8_t)min(31, (int)(R.u[r] >> 3));
+    R.cbucket[r] = (uint8_t)(min(31, (int)(R.u[r] >> 3)) | (all_free ? 32 : 0));
     atomicAdd(&s_n2a, n_lo + n_hi);
   }
   __syncthreads();
   phase_clock(3);
   const int total2 = s_n2a;
   if (VM == 16 && tid == 0) atomicAdd(a.why + 14, (unsigned long long)total2);
+  // bucket of a unit: (class, mode, U) -- capacity-free units apart from masked ones, so warps
+  // pulling consecutive units mostly run one path
+  auto bucket_of = [&](bool hi, int cb) { return (hi ? 64 : 0) + ((cb & 32) ? 0 : 32) + (cb & 31); };
+  auto scan_hist = [&]() {  // exclusive scan, descending buckets; s_n2b = total
+    __syncthreads();
+    if (tid == 0) {
+      int run = 0;
+      for (int b = NB - 1; b >= 0; --b) {
+        const int h = s_hist[b];
+        s_hist[b] = run;
+        run += h;
+      }
+      s_n2b = run;
+    }
+    __syncthreads();
+  };
   // ---- phase 2 in rounds of whole tasks whose units fit list2 (one round unless the tile
   //      has more than ncap surviving V): the surviving V, each an independent run against
-  //      the reference; argmin by atomicMin on (obj << 16 | V)
+  //      the best so far; argmin by atomicMin on (obj << 16 | V)
   for (int r0 = 0; r0 < nrec;) {
     __syncthreads();
     if (tid < 32) {  // round end r1: longest task range from r0 whose units fit ncap
@@ -730,29 +838,19 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
     for (int r = r0 + tid; r < r1; r += kLaneThreads) {
       const int packed = R.ncand[r];
       if (packed == 0 || R.state[r] == 1) continue;
-      const int ub = R.cbucket[r];
-      if (packed & 0xFF) atomicAdd(&s_hist[ub], packed & 0xFF);
-      if (packed >> 8) atomicAdd(&s_hist[32 + ub], packed >> 8);
+      const int cb = R.cbucket[r];
+      if (packed & 0xFF) atomicAdd(&s_hist[bucket_of(false, cb)], packed & 0xFF);
+      if (packed >> 8) atomicAdd(&s_hist[bucket_of(true, cb)], packed >> 8);
     }
-    __syncthreads();
-    if (tid == 0) {  // exclusive scan, descending buckets
-      int run = 0;
-      for (int b = NB - 1; b >= 0; --b) {
-        const int h = s_hist[b];
-        s_hist[b] = run;
-        run += h;
-      }
-      s_n2b = run;  // <= ncap by construction
-    }
-    __syncthreads();
+    scan_hist();
     // pass B: bucket-sorted units of the round (slot << 16 | V)
     for (int r = r0 + tid; r < r1; r += kLaneThreads) {
       const int packed = R.ncand[r];
       if (packed == 0 || R.state[r] == 1) continue;
       const int n_lo = packed & 0xFF, n_hi = packed >> 8;
-      const int ub = R.cbucket[r];
-      const int p_lo = n_lo ? atomicAdd(&s_hist[ub], n_lo) : 0;
-      const int p_hi = n_hi ? atomicAdd(&s_hist[32 + ub], n_hi) : 0;
+      const int cb = R.cbucket[r];
+      const int p_lo = n_lo ? atomicAdd(&s_hist[bucket_of(false, cb)], n_lo) : 0;
+      const int p_hi = n_hi ? atomicAdd(&s_hist[bucket_of(true, cb)], n_hi) : 0;
       Search s;
       walk(r, s);
       uint32_t V;
@@ -766,41 +864,61 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
         }
       }
     }
-    // pending phase-2 units per task of the round (its walks are done: sum_t is reused as the
-    // counter; later rounds walk only later tasks)
-    for (int r = r0 + tid; r < r1; r += kLaneThreads) {
-      const int packed = R.ncand[r];
-      R.sum_t[r] = (R.state[r] == 1) ? 0u : (uint32_t)((packed & 0xFF) + (packed >> 8));
-    }
     __syncthreads();
     run_units(
-        s_n2b,
+        std::true_type{}, s_n2b,
         [&](int q) {
           const uint32_t w = R.list2[q];
           const int r = (int)(w >> 16);
           const uint32_t V = w & 0xFFFFu;
-          Search s;
-          s.P = s_pp[R.k[r]];
-          s.have = true;
-          s.best = R.key[r] >> 16;
-          const uint64_t th = search_thr_approx(s, V);
-          load_unit(r, V, th > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)th, false);
+          const uint32_t thr = unit_thr(r, V, R.key[r] >> 16);
+          load_unit(r, V, thr, false, thr <= s_cap[R.k[r]]);
           return true;
         },
         [&](int st) -> bool {
-          const int r = u.e;
-          if (st == 1 && !u.write) atomicMin(&R.key[r], obj_key(u));
-          if (u.write) return false;  // this was the task's final mb run
-          // the lane finishing a task's last candidate writes the winner's mb if it is not the
-          // reference run (whose mb phase 1 already wrote)
-          if (atomicSub(&R.sum_t[r], 1u) != 1u) return false;
-          const uint32_t V = (uint32_t)(R.key[r] & 0xFFFFu);
-          if (V == (uint32_t)R.va[r]) return false;
-          load_unit(r, V, 0xFFFFFFFFu, true);
-          return true;
+          if (st == 1) atomicMin(&R.key[u.e], obj_key(u));
+          return false;
         });
     r0 = r1;
   }
+  // ---- phase 3: the mb row of every task whose winner is not its reference run (whose mb phase
+  //      1 wrote): one more run of the winning V, capacity-free when its known maximum bin time
+  //      is within cap_k
+  for (int b = tid; b < NB; b += kLaneThreads) s_hist[b] = 0;
+  __syncthreads();
+  auto rewrite_of = [&](int r, uint32_t& V, bool& F) -> bool {
+    if (R.state[r] == 1 || R.ncand[r] == 0) return false;
+    const unsigned long long key = R.key[r];
+    V = (uint32_t)(key & 0xFFFFu);
+    if (V == (uint32_t)R.va[r]) return false;
+    const uint64_t mx = (key >> 16) / (uint64_t)(s_pp[R.k[r]] - 1u + V);
+    F = mx <= (uint64_t)s_cap[R.k[r]];
+    return true;
+  };
+  for (int r = tid; r < nrec; r += kLaneThreads) {
+    uint32_t V;
+    bool F;
+    if (rewrite_of(r, V, F))
+      atomicAdd(&s_hist[bucket_of(VM == 32 || V > 8, min(31, (int)(R.u[r] >> 3)) | (F ? 32 : 0))], 1);
+  }
+  scan_hist();
+  for (int r = tid; r < nrec; r += kLaneThreads) {
+    uint32_t V;
+    bool F;
+    if (rewrite_of(r, V, F)) {
+      const int pos = atomicAdd(&s_hist[bucket_of(VM == 32 || V > 8, min(31, (int)(R.u[r] >> 3)) | (F ? 32 : 0))], 1);
+      R.list2[pos] = ((uint32_t)r << 16) | V | (F ? 0x8000u : 0u);
+    }
+  }
+  __syncthreads();
+  run_units(
+      std::true_type{}, s_n2b,
+      [&](int q) {
+        const uint32_t w = R.list2[q];
+        load_unit((int)(w >> 16), w & 0x7FFFu, 0xFFFFFFFFu, true, (w & 0x8000u) != 0u);
+        return true;
+      },
+      [&](int) -> bool { return false; });
 
   phase_clock(4);
   phase_clock(5);
