@@ -246,14 +246,14 @@ __device__ __forceinline__ uint32_t min_keys(const uint32_t (&keys)[VM]) {
 }
 
 template <int N, int VM>
-__device__ __forceinline__ void add_key(uint32_t (&keys)[VM], uint32_t mk, uint32_t tau_sh) {
+__device__ __forceinline__ void add_key(uint32_t (&keys)[VM], uint32_t mk, uint32_t nk) {
 #pragma unroll
   for (int b = 0; b < N; ++b)
     asm("{\n\t.reg .pred p;\n\t"
         "setp.eq.u32 p, %0, %1;\n\t"
-        "@p add.u32 %0, %0, %2;\n\t}"
+        "@p mov.u32 %0, %2;\n\t}"
         : "+r"(keys[b])
-        : "r"(mk), "r"(tau_sh));
+        : "r"(mk), "r"(nk));
 }
 
 // per-CTA task records (compacted slots), built in parallel before the lane phases
@@ -297,6 +297,7 @@ struct LaneUnit {
   uint16_t* mrow;
   uint32_t qw, cur, wbase, nxtw;
   uint32_t V, thr, mx, k, M;
+  uint32_t tb;  // STAGED: shared-window address of the cost column k (row 0)
   int e;
   bool write;
   bool F;  // capacity-free: no placement of this run can exceed MaxLen before it completes or aborts
@@ -323,11 +324,16 @@ __device__ __forceinline__ void unit_start(LaneUnit<VM>& u, uint32_t V, uint32_t
 // takes the next one (an all-zero word costs it one idle step), and the step's placement is
 // predicated on having a member, so the warp never splits inside the bin arithmetic.
 // STAGED: lengths at sm[0, B), costs at sm[B + i * kp + k] (shared window, 32-bit addressing).
+__device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
 template <int N, int VM, bool STAGED, bool FREE>
-__device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, uint32_t mnp, int B,
+__device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, uint32_t mnp, uint32_t sbase,
                                          const uint32_t* __restrict__ slen,
                                          const uint32_t* __restrict__ cst, int kp, uint32_t& ev) {
-  extern __shared__ __align__(16) uint32_t sm[];
   constexpr int SH = LaneCfg<VM>::SH;
   if (u.cur == 0 && u.qw < nwords) {
     u.cur = u.nxtw;
@@ -338,8 +344,9 @@ __device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, uint3
   const bool valid = u.cur != 0u;
   const uint32_t i = valid ? u.wbase + (uint32_t)(__ffs(u.cur) - 1) : 0u;
   u.cur &= u.cur - 1u;
-  const uint32_t l = STAGED ? sm[i] : slen[i];
-  const uint32_t tau = STAGED ? sm[B + i * kp + u.k] : cst[(size_t)i * kp + u.k];
+  // STAGED: 32-bit shared-window addresses (sbase: lengths; u.tb + 4 kp i: the cost of row i)
+  const uint32_t tau = STAGED ? ld_shared_u32(u.tb + i * (uint32_t)(kp * 4)) : cst[(size_t)i * kp + u.k];
+  const uint32_t l = FREE ? 0u : (STAGED ? ld_shared_u32(sbase + i * 4u) : slen[i]);
   uint32_t m0;
   if constexpr (FREE) {  // capacity cannot bind: plain least-time bin, bin tokens not tracked
     m0 = min_keys<N, VM>(u.keys);
@@ -349,7 +356,7 @@ __device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, uint3
   const bool ok = valid && (m0 >> 31) == 0u;
   const uint32_t mk = ok ? m0 : 0xFFFFFFFFu;  // matches no bin key: placement is a no-op
   if constexpr (FREE) {
-    add_key<N, VM>(u.keys, mk, tau << SH);
+    add_key<N, VM>(u.keys, mk, mk + (tau << SH));  // the chosen key's new value, computed once
   } else {
     place_key<N, VM>(u.keys, u.rem, mk, tau << SH, l);
   }
@@ -585,6 +592,7 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
   __syncthreads();
   const uint32_t* slen = STAGED ? sm : a.sorted_len + tbase;
   const uint32_t* cst = STAGED ? sm + B : a.cost + tbase * kp;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
   // alpha_k = min tau_ik / l_i over the iteration's sequences with l_i <= MaxLen_k (warp per scheme)
   for (int k = tid >> 5; k < a.n_schemes; k += kLaneThreads / 32) {
     const uint32_t ml = s_ml[k];
@@ -625,6 +633,7 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
     u.mrow = a.mb + (size_t)c * a.n_total + tbase;
     u.write = write;
     u.F = F;
+    u.tb = sbase + ((uint32_t)B + u.k) * 4u;
     unit_start<VM>(u, V, thr);
   };
   // Lanes pull consecutive units of a list sorted by (class, U) -- so the units a warp holds at
@@ -650,11 +659,11 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
 #pragma unroll 1
         for (int e = 0; e < kLaneEpoch && st == 0; ++e) {
           if (AF && fr) {
-            if (VM == 16 && narrow) st = unit_step<8, VM, STAGED, AF>(u, nwords_t, mnp, B, slen, cst, kp, ev);
-            else st = unit_step<VM, VM, STAGED, AF>(u, nwords_t, mnp, B, slen, cst, kp, ev);
+            if (VM == 16 && narrow) st = unit_step<8, VM, STAGED, AF>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
+            else st = unit_step<VM, VM, STAGED, AF>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
           } else {
-            if (VM == 16 && narrow) st = unit_step<8, VM, STAGED, false>(u, nwords_t, mnp, B, slen, cst, kp, ev);
-            else st = unit_step<VM, VM, STAGED, false>(u, nwords_t, mnp, B, slen, cst, kp, ev);
+            if (VM == 16 && narrow) st = unit_step<8, VM, STAGED, false>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
+            else st = unit_step<VM, VM, STAGED, false>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
           }
         }
         if (st) have = finish(st);  // finish may load a follow-up unit into this lane
