@@ -368,7 +368,7 @@ __device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, uint3
 }
 
 // VM = 16: every (c,t,j) of the tile, classes 8 / 16; a task needing some V > 16 is flagged
-//          for the VM = 32 pass.  VM = 32: flagged tasks only (whole-iteration tiles, records
+//          for the VM = 32 pass.  VM = 32: flagged tasks only (tiles of up to 2048 candidates, records
 //          compacted).  Tasks the lanes cannot hold (V > VM in the last pass, sumT over the key
 //          limit, an infeasible V_a and V_a + 1) go to the warp queue, which runs the sequential
 //          exact search.
@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
       continue;
     }
     const int r = atomicAdd(&s_nrec, 1);
-    if (r >= ncap) {  // record space full (whole-iteration tiles of the VM = 32 pass)
+    if (r >= ncap) {  // record space full (wide tiles of the VM = 32 pass)
       atomicAdd(a.why + 7, 1ull);
       to_queue(c, j);
       continue;
@@ -1121,6 +1121,46 @@ __device__ __forceinline__ bool lpt_warp(const uint32_t* __restrict__ mw, uint32
   return true;
 }
 
+// LPT(V <= 32) with packed keys, lane b = bin b: key = time << 5 | b (sumT < 2^26), a sign-bit
+// capacity mask as in the lanes, so one redux.sync min per sequence picks the least-time fitting
+// bin with the smallest index (same rule and result as lpt_warp).
+__device__ __forceinline__ bool lpt_warp_packed(const uint32_t* __restrict__ mw, uint32_t nwords,
+                                                uint32_t mstride, uint32_t V, uint32_t M,
+                                                const uint32_t* __restrict__ sl,
+                                                const uint32_t* __restrict__ cs, int kp, uint32_t k,
+                                                uint64_t thr64, bool write, uint16_t* __restrict__ mrow,
+                                                uint64_t& maxbin, uint64_t& evals) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t thr = thr64 > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)thr64;
+  uint32_t key = lane < V ? lane : 0xFFFFFFFFu;  // unused lanes never fit
+  uint32_t rem = M;                               // MaxLen - tokens of bin `lane`
+  uint32_t mx = 0;
+  MemberStream ms;
+  ms_open(ms, mw, nwords, mstride);
+  uint32_t cidx = 0, cl = 0, ctau = 0, n;
+  while ((n = ms_next32(ms, sl, cs, kp, k, cidx, cl, ctau)) != 0) {
+    for (uint32_t q = 0; q < n; ++q) {
+      const uint32_t l = __shfl_sync(HYD_FULL, cl, q);
+      const uint32_t tau = __shfl_sync(HYD_FULL, ctau, q);
+      const uint32_t iq = __shfl_sync(HYD_FULL, cidx, q);
+      const uint32_t d = rem - l;
+      const uint32_t mk = key | (d & 0x80000000u);
+      const uint32_t m = __reduce_min_sync(HYD_FULL, mk);
+      evals += V;
+      if (m >> 31) return false;  // no bin fits
+      if (mk == m) {
+        key += tau << 5;
+        rem = d;
+        if (write) mrow[iq] = (uint16_t)lane;
+      }
+      mx = max(mx, (m >> 5) + tau);
+      if (mx > thr) return false;
+    }
+  }
+  maxbin = mx;
+  return true;
+}
+
 template <typename TT>
 __device__ __forceinline__ bool lpt_warp_dispatch(const uint32_t* mw, uint32_t nwords, uint32_t mstride, uint32_t V,
                                                   uint32_t M, const uint32_t* sl, const uint32_t* cs,
@@ -1172,12 +1212,15 @@ __global__ void __launch_bounds__(256) k_pack_big(PackArgs a) {
     if (s.U) {
       search_init(s);
       const bool narrow = s.sumT < 0xFFFFFFFFull;
+      const bool packed = s.sumT < (1ull << 26) && s.M < 0x80000000u;  // lpt_warp_packed's keys
       uint32_t V, wV = 0;
       bool first = true;
       while ((V = search_next(s)) != 0) {
         const uint64_t thr = first ? ~0ull : search_thr_approx(s, V);
         uint64_t mx = 0;
-        const bool ok = narrow ? lpt_warp_dispatch<uint32_t>(mw, nwords_t, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, scr_t, scr_k, ev)
+        const bool ok = (packed && V <= 32u)
+                            ? lpt_warp_packed(mw, nwords_t, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, ev)
+                        : narrow ? lpt_warp_dispatch<uint32_t>(mw, nwords_t, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, scr_t, scr_k, ev)
                                : lpt_warp_dispatch<uint64_t>(mw, nwords_t, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, scr_t, scr_k, ev);
         if (ok && first) wV = V;
         first = false;
@@ -1185,7 +1228,9 @@ __global__ void __launch_bounds__(256) k_pack_big(PackArgs a) {
       }
       if (s.have && s.vbest != wV) {  // the winner's mb was not written by the first run
         uint64_t mx = 0;
-        if (narrow) lpt_warp_dispatch<uint32_t>(mw, nwords_t, (uint32_t)a.mnp, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, scr_t, scr_k, ev);
+        if (packed && s.vbest <= 32u)
+          lpt_warp_packed(mw, nwords_t, (uint32_t)a.mnp, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, ev);
+        else if (narrow) lpt_warp_dispatch<uint32_t>(mw, nwords_t, (uint32_t)a.mnp, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, scr_t, scr_k, ev);
         else lpt_warp_dispatch<uint64_t>(mw, nwords_t, (uint32_t)a.mnp, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, scr_t, scr_k, ev);
       }
     } else {
@@ -1284,7 +1329,7 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
   // (v / ptime / makespan rows and infeasible mb rows are written whole by the VMAX-16 pass)
 
   // persistent lanes: pass 1 (VMAX 16) CTA = one iteration x tc candidates (~2048 tasks);
-  // pass 2 (VMAX 32, flagged tasks, compacted records) CTA = one whole iteration
+  // pass 2 (VMAX 32, flagged tasks, compacted records) CTA = one iteration x up to 2048 candidates
   // two CTAs per SM: ~110 KB of dynamic smem each for the staged iteration + task records
   const size_t stage = ((size_t)batch * 4 * (1 + (size_t)k_pad) + 15) & ~(size_t)15;
   auto plan = [&](size_t budget, bool& staged, int& ncap, size_t& smem) {
@@ -1304,7 +1349,8 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
           : launch_lanes<false, 16>(grid1, smem1, s, a, tc1, max_np, ncap1);
   note_launch();
   if (e != cudaSuccess) return record_cuda_error(e);
-  const int tc2 = max(1, min(n_cand, 65535 / max_np));
+  // (at most 2048 candidates per CTA: wide iterations flag more tasks than one CTA's records hold)
+  const int tc2 = max(1, min(n_cand, min(2048, 65535 / max_np)));
   dim3 grid2((n_cand + tc2 - 1) / tc2, n_iter);
   e = st2 ? launch_lanes<true, 32>(grid2, smem2, s, a, tc2, max_np, ncap2)
           : launch_lanes<false, 32>(grid2, smem2, s, a, tc2, max_np, ncap2);
