@@ -197,14 +197,17 @@ struct LaneCfg {
   static constexpr uint64_t SUMT_LIMIT = 1ull << (31 - SH);
 };
 
+constexpr int pow2_ceil(int n) { return n <= 1 ? 1 : 2 * pow2_ceil((n + 1) / 2); }
+
 template <int N, int VM>
 __device__ __forceinline__ uint32_t argmin_keys(const uint32_t (&keys)[VM],
                                                 const uint32_t (&rem)[VM], uint32_t l) {
-  uint32_t m[N];
+  constexpr int P = pow2_ceil(N);  // padded with never-chosen keys (folded away)
+  uint32_t m[P];
 #pragma unroll
-  for (int b = 0; b < N; ++b) m[b] = keys[b] | ((rem[b] - l) & 0x80000000u);
+  for (int b = 0; b < P; ++b) m[b] = b < N ? keys[b] | ((rem[b] - l) & 0x80000000u) : 0xFFFFFFFFu;
 #pragma unroll
-  for (int w = N / 2; w > 0; w >>= 1)
+  for (int w = P / 2; w > 0; w >>= 1)
 #pragma unroll
     for (int b = 0; b < w; ++b) m[b] = min(m[b], m[b + w]);
   return m[0];
@@ -235,11 +238,12 @@ __device__ __forceinline__ void place_key(uint32_t (&keys)[VM], uint32_t (&rem)[
 // which can only let a later masked step see a bin as fitting -- and every bin fits for them).
 template <int N, int VM>
 __device__ __forceinline__ uint32_t min_keys(const uint32_t (&keys)[VM]) {
-  uint32_t m[N];
+  constexpr int P = pow2_ceil(N);
+  uint32_t m[P];
 #pragma unroll
-  for (int b = 0; b < N; ++b) m[b] = keys[b];
+  for (int b = 0; b < P; ++b) m[b] = b < N ? keys[b] : 0xFFFFFFFFu;
 #pragma unroll
-  for (int w = N / 2; w > 0; w >>= 1)
+  for (int w = P / 2; w > 0; w >>= 1)
 #pragma unroll
     for (int b = 0; b < w; ++b) m[b] = min(m[b], m[b + w]);
   return m[0];
@@ -652,17 +656,19 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
         else have = pull(q);
       }
       if (__all_sync(HYD_FULL, !have)) break;
-      const bool narrow = __all_sync(HYD_FULL, !have || u.V <= 8u);
+      // bins the warp's widest unit needs: VMAX 16 paths 8 / 16, VMAX 32 paths 24 / 32
+      constexpr int N0 = VM == 16 ? 8 : 24;
+      const bool narrow = __all_sync(HYD_FULL, !have || u.V <= (uint32_t)N0);
       const bool fr = AF && __all_sync(HYD_FULL, !have || u.F);
       if (have) {
         int st = 0;
 #pragma unroll 1
         for (int e = 0; e < kLaneEpoch && st == 0; ++e) {
           if (AF && fr) {
-            if (VM == 16 && narrow) st = unit_step<8, VM, STAGED, AF>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
+            if (narrow) st = unit_step<N0, VM, STAGED, AF>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
             else st = unit_step<VM, VM, STAGED, AF>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
           } else {
-            if (VM == 16 && narrow) st = unit_step<8, VM, STAGED, false>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
+            if (narrow) st = unit_step<N0, VM, STAGED, false>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
             else st = unit_step<VM, VM, STAGED, false>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
           }
         }
