@@ -152,6 +152,25 @@ def test_parity_wide_u64_path(env):
     compare_all(g, o, "u64")
 
 
+def test_parity_capacity_free_boundary(env):
+    """Linear costs (tau = b l exactly) make alpha = b and cap = b MaxLen tight: a bin's time is
+    b times its tokens, so the capacity-free certificate (thr <= cap) holds up to equality while
+    MaxLen binds often (lengths up to MaxLen / 2, V near ceil(S / MaxLen))."""
+    rng = np.random.default_rng(21)
+    sch = np.concatenate([
+        w.make_scheme(pp=2, max_len=4096, util_len=0, a_q32=0, b_q32=3 << 32, c_q32=0),
+        w.make_scheme(pp=1, max_len=2048, util_len=0, a_q32=0, b_q32=5 << 32, c_q32=0),
+        w.make_scheme(pp=3, max_len=6000, util_len=0, a_q32=0, b_q32=2 << 32, c_q32=1 << 32),
+        w.make_scheme(pp=4, max_len=3000, util_len=0, a_q32=0, b_q32=7 << 32, c_q32=0),
+    ])
+    L = rng.integers(100, 2049, (5, 256)).astype(np.uint32)
+    rows = [w.canonical(sch, [int(x) for x in rng.integers(0, 4, int(rng.integers(1, 9)))]) for _ in range(60)]
+    W = w.custom_workload(L, sch, rows)
+    g = run_gpu(env, W)
+    o = env["oracle"].assign_batch(W, n_threads=0)
+    compare_all(g, o, "capfree")
+
+
 @pytest.mark.parametrize("cfg", [2, 3, 4, 5])
 def test_parity_full_size_sampled(env, cfg):
     """BASELINE full sizes in the bench launch configuration; oracle on sampled pairs."""
