@@ -136,7 +136,8 @@ int hyd_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, i
  * (max_j ptime; UINT64_MAX if infeasible).  ws: hyd_pack_workspace() bytes; after the
  * call completes, the u64 at ws byte offset 16 holds the number of (sequence, micro-batch)
  * evaluations the LPT runs performed (diagnostic work counter for the roofline) and bytes
- * [24, 88) eight u64 counters of pipelines handed between the kernel's internal passes. */
+ * [24, 152) sixteen u64 diagnostic counters (pipelines handed between the internal passes and
+ * why, per-phase SM cycles of the lane pass, its phase-2 units and tasks; assign.py names them). */
 size_t hyd_pack_workspace(int n_iter, int batch, int n_cand, int max_np);
 int hyd_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch, int k_pad,
              const hyd_scheme* schemes, int n_schemes, const uint8_t* cand, const uint8_t* cand_np,

@@ -69,7 +69,7 @@ struct PackArgs {
   unsigned long long* q_count;
   unsigned long long* q_head;
   unsigned long long* evals;  // (item, bin) evaluations performed (ws bytes [16, 24))
-  unsigned long long* why;    // hand-off reason counters (ws bytes [24, 88)), diagnostic
+  unsigned long long* why;    // diagnostic counters (ws bytes [24, 152)): hand-offs, phase cycles
   unsigned long long* queue;
   unsigned long long q_cap;
   uint32_t* flags;  // [It*C*mnp bits] tasks handed from the VMAX-16 to the VMAX-32 lane pass
