@@ -161,7 +161,10 @@ __device__ __forceinline__ uint32_t packed_step(uint32_t l, const uint32_t (&tau
                                                 uint32_t (&key)[DP], uint32_t (&mults)[DP],
                                                 const uint32_t (&ml)[DP], int np, uint32_t& pend,
                                                 uint32_t (&plane)[SH],
-                                                unsigned long long* s_sum) {
+                                                unsigned long long* s_sum, uint32_t& pbj, uint32_t& pl) {
+  // S_j one step late: the previous decision's column is loaded before this step's pick, so the
+  // load's latency hides under it (same thread, program order: a repeat of the column is safe)
+  const unsigned long long sold = s_sum[pbj * kDispatchThreads];
   if (EMPTY && l <= pend) {  // rare: pipelines become feasible as l drops to their MaxLen
     uint32_t np2 = 0u;
 #pragma unroll
@@ -176,7 +179,9 @@ __device__ __forceinline__ uint32_t packed_step(uint32_t l, const uint32_t (&tau
   const uint32_t bj = packed_pick<DP, EMPTY>(tau, key, mults, 1u << SH);
 #pragma unroll  // shift bit b of j* in from the top: after the chunk, bit q = decision q
   for (int b = 0; b < SH; ++b) plane[b] = __funnelshift_r(plane[b], bj >> b, 1);
-  s_sum[bj * kDispatchThreads] += l;  // S_j column of this thread
+  s_sum[pbj * kDispatchThreads] = sold + pl;  // S_j column of this thread
+  pbj = bj;
+  pl = l;
   return bj;
 }
 
@@ -208,6 +213,7 @@ __device__ __forceinline__ void packed_run(const uint32_t* __restrict__ sl,
     pj[j] = TRANS ? cst + (size_t)kk[j] * stride : cst + kk[j];
   }
   const bool full_sectors = (B & 31) == 0 && ((size_t)prow & 15) == 0;
+  uint32_t pbj = 0u, pl = 0u;  // the decision whose S_j update is pending
   for (int i0 = 0; i0 < B; i0 += 32) {
     const int n = min(32, B - i0);
     bool empty = false;
@@ -229,9 +235,9 @@ __device__ __forceinline__ void packed_run(const uint32_t* __restrict__ sl,
 #pragma unroll
           for (int j = 0; j < DP; ++j) tau[j] = pj[j][i + u];
           if (warp_empty)
-            packed_step<DP, SH, true>(lq[u], tau, key, mults, ml, np, pend, plane, s_sum);
+            packed_step<DP, SH, true>(lq[u], tau, key, mults, ml, np, pend, plane, s_sum, pbj, pl);
           else
-            packed_step<DP, SH, false>(lq[u], tau, key, mults, ml, np, pend, plane, s_sum);
+            packed_step<DP, SH, false>(lq[u], tau, key, mults, ml, np, pend, plane, s_sum, pbj, pl);
         }
       }
       for (int q = n4; q < n; ++q) {
@@ -240,9 +246,9 @@ __device__ __forceinline__ void packed_run(const uint32_t* __restrict__ sl,
 #pragma unroll
         for (int j = 0; j < DP; ++j) tau[j] = pj[j][i];
         if (warp_empty)
-          packed_step<DP, SH, true>(sl[i], tau, key, mults, ml, np, pend, plane, s_sum);
+          packed_step<DP, SH, true>(sl[i], tau, key, mults, ml, np, pend, plane, s_sum, pbj, pl);
         else
-          packed_step<DP, SH, false>(sl[i], tau, key, mults, ml, np, pend, plane, s_sum);
+          packed_step<DP, SH, false>(sl[i], tau, key, mults, ml, np, pend, plane, s_sum, pbj, pl);
       }
     } else {
       for (int q = 0; q < n; ++q) {
@@ -252,9 +258,9 @@ __device__ __forceinline__ void packed_run(const uint32_t* __restrict__ sl,
 #pragma unroll
         for (int j = 0; j < DP; ++j) tau[j] = __ldg(pj[j] + (size_t)i * stride);
         if (warp_empty)
-          packed_step<DP, SH, true>(l, tau, key, mults, ml, np, pend, plane, s_sum);
+          packed_step<DP, SH, true>(l, tau, key, mults, ml, np, pend, plane, s_sum, pbj, pl);
         else
-          packed_step<DP, SH, false>(l, tau, key, mults, ml, np, pend, plane, s_sum);
+          packed_step<DP, SH, false>(l, tau, key, mults, ml, np, pend, plane, s_sum, pbj, pl);
       }
     }
     if (n < 32) {
@@ -304,6 +310,7 @@ __device__ __forceinline__ void packed_run(const uint32_t* __restrict__ sl,
         if (j < np) mrow[j] = xw[j];
     }
   }
+  s_sum[pbj * kDispatchThreads] += pl;  // the last decision's S_j
   uint64_t mx = 0ull;
 #pragma unroll
   for (int j = 0; j < DP; ++j) {
