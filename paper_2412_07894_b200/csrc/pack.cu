@@ -680,25 +680,6 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
   auto obj_key = [&](const LaneUnit<VM>& w) {
     return (((uint64_t)w.mx * (uint64_t)(s_pp[w.k] - 1 + w.V)) << 16) | w.V;
   };
-  // order-preserving compaction of perm[0..nrec) into list2 by one warp (ballot prefix)
-  auto compact = [&](auto&& keep) -> int {
-    __syncthreads();
-    if (tid < 32) {
-      int n = 0;
-      for (int q0 = 0; q0 < nrec; q0 += 32) {
-        const int q = q0 + lane;
-        const int r = q < nrec ? (int)R.perm[q] : 0;
-        const bool k = q < nrec && keep(r);
-        const unsigned m = __ballot_sync(HYD_FULL, k);
-        if (k) R.list2[n + __popc(m & ((1u << lane) - 1u))] = (uint32_t)r;
-        n += __popc(m);
-      }
-      if (lane == 0) s_n2a = n;
-    }
-    __syncthreads();
-    return s_n2a;
-  };
-
   phase_clock(0);
   // ---- phase 1: the V_a run of every task (writes mb); where LPT(V_a) is infeasible
   //      (capacity), the same lane goes on with V_a + 1, which then takes V_a's place as the
@@ -939,20 +920,19 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
   phase_clock(5);
   if (VM == 16 && tid == 0) atomicAdd(a.why + 15, (unsigned long long)nrec);
   // ---- outputs
-  if (VM == 16) {
+  if constexpr (VM == 16) {
     write_rows(nrec);
-    if (ev) atomicAdd(a.evals, (unsigned long long)ev);
-    return;
-  }
-  for (int r = tid; r < nrec; r += kLaneThreads) {  // VMAX-32 pass: its tasks' slots only
-    if (R.state[r] == 1) continue;
-    const int e = (int)R.eid[r];
-    const int c = c0 + e / mnp, j = e % mnp;
-    const size_t row = (size_t)c * a.n_iter + t;
-    const unsigned long long key = R.key[r];
-    a.v[row * HYD_MAX_PIPES + j] = (uint16_t)(key & 0xFFFFu);
-    a.ptime[row * HYD_MAX_PIPES + j] = key >> 16;
-    atomicMax(reinterpret_cast<unsigned long long*>(a.makespan + (size_t)t * a.n_cand + c), key >> 16);
+  } else {
+    for (int r = tid; r < nrec; r += kLaneThreads) {  // VMAX-32 pass: its tasks' slots only
+      if (R.state[r] == 1) continue;
+      const int e = (int)R.eid[r];
+      const int c = c0 + e / mnp, j = e % mnp;
+      const size_t row = (size_t)c * a.n_iter + t;
+      const unsigned long long key = R.key[r];
+      a.v[row * HYD_MAX_PIPES + j] = (uint16_t)(key & 0xFFFFu);
+      a.ptime[row * HYD_MAX_PIPES + j] = key >> 16;
+      atomicMax(reinterpret_cast<unsigned long long*>(a.makespan + (size_t)t * a.n_cand + c), key >> 16);
+    }
   }
   if (ev) atomicAdd(a.evals, (unsigned long long)ev);
 }
