@@ -148,6 +148,52 @@ __global__ void __launch_bounds__(NT) k_sort_cost(const uint32_t* __restrict__ l
   if (st && (tid & 31) == 0) atomicOr(status, st);
 }
 
+// Batches of at most 32 sequences (configuration 1): a WARP per iteration.  Lane i holds l_i; its
+// sorted position is the number of (l_j > l_i) or (l_j == l_i, j < i) over the row (32 shuffles),
+// which is the same stable order; the lane then writes its length, index and cost row there.
+__global__ void __launch_bounds__(256) k_sort_cost_warp(const uint32_t* __restrict__ len, int batch,
+                                                        const uint32_t* __restrict__ off,
+                                                        const hyd_scheme* __restrict__ schemes,
+                                                        int n_schemes, int k_pad, int n_iter,
+                                                        uint32_t* __restrict__ sorted_len,
+                                                        uint32_t* __restrict__ perm,
+                                                        uint32_t* __restrict__ cost,
+                                                        uint32_t* __restrict__ status) {
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= n_iter) return;
+  const int B = geo_bt(off, batch, t);
+  const size_t base = geo_base(off, batch, t);
+  if (off && lane == 0) {  // ragged batches: 1 <= B_t <= batch
+    const int d = (int)(__ldg(off + t + 1) - __ldg(off + t));
+    if (d < 1 || d > batch) atomicOr(status, HYD_F_BAD_LENGTH);
+  }
+  const bool mine = lane < B;
+  const uint32_t l = mine ? __ldg(len + base + lane) : 0u;
+  uint32_t rank = 0;
+  for (int j = 0; j < 32; ++j) {
+    const uint32_t lj = __shfl_sync(HYD_FULL, l, j);
+    rank += (j < B && (lj > l || (lj == l && j < lane))) ? 1u : 0u;
+  }
+  uint32_t st = 0;
+  if (mine) {
+    sorted_len[base + rank] = l;
+    perm[base + rank] = (uint32_t)lane;
+    uint4* crow = reinterpret_cast<uint4*>(cost + (base + rank) * k_pad);
+    for (int q = 0; q < (k_pad >> 2); ++q) {
+      uint32_t out[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int k = 4 * q + r;
+        out[r] = k < n_schemes ? eval_cost(schemes[k].a_q32, schemes[k].b_q32, schemes[k].c_q32, l, st) : 0u;
+      }
+      crow[q] = make_uint4(out[0], out[1], out[2], out[3]);
+    }
+  }
+  st = __reduce_or_sync(HYD_FULL, st);
+  if (st && lane == 0) atomicOr(status, st);
+}
+
 size_t sort_cost_smem(int batch, int nt, int n_schemes) {
   return (((size_t)batch * 4 + 16 * (size_t)nt * 4 + (size_t)batch * 4 + 15) & ~(size_t)15) +
          (size_t)n_schemes * 24;
@@ -158,7 +204,10 @@ int launch_sort_cost(const uint32_t* len, int n_iter, int batch, const uint32_t*
                      uint32_t* perm, uint32_t* cost, uint32_t* status, cudaStream_t s) {
   if (n_iter == 0) return HYD_OK;
   cudaError_t e;
-  if (batch <= 2048) {
+  if (batch <= 32) {
+    k_sort_cost_warp<<<(n_iter + 7) / 8, 256, 0, s>>>(len, batch, off, schemes, n_schemes, k_pad, n_iter,
+                                                      sorted_len, perm, cost, status);
+  } else if (batch <= 2048) {
     const size_t sm = sort_cost_smem(batch, 256, n_schemes);
     e = cudaFuncSetAttribute(k_sort_cost<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return record_cuda_error(e);
