@@ -80,14 +80,18 @@ __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
   }
   const bool words = (B & 3) == 0 && ((size_t)prow & 3) == 0;
   uint32_t word = 0u;
+  uint32_t pbj = 0u, pl = 0u;  // S_j one step late (as in packed_step)
   for (int i = 0; i < B; ++i) {
+    const unsigned long long sold = s_sum[pbj * kDispatchThreads];
     const uint32_t l = sl[i];
     const uint32_t* crow = cs + (size_t)i * k_pad;
     const uint32_t bit = 1u << (i & 31);
     const uint32_t bj =
         l > ml_min ? dispatch_step<DP, TT, true>(l, crow, staged, ml, kk, base, mult, bits, bit)
                    : dispatch_step<DP, TT, false>(l, crow, staged, ml, kk, base, mult, bits, bit);
-    s_sum[bj * kDispatchThreads] += l;  // S_j column of this thread
+    s_sum[pbj * kDispatchThreads] = sold + pl;  // S_j column of this thread
+    pbj = bj;
+    pl = l;
     if ((i & 31) == 31 || i == B - 1) {  // flush one membership word per pipeline
       const uint32_t w0 = (uint32_t)(i & ~31);
 #pragma unroll
@@ -111,6 +115,7 @@ __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
       prow[i] = (uint8_t)bj;
     }
   }
+  s_sum[pbj * kDispatchThreads] += pl;  // the last decision's S_j
   uint64_t m = 0ull;
 #pragma unroll
   for (int j = 0; j < DP; ++j)
