@@ -759,15 +759,17 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
     Search s;
     walk(r, s);
     int n_lo = 0, n_hi = 0;  // candidates with V <= 8 / V > 8 (VM = 32: all counted high)
-    uint32_t vmax = 0, V;
+    uint32_t vmax = 0, V, vmask = 0;
     bool all_free = true;
     const uint32_t cap = s_cap[R.k[r]];
     while ((V = search_next(s)) != 0) {
       vmax = max(vmax, V);
       if (VM == 16 && V <= 8) ++n_lo;
       else ++n_hi;
+      if (V <= 32u) vmask |= 1u << (V - 1u);
       all_free = all_free && unit_thr(r, V, R.key[r] >> 16) <= cap;
     }
+    R.sum_t[r] = vmask;  // the candidates as a bit set over V (sum_t is not read after this walk)
     if (vmax > (uint32_t)VM) {
       atomicAdd(a.why + (VM == 16 ? 3 : 6), 1ull);
       hand_off_e((int)R.eid[r]);
@@ -847,11 +849,9 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
       const int cb = R.cbucket[r];
       const int p_lo = n_lo ? atomicAdd(&s_hist[bucket_of(false, cb)], n_lo) : 0;
       const int p_hi = n_hi ? atomicAdd(&s_hist[bucket_of(true, cb)], n_hi) : 0;
-      Search s;
-      walk(r, s);
-      uint32_t V;
       int i_lo = 0, i_hi = 0;
-      while ((V = search_next(s)) != 0) {
+      for (uint32_t m = R.sum_t[r]; m != 0u; m &= m - 1u) {  // pass A's candidates
+        const uint32_t V = (uint32_t)__ffs(m);
         const uint32_t w = ((uint32_t)r << 16) | V;
         if (VM == 16 && V <= 8) {
           if (i_lo < n_lo) R.list2[p_lo + i_lo++] = w;
