@@ -334,7 +334,7 @@ __device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
   return v;
 }
 
-template <int N, int VM, bool STAGED, bool FREE>
+template <int N, int VM, bool STAGED, bool FREE, bool WRITE>
 __device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, uint32_t mnp, uint32_t sbase,
                                          const uint32_t* __restrict__ slen,
                                          const uint32_t* __restrict__ cst, int kp, uint32_t& ev) {
@@ -365,7 +365,7 @@ __device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, uint3
     place_key<N, VM>(u.keys, u.rem, mk, tau << SH, l);
   }
   u.mx = ok ? max(u.mx, (mk >> SH) + tau) : u.mx;
-  if (u.write && ok) u.mrow[i] = (uint16_t)(mk & ((1u << SH) - 1u));
+  if (WRITE && ok) u.mrow[i] = (uint16_t)(mk & ((1u << SH) - 1u));  // the phase's runs all write or none do
   ev += valid ? u.V : 0u;
   if (!valid) return u.qw >= nwords ? 1 : 0;  // every member placed / empty word
   return (!ok || u.mx > u.thr) ? 2 : 0;
@@ -644,8 +644,9 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
   // any time have the same class and similar U -- and refill as soon as their unit ends.
   // Between epochs of kLaneEpoch sequences, all lanes whose unit ended record it and pull the
   // next one together (converged); the VMAX code path is chosen per epoch for the whole warp.
-  auto run_units = [&](auto allow_free, int n_units, auto&& pull, auto&& finish) {
+  auto run_units = [&](auto allow_free, auto write_mb, int n_units, auto&& pull, auto&& finish) {
     constexpr bool AF = decltype(allow_free)::value;
+    constexpr bool WR = decltype(write_mb)::value;
     if (tid == 0) s_next = 0;
     __syncthreads();
     bool have = false, done = false;
@@ -665,11 +666,11 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
 #pragma unroll 1
         for (int e = 0; e < kLaneEpoch && st == 0; ++e) {
           if (AF && fr) {
-            if (narrow) st = unit_step<N0, VM, STAGED, AF>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
-            else st = unit_step<VM, VM, STAGED, AF>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
+            if (narrow) st = unit_step<N0, VM, STAGED, AF, WR>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
+            else st = unit_step<VM, VM, STAGED, AF, WR>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
           } else {
-            if (narrow) st = unit_step<N0, VM, STAGED, false>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
-            else st = unit_step<VM, VM, STAGED, false>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
+            if (narrow) st = unit_step<N0, VM, STAGED, false, WR>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
+            else st = unit_step<VM, VM, STAGED, false, WR>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
           }
         }
         if (st) have = finish(st);  // finish may load a follow-up unit into this lane
@@ -685,7 +686,7 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
   //      (capacity), the same lane goes on with V_a + 1, which then takes V_a's place as the
   //      reference run of the exact tests below
   run_units(
-      std::false_type{}, nrec,
+      std::false_type{}, std::true_type{}, nrec,
       [&](int q) {
         const int r = R.perm[q];
         load_unit(r, R.va[r], 0xFFFFFFFFu, true, false);
@@ -862,7 +863,7 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
     }
     __syncthreads();
     run_units(
-        std::true_type{}, s_n2b,
+        std::true_type{}, std::false_type{}, s_n2b,
         [&](int q) {
           const uint32_t w = R.list2[q];
           const int r = (int)(w >> 16);
@@ -908,7 +909,7 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
   }
   __syncthreads();
   run_units(
-      std::true_type{}, s_n2b,
+      std::true_type{}, std::true_type{}, s_n2b,
       [&](int q) {
         const uint32_t w = R.list2[q];
         load_unit((int)(w >> 16), w & 0x7FFFu, 0xFFFFFFFFu, true, (w & 0x8000u) != 0u);
