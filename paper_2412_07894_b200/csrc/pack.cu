@@ -334,7 +334,9 @@ __device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
   return v;
 }
 
-template <int N, int VM, bool STAGED, bool FREE, bool WRITE>
+// PH: the lane phase the run belongs to -- 1: V_a runs (write mb, no threshold), 2: candidate runs
+// (threshold, no mb), 3: winner re-runs (write mb; neither the threshold nor the maximum is needed)
+template <int N, int VM, bool STAGED, bool FREE, int PH>
 __device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, uint32_t mnp, uint32_t sbase,
                                          const uint32_t* __restrict__ slen,
                                          const uint32_t* __restrict__ cst, int kp, uint32_t& ev) {
@@ -364,11 +366,11 @@ __device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, uint3
   } else {
     place_key<N, VM>(u.keys, u.rem, mk, tau << SH, l);
   }
-  u.mx = ok ? max(u.mx, (mk >> SH) + tau) : u.mx;
-  if (WRITE && ok) u.mrow[i] = (uint16_t)(mk & ((1u << SH) - 1u));  // the phase's runs all write or none do
+  if (PH != 3) u.mx = ok ? max(u.mx, (mk >> SH) + tau) : u.mx;
+  if (PH != 2 && ok) u.mrow[i] = (uint16_t)(mk & ((1u << SH) - 1u));
   ev += valid ? u.V : 0u;
   if (!valid) return u.qw >= nwords ? 1 : 0;  // every member placed / empty word
-  return (!ok || u.mx > u.thr) ? 2 : 0;
+  return (!ok || (PH == 2 && u.mx > u.thr)) ? 2 : 0;
 }
 
 // VM = 16: every (c,t,j) of the tile, classes 8 / 16; a task needing some V > 16 is flagged
@@ -644,9 +646,9 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
   // any time have the same class and similar U -- and refill as soon as their unit ends.
   // Between epochs of kLaneEpoch sequences, all lanes whose unit ended record it and pull the
   // next one together (converged); the VMAX code path is chosen per epoch for the whole warp.
-  auto run_units = [&](auto allow_free, auto write_mb, int n_units, auto&& pull, auto&& finish) {
+  auto run_units = [&](auto allow_free, auto phase, int n_units, auto&& pull, auto&& finish) {
     constexpr bool AF = decltype(allow_free)::value;
-    constexpr bool WR = decltype(write_mb)::value;
+    constexpr int WR = decltype(phase)::value;
     if (tid == 0) s_next = 0;
     __syncthreads();
     bool have = false, done = false;
@@ -686,7 +688,7 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
   //      (capacity), the same lane goes on with V_a + 1, which then takes V_a's place as the
   //      reference run of the exact tests below
   run_units(
-      std::false_type{}, std::true_type{}, nrec,
+      std::false_type{}, std::integral_constant<int, 1>{}, nrec,
       [&](int q) {
         const int r = R.perm[q];
         load_unit(r, R.va[r], 0xFFFFFFFFu, true, false);
@@ -863,7 +865,7 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
     }
     __syncthreads();
     run_units(
-        std::true_type{}, std::false_type{}, s_n2b,
+        std::true_type{}, std::integral_constant<int, 2>{}, s_n2b,
         [&](int q) {
           const uint32_t w = R.list2[q];
           const int r = (int)(w >> 16);
@@ -909,7 +911,7 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
   }
   __syncthreads();
   run_units(
-      std::true_type{}, std::true_type{}, s_n2b,
+      std::true_type{}, std::integral_constant<int, 3>{}, s_n2b,
       [&](int q) {
         const uint32_t w = R.list2[q];
         load_unit((int)(w >> 16), w & 0x7FFFu, 0xFFFFFFFFu, true, (w & 0x8000u) != 0u);
