@@ -50,6 +50,7 @@ struct PackArgs {
   const uint32_t* sorted_len;
   const uint32_t* cost;
   int n_iter, batch, k_pad;  // batch: the largest batch (row stride of members, scratch)
+  uint32_t kp4;              // 4 k_pad: the staged cost row stride in bytes
   const uint32_t* off;       // ragged CSR offsets [n_iter + 1] or nullptr (uniform)
   size_t n_total;            // rows of iteration-indexed arrays (n_iter * batch if uniform)
   const hyd_scheme* schemes;
@@ -339,7 +340,7 @@ __device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
 template <int N, int VM, bool STAGED, bool FREE, int PH>
 __device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, uint32_t mnp, uint32_t sbase,
                                          const uint32_t* __restrict__ slen,
-                                         const uint32_t* __restrict__ cst, int kp, uint32_t& ev) {
+                                         const uint32_t* __restrict__ cst, int kp, uint32_t kp4, uint32_t& ev) {
   constexpr int SH = LaneCfg<VM>::SH;
   if (u.cur == 0 && u.qw < nwords) {
     u.cur = u.nxtw;
@@ -351,7 +352,7 @@ __device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, uint3
   const uint32_t i = valid ? u.wbase + (uint32_t)(__ffs(u.cur) - 1) : 0u;
   u.cur &= u.cur - 1u;
   // STAGED: 32-bit shared-window addresses (sbase: lengths; u.tb + 4 kp i: the cost of row i)
-  const uint32_t tau = STAGED ? ld_shared_u32(u.tb + i * (uint32_t)(kp * 4)) : cst[(size_t)i * kp + u.k];
+  const uint32_t tau = STAGED ? ld_shared_u32(u.tb + i * kp4) : cst[(size_t)i * kp + u.k];
   const uint32_t l = FREE ? 0u : (STAGED ? ld_shared_u32(sbase + i * 4u) : slen[i]);
   uint32_t m0;
   if constexpr (FREE) {  // capacity cannot bind: plain least-time bin, bin tokens not tracked
@@ -668,11 +669,11 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
 #pragma unroll 1
         for (int e = 0; e < kLaneEpoch && st == 0; ++e) {
           if (AF && fr) {
-            if (narrow) st = unit_step<N0, VM, STAGED, AF, WR>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
-            else st = unit_step<VM, VM, STAGED, AF, WR>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
+            if (narrow) st = unit_step<N0, VM, STAGED, AF, WR>(u, nwords_t, mnp, sbase, slen, cst, kp, a.kp4, ev);
+            else st = unit_step<VM, VM, STAGED, AF, WR>(u, nwords_t, mnp, sbase, slen, cst, kp, a.kp4, ev);
           } else {
-            if (narrow) st = unit_step<N0, VM, STAGED, false, WR>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
-            else st = unit_step<VM, VM, STAGED, false, WR>(u, nwords_t, mnp, sbase, slen, cst, kp, ev);
+            if (narrow) st = unit_step<N0, VM, STAGED, false, WR>(u, nwords_t, mnp, sbase, slen, cst, kp, a.kp4, ev);
+            else st = unit_step<VM, VM, STAGED, false, WR>(u, nwords_t, mnp, sbase, slen, cst, kp, a.kp4, ev);
           }
         }
         if (st) have = finish(st);  // finish may load a follow-up unit into this lane
@@ -1281,6 +1282,7 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
   a.off = off;
   a.n_total = n_total;
   a.k_pad = k_pad;
+  a.kp4 = 4u * (uint32_t)k_pad;
   a.schemes = schemes;
   a.n_schemes = n_schemes;
   a.cand = cand;
