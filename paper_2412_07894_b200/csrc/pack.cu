@@ -665,16 +665,27 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
       const bool narrow = __all_sync(HYD_FULL, !have || u.V <= (uint32_t)N0);
       const bool fr = AF && __all_sync(HYD_FULL, !have || u.F);
       if (have) {
-        int st = 0;
+        // one epoch on the chosen path (the path is fixed for the epoch: one loop per path)
+        auto epoch = [&](auto n_c, auto f_c) -> int {
+          constexpr int NN = decltype(n_c)::value;
+          constexpr bool FF = decltype(f_c)::value;
+          int st = 0;
 #pragma unroll 1
-        for (int e = 0; e < kLaneEpoch && st == 0; ++e) {
-          if (AF && fr) {
-            if (narrow) st = unit_step<N0, VM, STAGED, AF, WR>(u, nwords_t, mnp, sbase, slen, cst, kp, a.kp4, ev);
-            else st = unit_step<VM, VM, STAGED, AF, WR>(u, nwords_t, mnp, sbase, slen, cst, kp, a.kp4, ev);
-          } else {
-            if (narrow) st = unit_step<N0, VM, STAGED, false, WR>(u, nwords_t, mnp, sbase, slen, cst, kp, a.kp4, ev);
-            else st = unit_step<VM, VM, STAGED, false, WR>(u, nwords_t, mnp, sbase, slen, cst, kp, a.kp4, ev);
-          }
+          for (int e = 0; e < kLaneEpoch && st == 0; ++e)
+            st = unit_step<NN, VM, STAGED, FF, WR>(u, nwords_t, mnp, sbase, slen, cst, kp, a.kp4, ev);
+          return st;
+        };
+        int st;
+        if constexpr (AF) {
+          if (fr)
+            st = narrow ? epoch(std::integral_constant<int, N0>{}, std::true_type{})
+                        : epoch(std::integral_constant<int, VM>{}, std::true_type{});
+          else
+            st = narrow ? epoch(std::integral_constant<int, N0>{}, std::false_type{})
+                        : epoch(std::integral_constant<int, VM>{}, std::false_type{});
+        } else {
+          st = narrow ? epoch(std::integral_constant<int, N0>{}, std::false_type{})
+                      : epoch(std::integral_constant<int, VM>{}, std::false_type{});
         }
         if (st) have = finish(st);  // finish may load a follow-up unit into this lane
       }
