@@ -42,7 +42,7 @@ namespace hyd {
 constexpr int kLaneThreads = 256;
 constexpr size_t kLaneSmem16 = 74 * 1024;   // VMAX 16 pass: 3 CTAs per SM
 constexpr size_t kLaneSmem32 = 110 * 1024;  // VMAX 32 pass: 2 CTAs per SM
-constexpr int kLaneEpoch = 16;     // sequences per lane between bookkeeping phases
+constexpr int kLaneEpoch = 24;     // sequences per lane between bookkeeping phases
 constexpr int kBigRMax = 8;       // k_pack_big: register bins per lane (V <= 256)
 constexpr int kBigWarps = 3584;   // persistent warps of k_pack_big (scratch slots): 148 SMs x 24
 
