@@ -71,6 +71,53 @@ def peaks():
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def newest_profile(name):
+    """Newest committed profiles/rNN/<name> (rounds sort lexically), else None."""
+    import glob
+
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", name)))
+    return paths[-1] if paths else None
+
+
+def alu_peak(pk, how):
+    """Integer-instruction issue ceiling in G thread-instructions/s: the measured LPT-mix
+    microbenchmark (tools/int_peak.py -> profiles/rNN/int_peak.json), else the nominal
+    148 SM x 128 lanes x clock, saying which."""
+    p = newest_profile("int_peak.json")
+    if p:
+        try:
+            d = json.load(open(p))
+            return float(d["peak_gops"]), f"measured: {os.path.relpath(p, ROOT)} ({d.get('peak_kind', 'mix')})"
+        except Exception:
+            pass
+    sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
+    return 148 * 128 * sm_mhz * 1e6 / 1e9, f"nominal 148 SM x 128 INT32 lanes x {sm_mhz:.0f} MHz ({how} clock)"
+
+
+def alg_evals_per_ci(cfg):
+    """SURVEY §8(d) algorithmic pack work per c-i for this config (tools/alg_evals.py, oracle only)."""
+    p = newest_profile("alg_evals.json")
+    if not p:
+        return None, None
+    try:
+        d = json.load(open(p))["configs"][str(cfg)]
+        return float(d["evals_per_ci"]), os.path.relpath(p, ROOT)
+    except Exception:
+        return None, None
+
+
+def cpu_info():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
 
@@ -133,10 +180,12 @@ def sub_workload(W, its, cs):
                        W.k_pad, offsets=off)
 
 
-def run_oracle(W, **kw):
+def run_oracle(W, n_threads=0, **kw):
     import oracle
 
-    return oracle.assign_batch_ragged(W) if W.ragged else oracle.assign_batch(W, n_threads=0, **kw)
+    if W.ragged:
+        return oracle.assign_batch_ragged(W, n_threads=n_threads)
+    return oracle.assign_batch(W, n_threads=n_threads, **kw)
 
 
 # ----------------------------------------------------------------------------- CPU oracle leg
@@ -164,6 +213,13 @@ def oracle_sample(W, target_s, rng_seed=0, max_cand=None, trials=0, seed=0):
     run_oracle(sub, **({"trials": trials, "seed": seed} if trials else {}))
     dt = time.perf_counter() - t0
     cores = os.cpu_count() or 1
+    # the same oracle on ONE thread, on a slice of the sample sized to about a quarter of target_s
+    per1 = dt * min(cores, nc) / (nc * n_it)  # ~ seconds per c-i on one thread
+    n1 = max(1, min(nc, int(0.25 * target_s / max(per1, 1e-9))))
+    sub1 = sub_workload(W, its[:1], cs[:n1])
+    t1 = time.perf_counter()
+    run_oracle(sub1, n_threads=1, **({"trials": trials, "seed": seed} if trials else {}))
+    dt1 = time.perf_counter() - t1
     return {
         "value": (nc * n_it) / dt,
         "unit": UNIT,
@@ -171,6 +227,9 @@ def oracle_sample(W, target_s, rng_seed=0, max_cand=None, trials=0, seed=0):
         "kind": "oracle",
         "sample": f"{nc} candidates x {n_it} iterations of cfg{W.cfg} ({nc * n_it} c-i, steps a1-a5"
                   + (f", Alg. 1 with {trials} trials" if trials else "") + f"), {dt:.1f} s on {min(cores, nc)} threads",
+        "value_1thread": n1 / dt1,
+        "sample_1thread": f"{n1} candidates x 1 iteration ({n1} c-i) on 1 thread, {dt1:.1f} s",
+        **cpu_info(),
         "seconds": dt,
     }
 
@@ -214,7 +273,8 @@ def run_reference(args):
         "data": "synthetic",
         "config": {"workload": W.name, "sample_per_step": f"{per_step} candidates x 2 iterations"},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": min(cores, per_step), "kind": "oracle",
-                         "sample": f"{per_step} random candidates x 2 random iterations of cfg{W.cfg} per step"},
+                         "sample": f"{per_step} random candidates x 2 random iterations of cfg{W.cfg} per step",
+                         **cpu_info()},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -386,8 +446,7 @@ def run_dp(args):
         cpu = {"value": ct / dt, "unit": "transitions/s", "cores": 1, "kind": "oracle",
                "sample": f"integer DP (scale 1) on the same lengths and length grid, {ct} transitions in {dt:.1f} s"}
     pk, how = peaks()
-    sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
-    alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e9
+    alu, alu_src = alu_peak(pk, how)
     probes = dp_probes(W.schemes, step, J, N, scale)
     ops = 24.0 * probes  # ~24 int ops per probe (two 64x64->128 products, compares)
     achieved = ops / (ms / 1000.0) / 1e9
@@ -400,9 +459,8 @@ def run_dp(args):
                    "length_step": step, "buckets": J, "gpus": N, "gpu_step": 1 / scale, "transitions": trans,
                    "probes_evaluated": probes,
                    "proposed_candidates": int(len(sel))},
-        "roofline": {"kernel": "k_dp_solve", "bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Gop/s",
-                     "frac": achieved / alu_peak, "traffic": None,
-                     "peak_source": f"148 SM x 128 INT32 lanes x {sm_mhz:.0f} MHz ({how} clock)"},
+        "roofline": {"kernel": "k_dp_solve", "bound": "alu", "achieved": achieved, "peak": alu, "unit": "Gop/s",
+                     "frac": achieved / alu, "traffic": None, "peak_source": alu_src},
         "gpu_launches": int(launches), "clocks": clocks,
     }
     if cpu:
@@ -550,12 +608,18 @@ def main():
     # ---- roofline of the dominant kernel (largest share of the step)
     pk, how = peaks()
     dom = int(np.argmax(per_kernel[:4]))
-    roof = roofline(names[dom], per_kernel[dom], W, A, pk, how, local_ci=C_local * It_local)
+    roof = roofline(names[dom], per_kernel[dom], W, A, pk, how, local_ci=C_local * It_local, world=world)
 
     # ---- end-to-end through the public host-buffer API (hyd_assign_host)
-    e2e = None
+    e2e, H = None, None
     if not args.no_e2e and not args.profile and not args.trials:  # hyd_assign_host runs HYD-H1 only
-        e2e = run_e2e(args, W, sh, cand, cand_np, lens, world, dev)
+        e2e, H = run_e2e(args, W, sh, cand, cand_np, lens, world, dev)
+
+    # ---- a6 on hardware (N > 1, outside the timed region): reduced keys and every rank's winner
+    #      rows against a one-rank run over all candidates
+    a6 = None
+    if world > 1 and not args.profile and not args.trials:
+        a6 = verify_multi(W, sh, A, H, world, rank, dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
@@ -598,13 +662,60 @@ def main():
         }
         if e2e is not None:
             line["e2e"] = e2e
+        if a6 is not None:
+            line["a6_check"] = a6
         if cpu is not None:
             line["cpu_baseline"] = {k: v for k, v in cpu.items() if k != "seconds"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    if a6 is not None and not (a6["keys_equal_one_rank"] and a6["winner_rows_equal_one_rank"]):
+        print("ERROR: multi-GPU result differs from the one-rank run", file=sys.stderr)
+        return 3
     return 0
+
+
+def verify_multi(W, sh, A, H, world, rank, dev):
+    """Rank 0 runs the whole workload on one GPU; every rank compares its reduced keys (device
+    path) and its hyd_assign_host outputs (keys + winner rows of every iteration it holds)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2412_07894_b200 import assign
+
+    offs = W.offsets if W.ragged else None
+    ref = None
+    if rank == 0:
+        F = assign.Assigner(W.schemes, W.cand, W.cand_np, W.n_iter, W.batch, W.k_pad, device=dev, offsets=offs)
+        F.run(assign.lengths_to_device(W.lengths, dev))
+        ref = {"key": F.key.cpu().numpy()}
+        del F
+        torch.cuda.empty_cache()
+        if H is not None:
+            HF = assign.HostAssigner(W.schemes, W.cand, W.cand_np, W.n_iter, W.batch, W.k_pad, offsets=offs)
+            HF(torch.from_numpy(np.ascontiguousarray(W.lengths).view(np.int32)).pin_memory())
+            for k in ("win_pipe", "win_mb", "win_v", "win_ptime"):
+                ref[k] = getattr(HF, k).numpy().copy()
+            assert np.array_equal(HF.key.numpy(), ref["key"])
+            del HF
+            torch.cuda.empty_cache()
+    obj = [ref]
+    dist.broadcast_object_list(obj, src=0)
+    ref = obj[0]
+    lo, hi = sh.iter_lo, sh.iter_hi
+    keys_ok = bool(np.array_equal(A.key.cpu().numpy(), ref["key"][lo:hi]))
+    rows_ok = True
+    if H is not None:
+        rows_ok = bool(np.array_equal(H.key.numpy(), ref["key"][lo:hi]))
+        for k in ("win_pipe", "win_mb", "win_v", "win_ptime"):
+            rows_ok = rows_ok and bool(np.array_equal(getattr(H, k).numpy(), ref[k][lo:hi]))
+    flags = torch.tensor([int(keys_ok), int(rows_ok)], dtype=torch.int32, device=dev)
+    dist.all_reduce(flags, op=dist.ReduceOp.MIN)
+    return {"keys_equal_one_rank": bool(flags[0].item()), "winner_rows_equal_one_rank": bool(flags[1].item()),
+            "ranks": world, "checked": "outside the timed region: device-path keys after the last step and the "
+                                      "e2e call's keys + win_pipe/win_mb/win_v/win_ptime on every rank vs rank 0's "
+                                      "one-GPU run over all candidates"}
 
 
 def ncu_traffic(cfg, prefix):
@@ -624,32 +735,42 @@ def ncu_traffic(cfg, prefix):
         return None, None
 
 
-def roofline(name, ms, W, A, pk, how, local_ci):
-    """Algorithmic work per launch / CUDA-event duration (DESIGN.md §5)."""
+def roofline(name, ms, W, A, pk, how, local_ci, world=1):
+    """Algorithmic work per launch / CUDA-event duration (DESIGN.md §5, §6)."""
     B, D = (W.n_total / W.n_iter if W.ragged else W.batch), int(W.cand_np.max())
-    sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
-    alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e9  # int32 lane-ops/s in Gop/s (DESIGN.md §5)
+    alu, alu_src = alu_peak(pk, how)
     hbm = float(pk.get("hbm_gbs", 6650.0))
     if name == "pack":
         cnt = A.pack_counters()
-        ops = 6.0 * cnt["bin_evals"]  # ~6 int32 ops per (item, bin) evaluation
+        ops_exec = 6.0 * cnt["bin_evals"]  # ~6 int32 instructions per executed (item, bin) evaluation
+        per_ci, alg_src = alg_evals_per_ci(W.cfg)
+        ops = 6.0 * per_ci * local_ci if per_ci else ops_exec  # algorithmic: exact pruned search
         achieved = ops / (ms / 1000.0) / 1e9
         traffic, src = ncu_traffic(W.cfg, ("k_pack_",))
+        if world > 1:  # the committed ncu capture is of the N = 1 launch: not this shard's
+            traffic, src = None, "n/a at N > 1 (ncu captures are single-GPU)"
         return {"kernel": "pack (k_pack_lanes + k_pack_big)", "bound": "alu", "achieved": achieved,
-                "peak": alu_peak, "unit": "Gop/s", "frac": achieved / alu_peak, "traffic": traffic,
+                "peak": alu, "unit": "Gop/s", "frac": achieved / alu,
+                "frac_executed": ops_exec / (ms / 1000.0) / 1e9 / alu,
+                "traffic": traffic,
                 "traffic_unit": "bytes/launch (dram read+write, ncu --set full)", "traffic_source": src,
                 "algorithmic_bytes_per_launch": local_ci * (3 * B + 10 * D + 8),
-                "algorithmic_ops_per_launch": ops, "bin_evals_per_launch": cnt["bin_evals"],
+                "algorithmic_ops_per_launch": ops, "algorithmic_evals_per_ci": per_ci,
+                "algorithmic_source": alg_src or "none: executed evaluations used",
+                "executed_ops_per_launch": ops_exec, "bin_evals_per_launch": cnt["bin_evals"],
+                "executed_evals_per_ci": cnt["bin_evals"] / max(local_ci, 1),
                 "queued_tasks": cnt["queued_tasks"], "handoff": cnt.get("handoff"),
                 "hbm_algorithmic_GBps": local_ci * (3 * B + 10 * D + 8) / (ms / 1000.0) / 1e9,
-                "peak_source": f"148 SM x 128 INT32 lanes x {sm_mhz:.0f} MHz ({how} clock)"}
+                "hbm_frac_algorithmic": local_ci * (3 * B + 10 * D + 8) / (ms / 1000.0) / 1e9 / hbm,
+                "peak_source": alu_src, "ops_model": "6 int32 instructions per (sequence, micro-batch) evaluation"}
     if name == "dispatch":
         ev = A.dispatch_evals(A._lens_host) * max(A.trials, 1)
         ops = (8.0 if A.trials else 6.0) * ev  # DESIGN.md §6: int ops per (sequence, feasible pipeline)
         achieved = ops / (ms / 1000.0) / 1e9
-        return {"kernel": "dispatch" + (f" (Alg. 1, {A.trials} trials)" if A.trials else ""), "bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Gop/s",
-                "frac": achieved / alu_peak, "traffic": None, "algorithmic_ops_per_launch": ops,
-                "peak_source": f"148 SM x 128 INT32 lanes x {sm_mhz:.0f} MHz ({how} clock)"}
+        return {"kernel": "dispatch" + (f" (Alg. 1, {A.trials} trials)" if A.trials else ""), "bound": "alu",
+                "achieved": achieved, "peak": alu, "unit": "Gop/s",
+                "frac": achieved / alu, "traffic": None, "algorithmic_ops_per_launch": ops,
+                "peak_source": alu_src}
     byts = {"sort_cost": A.n_iter * B * (4 + 8 + 4 * A.k_pad), "select": A.n_iter * A.n_cand * 8 + 8 * A.n_iter}[name]
     achieved = byts / (ms / 1000.0) / 1e9
     return {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -688,7 +809,9 @@ def run_e2e(args, W, sh, cand, cand_np, lens, world, dev):
     ms = float(t.item())
     return {"value": W.n_cand * W.n_iter / (ms / 1000.0), "unit": UNIT,
             "h2d_bytes_per_step": int(lh.numel() * 4 + H.h2d_bytes_fixed), "d2h_bytes_per_step": int(H.d2h_bytes),
-            "ms_per_step": ms, "api": ("hyd_assign_host_ragged" if W.ragged else "hyd_assign_host") + " (pinned host buffers)"}
+            "ms_per_step": ms, "api": ("hyd_assign_host_ragged" if W.ragged else "hyd_assign_host") + " (pinned host buffers)"
+            + (", incl. the NCCL key allreduce-MIN and winner-row allreduce-SUM (every rank gets every plan)"
+               if sh.needs_reduce else "")}, H
 
 
 if __name__ == "__main__":

@@ -13,8 +13,10 @@
  * Conventions (all entry points):
  *   - Pointers are DEVICE pointers unless the name ends in _host.  Every call is
  *     stream-ordered and asynchronous on `stream` (a cudaStream_t passed as void*).
- *   - The caller owns every buffer.  The library allocates nothing and keeps no global
- *     state; scratch memory is a caller-provided device workspace.
+ *   - The caller owns every buffer.  The library allocates no device memory; scratch memory is
+ *     a caller-provided device workspace.  Its only global state is diagnostic: a launch
+ *     counter (hyd_kernel_launches, atomic) and the text of the last CUDA error seen by the
+ *     calling thread (hyd_last_cuda_error, thread-local); neither affects any result.
  *   - Host-side argument validation returns a negative HYD_E_* code synchronously and
  *     launches nothing.  Data-dependent faults set HYD_F_* bits in the device word
  *     `status` (OR-ed, never cleared by the library); the caller reads it after syncing.
@@ -23,7 +25,8 @@
  *     pipe row = 0xFF, mb row = 0xFFFF, v = ptime = 0, lb = makespan = UINT64_MAX.
  *   - Sequence-indexed outputs are indexed by SORTED position i (length descending,
  *     original index ascending); perm[t][i] is the original index of position i.
- *   - Limits: 1 <= batch <= HYD_MAX_BATCH; 1 <= n_schemes <= HYD_MAX_SCHEMES;
+ *   - Limits: 0 <= n_iter <= HYD_MAX_ITER (iterations map to a grid dimension);
+ *     1 <= batch <= HYD_MAX_BATCH; 1 <= n_schemes <= HYD_MAX_SCHEMES;
  *     k_pad % 4 == 0 and k_pad >= n_schemes; 1 <= cand_np[c] <= max_np <= 32;
  *     1 <= pp <= HYD_MAX_PP; max_len >= 1; n_cand + cand_offset <= 2^20 - 1 (global candidate
  *     index <= 2^20 - 2, so no key equals the INT64_MAX "none" sentinel).
@@ -38,6 +41,7 @@
 extern "C" {
 #endif
 
+#define HYD_MAX_ITER 65535
 #define HYD_MAX_BATCH 16384
 #define HYD_MAX_SCHEMES 64
 #define HYD_MAX_PIPES 32
@@ -74,7 +78,8 @@ enum {
   HYD_F_ZERO_COST = 2u,     /* a cost evaluated to 0 */
   HYD_F_BAD_LENGTH = 4u,    /* a length was 0 or > 2^24 */
   HYD_F_KEY_RANGE = 8u,     /* a feasible makespan >= 2^43 (excluded from selection) */
-  HYD_F_NOT_CANONICAL = 16u /* device-side candidate check failed (treated infeasible) */
+  HYD_F_NOT_CANONICAL = 16u, /* device-side candidate check failed (treated infeasible) */
+  HYD_F_BAD_PIPE = 32u       /* hyd_pipe_index: a pipe row is not an assignment (treated infeasible) */
 };
 
 /* ---- a1+a2: per-iteration stable sort + cost table ------------------------------------
@@ -122,8 +127,26 @@ int hyd_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, i
                  hyd_pipe_stats* stats, uint32_t* members, uint32_t* status, void* ws,
                  size_t ws_bytes, void* stream);
 
+/* ---- a3 -> a4 interface from an arbitrary stage-1 result ---------------------------------
+ * hyd_pipe_index: builds the (stats, members) that hyd_pack consumes from ANY stage-1
+ * assignment pipe [n_cand][n_iter][batch] u8 (the m_ij matrix of Eq. 3) -- e.g. a
+ * host-side Alg. 1 or the caller's own dispatcher -- and lb [n_cand][n_iter] u64 =
+ * Eq. 2's max_j (sum T(l, P_j) + T(longest on j, P_j)(PP_j - 1)) (lb may be NULL).  A row is an
+ * assignment iff every entry j satisfies j < cand_np[c] and MaxLen_j >= l_i (J_i), or,
+ * for a pair with l_0 > MaxLen_0 (infeasible), every entry is 0xFF.  Any other row sets
+ * HYD_F_BAD_PIPE and the pair is marked infeasible (hyd_pack then writes its infeasible rows).
+ * Layouts, sizes and the ragged form as hyd_dispatch / hyd_dispatch_ragged.  No workspace. */
+int hyd_pipe_index(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch, int k_pad,
+                   const hyd_scheme* schemes, int n_schemes, const uint8_t* cand, const uint8_t* cand_np,
+                   int n_cand, int max_np, const uint8_t* pipe, uint64_t* lb, hyd_pipe_stats* stats,
+                   uint32_t* members, uint32_t* status, void* stream);
+
 /* ---- a4: stage 2 packing (Eq. 1 + App. D) -------------------------------------------
- * Inputs include pipe, stats and members from hyd_dispatch (same n_cand/n_iter/max_np).
+ * The stage-1 result enters as `pipe` together with its index (stats, members): both come
+ * from hyd_dispatch / hyd_dispatch_alg1 (which emit them while deciding) or, for a pipe made
+ * anywhere else, from hyd_pipe_index (same n_cand/n_iter/max_np).  The kernels read the
+ * index; `pipe` is the assignment it describes (a stats/members pair that does not describe
+ * `pipe` is a caller error: the outputs are then those of the assignment the index describes).
  * For each (c,t,j): the pipeline's sequences Q (sorted order), U = |Q|, S = sum l:
  * V in [max(ceil(S/MaxLen),1), min(floor(S/UtilLen),U)] (clamped up to the lower end);
  * LPT(V): each sequence to the least-time micro-batch that stays within MaxLen (smallest
@@ -166,13 +189,24 @@ int hyd_gather_winners(const int64_t* key, const uint32_t* perm, const uint8_t* 
 
 /* ---- end-to-end call on HOST buffers -----------------------------------------------------
  * Copies len_host [n_iter][batch] (and the scheme/candidate tables) to the device, runs
- * a1-a5, calls reduce(key_dev, n_iter, user, stream) if non-null (the a6 allreduce-MIN over
- * the caller's process group; must be stream-ordered), gathers the winners and copies
- * key_host [n_iter], win_pipe_host [n_iter][batch], win_mb_host [n_iter][batch] (original
- * order; rows of iterations won by another rank are unspecified), win_v_host/win_ptime_host
- * [n_iter][32] and *status_host back, then synchronises `stream`.  Pinned host memory
- * gives asynchronous copies.  ws: hyd_assign_workspace() bytes of device memory. */
-typedef int (*hyd_reduce_fn)(int64_t* key_dev, int n_iter, void* user, void* stream);
+ * a1-a5, and returns the selected plan of every iteration (step 4, "select the optimal one",
+ * P:446-448): key_host [n_iter], win_pipe_host [n_iter][batch], win_mb_host
+ * [n_iter][batch] (ORIGINAL sequence order), win_v_host / win_ptime_host [n_iter][32] and
+ * *status_host; then synchronises `stream`.  Pinned host memory gives asynchronous copies.
+ * Rows of an all-infeasible iteration (key INT64_MAX) are zero.
+ * Multi-GPU (one process per GPU, this rank holding candidates [cand_offset, cand_offset +
+ * n_cand)): pass a collective callback `coll`.  The library calls it twice, in stream order:
+ *   1. coll(key_dev, n_iter, HYD_COLL_MIN_I64, user, stream): allreduce-MIN of the int64 keys
+ *      over the caller's process group (a6) -- afterwards key holds the global winners;
+ *   2. coll(rows_dev, n_words, HYD_COLL_SUM_I32, user, stream): allreduce-SUM of int32 words
+ *      over the winner-row block (win_pipe | win_mb | win_v | win_ptime, zero-filled, each rank
+ *      writing only the rows of iterations its candidates won), so every rank ends with every
+ *      iteration's plan (exactly one rank contributes a non-zero row per iteration).
+ * The callback must enqueue its work on `stream` (or order it after `stream`'s prior work and
+ * before its later work) and return 0; non-zero aborts with HYD_E_REDUCE.  coll = NULL: a
+ * single rank (no exchange).  ws: hyd_assign_workspace() bytes of device memory. */
+enum { HYD_COLL_MIN_I64 = 0, HYD_COLL_SUM_I32 = 1 };
+typedef int (*hyd_collective_fn)(void* buf_dev, size_t count, int op, void* user, void* stream);
 size_t hyd_assign_workspace(int n_iter, int batch, int n_schemes, int k_pad, int n_cand, int max_np);
 /* byte offset of the device key buffer [n_iter] i64 inside the assign workspace */
 size_t hyd_assign_key_offset(int n_iter, int batch, int n_schemes, int k_pad, int n_cand, int max_np);
@@ -180,7 +214,7 @@ int hyd_assign_host(const uint32_t* len_host, int n_iter, int batch, const hyd_s
                     int n_schemes, int k_pad, const uint8_t* cand_host, const uint8_t* cand_np_host,
                     int n_cand, int cand_offset, int64_t* key_host, uint8_t* win_pipe_host,
                     uint16_t* win_mb_host, uint16_t* win_v_host, uint64_t* win_ptime_host,
-                    uint32_t* status_host, hyd_reduce_fn reduce, void* reduce_user, void* ws,
+                    uint32_t* status_host, hyd_collective_fn coll, void* coll_user, void* ws,
                     size_t ws_bytes, void* stream);
 
 /* ---- NEXT-1: Alg. 1 as stage 1 (T random trials) ----------------------
@@ -239,6 +273,12 @@ int hyd_pack_ragged(const uint32_t* sorted_len, const uint32_t* cost, int n_iter
                     const hyd_pipe_stats* stats, const uint32_t* members, uint16_t* mb, uint16_t* v,
                     uint64_t* ptime, uint64_t* makespan, uint32_t* status, void* ws,
                     size_t ws_bytes, void* stream);
+int hyd_pipe_index_ragged(const uint32_t* sorted_len, const uint32_t* cost, int n_iter,
+                          const uint32_t* offsets, int n_total, int batch_max, int k_pad,
+                          const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
+                          const uint8_t* cand_np, int n_cand, int max_np, const uint8_t* pipe,
+                          uint64_t* lb, hyd_pipe_stats* stats, uint32_t* members, uint32_t* status,
+                          void* stream);
 int hyd_gather_winners_ragged(const int64_t* key, const uint32_t* perm, const uint8_t* pipe,
                               const uint16_t* mb, const uint16_t* v, const uint64_t* ptime,
                               int n_iter, const uint32_t* offsets, int n_total, int batch_max,
@@ -253,7 +293,7 @@ int hyd_assign_host_ragged(const uint32_t* len_host, int n_iter, const uint32_t*
                            const uint8_t* cand_host, const uint8_t* cand_np_host, int n_cand,
                            int cand_offset, int64_t* key_host, uint8_t* win_pipe_host,
                            uint16_t* win_mb_host, uint16_t* win_v_host, uint64_t* win_ptime_host,
-                           uint32_t* status_host, hyd_reduce_fn reduce, void* reduce_user, void* ws,
+                           uint32_t* status_host, hyd_collective_fn coll, void* coll_user, void* ws,
                            size_t ws_bytes, void* stream);
 
 /* ---- NEXT-3: strategy-proposal dynamic programme (§5) -------------------------
@@ -284,6 +324,15 @@ int hyd_dp_propose(const uint32_t* lengths, int n_seq, const hyd_scheme* schemes
                    int step, int J, int n_gpus, int scale, uint64_t* t_num, uint64_t* t_den,
                    int32_t* choice, uint16_t* counts, uint8_t* rows, uint8_t* valid, uint8_t* keep,
                    uint32_t* status, void* ws, size_t ws_bytes, void* stream);
+
+/* hyd_dp_candidates: the proposed subset of a hyd_dp_propose result (rows / keep) as the
+ * candidate tables hyd_dispatch takes, in first-occurrence (l, m) order: cand [M][32] u8 with
+ * the pipelines in canonical order (MaxLen non-increasing, scheme index ascending),
+ * each scheme repeated by its pipeline count, padded with 0xFF; cand_np [M] u8 (0 for a row
+ * with more than HYD_MAX_PIPES pipelines); *n_out (device i32) = M.  Capacity: (J + 1) *
+ * HYD_DP_MAX_ROUND rows.  schemes: the table passed to hyd_dp_propose. */
+int hyd_dp_candidates(const uint8_t* rows, const uint8_t* keep, int J, const hyd_scheme* schemes,
+                      int n_schemes, uint8_t* cand, uint8_t* cand_np, int32_t* n_out, void* stream);
 
 /* ---- NEXT-4: exact Eq. 3 optimum for small batches (gap study P:654) --------------
  * For each listed (pair_c[p], pair_t[p]): the minimum over every dispatch (each sequence on a

@@ -67,6 +67,10 @@ def lib():
             _u32p, _u32p, I, I, _voidp, _u8p, I, _u8p, C.POINTER(C.c_uint64), _u16p, _u16p, _u64p, U32P,
         ]
         L.hydref_assign_pair.restype = C.c_uint64
+        L.hydref_pack_pair.argtypes = [
+            _u32p, _u32p, I, I, _voidp, _u8p, I, _u8p, _u16p, _u16p, _u64p, U32P,
+        ]
+        L.hydref_pack_pair.restype = C.c_uint64
         L.hydref_select.argtypes = [_u64p, I, I, U32P]
         L.hydref_select.restype = C.c_int64
         L.hydref_assign_batch.argtypes = [
@@ -173,6 +177,54 @@ def pack_pipeline(ell, tau, scheme_row):
     v, pt, st = C.c_uint16(0), C.c_uint64(0), C.c_uint32(0)
     lib().hydref_pack_pipeline(ell, tau, ell.size, _sch_ptr(s), C.byref(v), C.byref(pt), mb, C.byref(st))
     return int(v.value), int(pt.value), mb[: ell.size], int(st.value)
+
+
+def is_assignment(sorted_len, schemes, cand_row, pipe):
+    """Whether ``pipe`` is a stage-1 result of Eq. 3 for this (c, t): every sequence
+    i on exactly one pipeline j of the candidate with MaxLen(P_j) >= l_i (J_i); for an
+    infeasible pair (l_0 > MaxLen_0) the only result is the all-0xFF row.  Returns
+    (valid, feasible)."""
+    ml = [int(schemes["max_len"][k]) for k in cand_row]
+    feasible = int(sorted_len[0]) <= ml[0]
+    if not feasible:
+        return all(int(p) == 0xFF for p in pipe), False
+    ok = all(int(p) < len(cand_row) and ml[int(p)] >= int(l) for p, l in zip(pipe, sorted_len))
+    return ok, True
+
+
+def eq2_lb(sorted_len, cost_tab, schemes, cand_row, pipe):
+    """Eq. 2 (P:636) of an assignment: max_j (sum_i m_ij T(l_i, P_j) + T(max l, P_j)(PP_j - 1));
+    under sorted order the first member of j is its longest (T non-decreasing in l)."""
+    best = 0
+    for j, k in enumerate(cand_row):
+        idx = [i for i in range(len(pipe)) if int(pipe[i]) == j]
+        if not idx:
+            continue
+        tau = [int(cost_tab[i][k]) for i in idx]
+        best = max(best, sum(tau) + max(tau) * (int(schemes["pp"][k]) - 1))
+    return best
+
+
+def pack_pair(sorted_len, cost_tab, schemes, cand_row, pipe):
+    """Steps 5-6 of HYD-H1 for one (c, t) whose stage-1 result ``pipe`` [B] is given (any
+    assignment, e.g. Alg. 1's or a caller's): (makespan, mb [B], v [32], ptime [32], lb, valid).
+    A row that is not an assignment (``is_assignment``) is handled as an infeasible pair:
+    makespan and lb UINT64_MAX, mb 0xFFFF, v = ptime = 0."""
+    B, k_pad = cost_tab.shape
+    ok, feas = is_assignment(sorted_len, schemes, cand_row, pipe)
+    v = np.zeros(32, np.uint16)
+    pt = np.zeros(32, np.uint64)
+    if not (ok and feas):
+        return 2**64 - 1, np.full(B, 0xFFFF, np.uint16), v, pt, 2**64 - 1, ok
+    row = np.full(32, 0xFF, np.uint8)
+    row[: len(cand_row)] = cand_row
+    mb = np.empty(B, np.uint16)
+    st = C.c_uint32(0)
+    ms = lib().hydref_pack_pair(
+        np.ascontiguousarray(sorted_len, np.uint32), np.ascontiguousarray(cost_tab, np.uint32).ravel(), B, k_pad,
+        _sch_ptr(schemes), row, len(cand_row), np.ascontiguousarray(pipe, np.uint8), mb, v, pt, C.byref(st),
+    )
+    return int(ms), mb, v, pt, eq2_lb(sorted_len, cost_tab, schemes, cand_row, pipe), True
 
 
 def select(makespan, cand_offset=0):

@@ -59,6 +59,16 @@ def reduce_keys(key, group=None):
     return key
 
 
+def share_rows(words, group=None):
+    """Winner follow-up: allreduce(SUM) of the zero-filled winner-row block
+    (int32 words); each iteration's rows are non-zero on the one rank that owns its winner,
+    so the sum is that rank's rows and every rank receives every iteration's plan."""
+    import torch.distributed as dist
+
+    dist.all_reduce(words, op=dist.ReduceOp.SUM, group=group)
+    return words
+
+
 def schemes_bytes(schemes) -> np.ndarray:
     s = np.ascontiguousarray(schemes)
     assert s.dtype.itemsize == 48
@@ -269,9 +279,11 @@ def lengths_to_device(lengths, device=None):
 class HostAssigner:
     """End-to-end path on HOST buffers through ``hyd_assign_host`` (the user-facing call).
 
-    Per call: H2D of the lengths (and tables), a1-a5 on the device, the optional
-    allreduce callback (a6), winner gather, D2H of keys + winners' plans in ORIGINAL
-    sequence order, one stream synchronisation.
+    Per call: H2D of the lengths (and tables), a1-a5 on the device, and with ``reduce``
+    (N > 1 ranks, candidates sharded) the two collectives of include/hyd.h -- allreduce-MIN of
+    the keys (a6), then allreduce-SUM of the zero-filled winner rows so every rank holds every
+    iteration's plan -- winner gather, D2H of keys + winners' plans in ORIGINAL sequence order,
+    one stream synchronisation.  The collectives run ordered on the stream passed to the call.
     """
 
     def __init__(self, schemes, cand, cand_np, n_iter, batch, k_pad, cand_offset=0, group=None, reduce=False,
@@ -309,21 +321,33 @@ class HostAssigner:
         self.group = group
         self._cb = None
         if reduce:
-            def _reduce(key_ptr, n, user, stream):
-                try:
-                    assert key_ptr == self.key_view.data_ptr() and n == self.n_iter
-                    reduce_keys(self.key_view, self.group)
-                    return 0
-                except Exception:  # reported as HYD_E_REDUCE
-                    return 1
-
-            self._cb = hyd.REDUCE_FN(_reduce)
+            self._cb = hyd.COLL_FN(self._collective)
         # host copies of the (fixed) tables, pinned
         self._sch = torch.from_numpy(schemes_bytes(self.schemes).copy()).pin_memory()
         self._cand = torch.from_numpy(self.cand.copy()).pin_memory()
         self._cnp = torch.from_numpy(self.cand_np.copy()).pin_memory()
         self._off = (torch.from_numpy(self.offsets.view(np.int32).copy()).pin_memory()
                      if self.offsets is not None else None)
+
+    def _collective(self, ptr, count, op, user, stream):
+        """hyd_collective_fn: the buffer is a slice of this assigner's workspace; the collective
+        runs ordered on the stream the library passes (include/hyd.h)."""
+        torch = self.torch
+        try:
+            width = 8 if op == hyd.COLL_MIN_I64 else 4
+            off, nbytes = int(ptr) - self.ws.data_ptr(), int(count) * width
+            if op not in (hyd.COLL_MIN_I64, hyd.COLL_SUM_I32) or off < 0 or off + nbytes > self.ws.numel():
+                return 1
+            buf = self.ws[off : off + nbytes]
+            s = torch.cuda.ExternalStream(int(stream)) if stream else torch.cuda.default_stream(self.ws.device)
+            with torch.cuda.stream(s):
+                if op == hyd.COLL_MIN_I64:
+                    reduce_keys(buf.view(torch.int64), self.group)
+                else:
+                    share_rows(buf.view(torch.int32), self.group)
+            return 0
+        except Exception:  # reported as HYD_E_REDUCE
+            return 1
 
     @property
     def h2d_bytes_fixed(self) -> int:
@@ -391,19 +415,20 @@ class Proposer:
 
     def candidates(self):
         """Proposed subset as per-scheme pipeline counts [M][K] (first-occurrence order) and as
-        candidate tables (cand [M][32] u8 in canonical order, cand_np [M] u8)."""
-        self.torch.cuda.synchronize(self.dev)
+        candidate tables (cand [M][32] u8 in canonical order, cand_np [M] u8), the tables made on
+        the device by hyd_dp_candidates."""
+        torch = self.torch
+        M = (self.J + 1) * hyd.DP_MAX_ROUND
+        cand = torch.empty((M, hyd.MAX_PIPES), dtype=torch.uint8, device=self.dev)
+        cnp = torch.empty((M,), dtype=torch.uint8, device=self.dev)
+        n_out = torch.zeros((1,), dtype=torch.int32, device=self.dev)
+        hyd.dp_candidates(self.rows, self.keep, self.J, self.schemes, self.K, cand, cnp, n_out)
+        torch.cuda.synchronize(self.dev)
+        n = int(n_out.item())
         rows = self.rows.cpu().numpy().reshape(-1, self.K)
         keep = self.keep.cpu().numpy().reshape(-1).astype(bool)
         sel = rows[keep]
-        ml = self.schemes_np["max_len"].astype(np.int64)
-        order = sorted(range(self.K), key=lambda k: (-ml[k], k))  # canonical pipelines (P:623)
-        cand = np.full((sel.shape[0], hyd.MAX_PIPES), 0xFF, np.uint8)
-        cnp = np.zeros(sel.shape[0], np.uint8)
-        for m, r in enumerate(sel):
-            ks = [k for k in order for _ in range(int(r[k]))]
-            if len(ks) > hyd.MAX_PIPES:
-                raise hyd.HydError(f"proposed candidate with {len(ks)} pipelines > {hyd.MAX_PIPES}")
-            cand[m, : len(ks)] = ks
-            cnp[m] = len(ks)
+        cand, cnp = cand[:n].cpu().numpy(), cnp[:n].cpu().numpy()
+        if (cnp == 0).any():
+            raise hyd.HydError(f"a proposed candidate has more than {hyd.MAX_PIPES} pipelines")
         return sel, cand, cnp

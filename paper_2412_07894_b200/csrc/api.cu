@@ -18,6 +18,9 @@ int launch_pack(const uint32_t*, const uint32_t*, int, int, const uint32_t*, siz
                 const uint8_t*, const uint8_t*, int, int, const uint8_t*, const hyd_pipe_stats*,
                 const uint32_t*, uint16_t*, uint16_t*, uint64_t*, uint64_t*, uint32_t*, void*, size_t,
                 cudaStream_t);
+int launch_pipe_index(const uint32_t*, const uint32_t*, int, int, const uint32_t*, size_t, int, const hyd_scheme*,
+                      int, const uint8_t*, const uint8_t*, int, int, const uint8_t*, uint64_t*, hyd_pipe_stats*,
+                      uint32_t*, uint32_t*, cudaStream_t);
 int launch_select(const uint64_t*, int, int, int, int64_t*, uint32_t*, cudaStream_t);
 int launch_gather(const int64_t*, const uint32_t*, const uint8_t*, const uint16_t*, const uint16_t*,
                   const uint64_t*, int, int, const uint32_t*, size_t, int, int, uint8_t*, uint16_t*,
@@ -38,6 +41,8 @@ int launch_eq1_exact(const uint32_t*, const uint32_t*, int, int, int, const hyd_
                      const int32_t*, int, unsigned long long, uint32_t*, uint64_t*, uint64_t*,
                      uint8_t*, uint32_t*, cudaStream_t);
 size_t dp_workspace(int, int);
+int launch_dp_candidates(const uint8_t*, const uint8_t*, int, const hyd_scheme*, int, uint8_t*, uint8_t*, int32_t*,
+                         cudaStream_t);
 int launch_dp(const uint32_t*, int, const hyd_scheme*, int, int, int, int, int, uint64_t*, uint64_t*,
               int32_t*, uint16_t*, uint8_t*, uint8_t*, uint8_t*, uint32_t*, void*, cudaStream_t);
 
@@ -53,7 +58,7 @@ int record_cuda_error(cudaError_t e) {
 }
 
 static bool common_ok(int n_iter, int batch, int n_schemes, int k_pad) {
-  return n_iter >= 0 && batch >= 1 && batch <= HYD_MAX_BATCH && n_schemes >= 1 &&
+  return n_iter >= 0 && n_iter <= HYD_MAX_ITER && batch >= 1 && batch <= HYD_MAX_BATCH && n_schemes >= 1 &&
          n_schemes <= HYD_MAX_SCHEMES && k_pad >= n_schemes && (k_pad % 4) == 0 &&
          k_pad <= HYD_MAX_SCHEMES;
 }
@@ -216,6 +221,32 @@ int hyd_dispatch_ragged(const uint32_t* sorted_len, const uint32_t* cost, int n_
                          status, ws, (cudaStream_t)stream);
 }
 
+int hyd_pipe_index(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch, int k_pad,
+                   const hyd_scheme* schemes, int n_schemes, const uint8_t* cand, const uint8_t* cand_np,
+                   int n_cand, int max_np, const uint8_t* pipe, uint64_t* lb, hyd_pipe_stats* stats,
+                   uint32_t* members, uint32_t* status, void* stream) {
+  if (!sorted_len || !cost || !schemes || !cand || !cand_np || !pipe || !stats || !members || !status ||
+      !common_ok(n_iter, batch, n_schemes, k_pad) || !cand_ok(n_cand, max_np))
+    return HYD_E_INVALID;
+  return launch_pipe_index(sorted_len, cost, n_iter, batch, nullptr, (size_t)n_iter * batch, k_pad, schemes,
+                           n_schemes, cand, cand_np, n_cand, max_np, pipe, lb, stats, members, status,
+                           (cudaStream_t)stream);
+}
+
+int hyd_pipe_index_ragged(const uint32_t* sorted_len, const uint32_t* cost, int n_iter,
+                          const uint32_t* offsets, int n_total, int batch_max, int k_pad,
+                          const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
+                          const uint8_t* cand_np, int n_cand, int max_np, const uint8_t* pipe,
+                          uint64_t* lb, hyd_pipe_stats* stats, uint32_t* members, uint32_t* status,
+                          void* stream) {
+  if (!sorted_len || !cost || !offsets || !schemes || !cand || !cand_np || !pipe || !stats || !members ||
+      !status || n_total < 0 || !common_ok(n_iter, batch_max, n_schemes, k_pad) || !cand_ok(n_cand, max_np))
+    return HYD_E_INVALID;
+  return launch_pipe_index(sorted_len, cost, n_iter, batch_max, offsets, (size_t)n_total, k_pad, schemes,
+                           n_schemes, cand, cand_np, n_cand, max_np, pipe, lb, stats, members, status,
+                           (cudaStream_t)stream);
+}
+
 size_t hyd_alg1_workspace(int n_iter) {
   if (n_iter < 0) return 0;
   return alg1_workspace(n_iter);
@@ -223,7 +254,7 @@ size_t hyd_alg1_workspace(int n_iter) {
 
 int hyd_alg1_permutations(uint64_t seed, int n_iter, int batch, int trials, uint16_t* order,
                           void* stream) {
-  if (!order || n_iter < 0 || batch < 1 || batch > HYD_MAX_BATCH || trials < 1 ||
+  if (!order || n_iter < 0 || n_iter > HYD_MAX_ITER || batch < 1 || batch > HYD_MAX_BATCH || trials < 1 ||
       trials > HYD_MAX_TRIALS)
     return HYD_E_INVALID;
   return launch_alg1_perm(seed, n_iter, batch, trials, order, (cudaStream_t)stream);
@@ -292,6 +323,14 @@ int hyd_dp_propose(const uint32_t* lengths, int n_seq, const hyd_scheme* schemes
                    counts, rows, valid, keep, status, ws, (cudaStream_t)stream);
 }
 
+int hyd_dp_candidates(const uint8_t* rows, const uint8_t* keep, int J, const hyd_scheme* schemes,
+                      int n_schemes, uint8_t* cand, uint8_t* cand_np, int32_t* n_out, void* stream) {
+  if (!rows || !keep || !schemes || !cand || !cand_np || !n_out || J < 1 || J > 4095 || n_schemes < 1 ||
+      n_schemes > HYD_MAX_SCHEMES)
+    return HYD_E_INVALID;
+  return launch_dp_candidates(rows, keep, J, schemes, n_schemes, cand, cand_np, n_out, (cudaStream_t)stream);
+}
+
 size_t hyd_pack_workspace(int n_iter, int batch, int n_cand, int max_np) {
   if (n_iter < 0 || batch < 1 || n_cand < 0 || max_np < 1) return 0;
   return pack_workspace(n_iter, batch, n_cand, max_np);
@@ -331,7 +370,7 @@ int hyd_pack_ragged(const uint32_t* sorted_len, const uint32_t* cost, int n_iter
 
 int hyd_select_best(const uint64_t* makespan, int n_iter, int n_cand, int cand_offset,
                     int64_t* key, uint32_t* status, void* stream) {
-  if (!makespan || !key || !status || n_iter < 0 || n_cand < 0 || cand_offset < 0 ||
+  if (!makespan || !key || !status || n_iter < 0 || n_iter > HYD_MAX_ITER || n_cand < 0 || cand_offset < 0 ||
       (long long)n_cand + cand_offset > (1ll << HYD_KEY_SHIFT) - 1)
     return HYD_E_INVALID;
   return launch_select(makespan, n_iter, n_cand, cand_offset, key, status, (cudaStream_t)stream);
@@ -342,7 +381,7 @@ int hyd_gather_winners(const int64_t* key, const uint32_t* perm, const uint8_t* 
                        int batch, int n_cand, int cand_offset, uint8_t* win_pipe, uint16_t* win_mb,
                        uint16_t* win_v, uint64_t* win_ptime, void* stream) {
   if (!key || !perm || !pipe || !mb || !v || !ptime || !win_pipe || !win_mb || !win_v ||
-      !win_ptime || n_iter < 0 || batch < 1 || batch > HYD_MAX_BATCH || n_cand < 0 ||
+      !win_ptime || n_iter < 0 || n_iter > HYD_MAX_ITER || batch < 1 || batch > HYD_MAX_BATCH || n_cand < 0 ||
       cand_offset < 0)
     return HYD_E_INVALID;
   return launch_gather(key, perm, pipe, mb, v, ptime, n_iter, batch, nullptr, (size_t)n_iter * batch,
@@ -355,7 +394,7 @@ int hyd_gather_winners_ragged(const int64_t* key, const uint32_t* perm, const ui
                               int n_cand, int cand_offset, uint8_t* win_pipe, uint16_t* win_mb,
                               uint16_t* win_v, uint64_t* win_ptime, void* stream) {
   if (!key || !perm || !pipe || !mb || !v || !ptime || !offsets || !win_pipe || !win_mb ||
-      !win_v || !win_ptime || n_iter < 0 || n_total < 0 || batch_max < 1 ||
+      !win_v || !win_ptime || n_iter < 0 || n_iter > HYD_MAX_ITER || n_total < 0 || batch_max < 1 ||
       batch_max > HYD_MAX_BATCH || n_cand < 0 || cand_offset < 0)
     return HYD_E_INVALID;
   return launch_gather(key, perm, pipe, mb, v, ptime, n_iter, batch_max, offsets, (size_t)n_total,
@@ -390,7 +429,7 @@ static int assign_host_impl(const uint32_t* len_host, int n_iter, const uint32_t
                             const uint8_t* cand_host, const uint8_t* cand_np_host, int n_cand,
                             int cand_offset, int64_t* key_host, uint8_t* win_pipe_host,
                             uint16_t* win_mb_host, uint16_t* win_v_host, uint64_t* win_ptime_host,
-                            uint32_t* status_host, hyd_reduce_fn reduce, void* reduce_user,
+                            uint32_t* status_host, hyd_collective_fn coll, void* coll_user,
                             void* ws, size_t ws_bytes, void* stream) {
   if (!len_host || !schemes_host || !cand_host || !cand_np_host || !key_host || !win_pipe_host ||
       !win_mb_host || !win_v_host || !win_ptime_host || !status_host ||
@@ -461,11 +500,15 @@ static int assign_host_impl(const uint32_t* len_host, int n_iter, const uint32_t
   if (rc) return rc;
   rc = launch_select(ms, n_iter, n_cand, cand_offset, key, st, s);
   if (rc) return rc;
-  if (reduce && reduce(key, n_iter, reduce_user, stream) != 0) return HYD_E_REDUCE;
+  if (coll && coll(key, It, HYD_COLL_MIN_I64, coll_user, stream) != 0) return HYD_E_REDUCE;
+  // winner rows: zero-filled block, each rank writes the iterations its candidates won
+  const size_t rows_bytes = L.disp_ws - L.win_pipe;  // win_pipe | win_mb | win_v | win_ptime (256-aligned)
+  HYD_CK(cudaMemsetAsync(D(L.win_pipe), 0, rows_bytes, s));
   rc = launch_gather(key, perm, pipe, mb, vv, pt, n_iter, batch, off, N, n_cand, cand_offset,
                      static_cast<uint8_t*>(D(L.win_pipe)), static_cast<uint16_t*>(D(L.win_mb)),
                      static_cast<uint16_t*>(D(L.win_v)), static_cast<uint64_t*>(D(L.win_ptime)), s);
   if (rc) return rc;
+  if (coll && coll(D(L.win_pipe), rows_bytes / 4, HYD_COLL_SUM_I32, coll_user, stream) != 0) return HYD_E_REDUCE;
   HYD_CK(cudaMemcpyAsync(key_host, key, It * 8, cudaMemcpyDeviceToHost, s));
   HYD_CK(cudaMemcpyAsync(win_pipe_host, D(L.win_pipe), N, cudaMemcpyDeviceToHost, s));
   HYD_CK(cudaMemcpyAsync(win_mb_host, D(L.win_mb), N * 2, cudaMemcpyDeviceToHost, s));
@@ -481,11 +524,11 @@ int hyd_assign_host(const uint32_t* len_host, int n_iter, int batch, const hyd_s
                     int n_schemes, int k_pad, const uint8_t* cand_host, const uint8_t* cand_np_host,
                     int n_cand, int cand_offset, int64_t* key_host, uint8_t* win_pipe_host,
                     uint16_t* win_mb_host, uint16_t* win_v_host, uint64_t* win_ptime_host,
-                    uint32_t* status_host, hyd_reduce_fn reduce, void* reduce_user, void* ws,
+                    uint32_t* status_host, hyd_collective_fn coll, void* coll_user, void* ws,
                     size_t ws_bytes, void* stream) {
   return assign_host_impl(len_host, n_iter, nullptr, batch, schemes_host, n_schemes, k_pad,
                           cand_host, cand_np_host, n_cand, cand_offset, key_host, win_pipe_host,
-                          win_mb_host, win_v_host, win_ptime_host, status_host, reduce, reduce_user,
+                          win_mb_host, win_v_host, win_ptime_host, status_host, coll, coll_user,
                           ws, ws_bytes, stream);
 }
 
@@ -494,12 +537,12 @@ int hyd_assign_host_ragged(const uint32_t* len_host, int n_iter, const uint32_t*
                            const uint8_t* cand_host, const uint8_t* cand_np_host, int n_cand,
                            int cand_offset, int64_t* key_host, uint8_t* win_pipe_host,
                            uint16_t* win_mb_host, uint16_t* win_v_host, uint64_t* win_ptime_host,
-                           uint32_t* status_host, hyd_reduce_fn reduce, void* reduce_user, void* ws,
+                           uint32_t* status_host, hyd_collective_fn coll, void* coll_user, void* ws,
                            size_t ws_bytes, void* stream) {
   if (!offsets_host) return HYD_E_INVALID;
   return assign_host_impl(len_host, n_iter, offsets_host, batch_max, schemes_host, n_schemes, k_pad,
                           cand_host, cand_np_host, n_cand, cand_offset, key_host, win_pipe_host,
-                          win_mb_host, win_v_host, win_ptime_host, status_host, reduce, reduce_user,
+                          win_mb_host, win_v_host, win_ptime_host, status_host, coll, coll_user,
                           ws, ws_bytes, stream);
 }
 

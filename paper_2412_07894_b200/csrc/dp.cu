@@ -311,6 +311,75 @@ __global__ void k_dp_unique(const uint8_t* __restrict__ rows, const uint8_t* __r
   keep[m] = 1;
 }
 
+// The proposed subset (keep = 1, in (j, r) order) as candidate tables the assignment takes:
+// pipelines in canonical order (MaxLen non-increasing, scheme index ascending: P:623), each
+// scheme repeated by its pipeline count.  One CTA: a block-wide exclusive scan of keep gives
+// each kept row its output index; a row with more than HYD_MAX_PIPES pipelines gets cand_np 0.
+constexpr int kDpCandThreads = 1024;
+__global__ void __launch_bounds__(kDpCandThreads)
+    k_dp_candidates(const uint8_t* __restrict__ rows, const uint8_t* __restrict__ keep, int M,
+                    const hyd_scheme* __restrict__ schemes, int K, uint8_t* __restrict__ cand,
+                    uint8_t* __restrict__ cand_np, int32_t* __restrict__ n_out) {
+  __shared__ uint8_t s_order[HYD_MAX_SCHEMES];  // canonical position -> scheme
+  __shared__ int s_warp[kDpCandThreads / 32];
+  __shared__ int s_base;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < K) {  // rank of scheme tid in (MaxLen desc, k asc)
+    const uint32_t m = schemes[tid].max_len;
+    int r = 0;
+    for (int q = 0; q < K; ++q) {
+      const uint32_t mq = schemes[q].max_len;
+      r += (mq > m || (mq == m && q < tid)) ? 1 : 0;
+    }
+    s_order[r] = (uint8_t)tid;
+  }
+  if (tid == 0) s_base = 0;
+  __syncthreads();
+  for (int m0 = 0; m0 < M; m0 += kDpCandThreads) {
+    const int m = m0 + tid;
+    const int kp = (m < M && keep[m]) ? 1 : 0;
+    const unsigned bal = __ballot_sync(HYD_FULL, kp);
+    if (lane == 0) s_warp[warp] = __popc(bal);
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the warp counts
+      int x = s_warp[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(HYD_FULL, x, o);
+        if (lane >= o) x += y;
+      }
+      s_warp[lane] = x - s_warp[lane];
+    }
+    __syncthreads();
+    const int at = s_base + s_warp[warp] + __popc(bal & ((1u << lane) - 1u));
+    if (kp) {
+      const uint8_t* row = rows + (size_t)m * K;
+      uint8_t* out = cand + (size_t)at * HYD_MAX_PIPES;
+      int n = 0;
+      for (int q = 0; q < K; ++q) {
+        const int k = s_order[q];
+        for (int r = 0; r < (int)row[k]; ++r, ++n)
+          if (n < HYD_MAX_PIPES) out[n] = (uint8_t)k;
+      }
+      for (int q = n; q < HYD_MAX_PIPES; ++q) out[q] = 0xFF;
+      cand_np[at] = n <= HYD_MAX_PIPES ? (uint8_t)n : 0;
+    }
+    __syncthreads();
+    if (tid == kDpCandThreads - 1) s_base = at + kp;
+    __syncthreads();
+  }
+  if (tid == 0) *n_out = s_base;
+}
+
+int launch_dp_candidates(const uint8_t* rows, const uint8_t* keep, int J, const hyd_scheme* schemes, int K,
+                         uint8_t* cand, uint8_t* cand_np, int32_t* n_out, cudaStream_t s) {
+  const int M = (J + 1) * HYD_DP_MAX_ROUND;
+  k_dp_candidates<<<1, kDpCandThreads, 0, s>>>(rows, keep, M, schemes, K, cand, cand_np, n_out);
+  note_launch();
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? HYD_OK : record_cuda_error(e);
+}
+
 size_t dp_workspace(int K, int J) {
   return ((size_t)K * (J + 1) * 8 + 255) & ~(size_t)255;  // prefix sums
 }

@@ -377,7 +377,7 @@ __device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, uint3
 // VM = 16: every (c,t,j) of the tile, classes 8 / 16; a task needing some V > 16 is flagged
 //          for the VM = 32 pass.  VM = 32: flagged tasks only (tiles of up to 2048 candidates, records
 //          compacted).  Tasks the lanes cannot hold (V > VM in the last pass, sumT over the key
-//          limit, an infeasible V_a and V_a + 1) go to the warp queue, which runs the sequential
+//          limit, no feasible LPT(V) for V_a <= V <= min(V_hi, VM)) go to the warp queue, which runs the sequential
 //          exact search.
 template <bool STAGED, int VM>
 __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(PackArgs a, int tc, int mnp, int ncap) {
@@ -697,8 +697,9 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
   };
   phase_clock(0);
   // ---- phase 1: the V_a run of every task (writes mb); where LPT(V_a) is infeasible
-  //      (capacity), the same lane goes on with V_a + 1, which then takes V_a's place as the
-  //      reference run of the exact tests below
+  //      (capacity), the same lane goes on with V_a + 1, V_a + 2, ... (up to min(V_hi, VM)); the
+  //      first feasible one takes V_a's place as the reference run of the exact tests below (any
+  //      completed run is a valid reference: the walk re-examines every other V of the range)
   run_units(
       std::false_type{}, std::integral_constant<int, 1>{}, nrec,
       [&](int q) {
@@ -714,7 +715,7 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
         }
         R.key[r] = kBottom;
         const uint32_t V = u.V + 1u;
-        if (V > (uint32_t)R.vhi[r] || V > (uint32_t)VM || V != (uint32_t)R.va[r] + 1u) return false;
+        if (V > (uint32_t)R.vhi[r] || V > (uint32_t)VM) return false;
         R.va[r] = (uint16_t)V;
         load_unit(r, V, 0xFFFFFFFFu, true, false);
         return true;  // keep the lane on this task

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libhyd.so")
 
 HYD_OK = 0
-STATUS_BITS = {1: "OVERFLOW", 2: "ZERO_COST", 4: "BAD_LENGTH", 8: "KEY_RANGE", 16: "NOT_CANONICAL"}
+STATUS_BITS = {1: "OVERFLOW", 2: "ZERO_COST", 4: "BAD_LENGTH", 8: "KEY_RANGE", 16: "NOT_CANONICAL", 32: "BAD_PIPE"}
 MAX_PIPES = 32
 PIPE_STATS_BYTES = 24  # sizeof(hyd_pipe_stats)
 KEY_SHIFT = 20
@@ -50,6 +50,9 @@ EXPORTS = (
     "hyd_alg1_workspace",
     "hyd_alg1_permutations",
     "hyd_dispatch_alg1",
+    "hyd_pipe_index",
+    "hyd_pipe_index_ragged",
+    "hyd_dp_candidates",
 )
 
 
@@ -57,7 +60,9 @@ class HydError(RuntimeError):
     pass
 
 
-REDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p)
+# hyd_collective_fn(buf_dev, count, op, user, stream); op: COLL_MIN_I64 / COLL_SUM_I32
+COLL_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p, C.c_void_p)
+COLL_MIN_I64, COLL_SUM_I32 = 0, 1
 _lib = None
 
 
@@ -80,7 +85,7 @@ def lib():
         "hyd_gather_winners": ([P, P, P, P, P, P, I, I, I, I, P, P, P, P, P], I),
         "hyd_assign_workspace": ([I, I, I, I, I, I], Z),
         "hyd_assign_key_offset": ([I, I, I, I, I, I], Z),
-        "hyd_assign_host": ([P, I, I, P, I, I, P, P, I, I, P, P, P, P, P, P, REDUCE_FN, P, P, Z, P], I),
+        "hyd_assign_host": ([P, I, I, P, I, I, P, P, I, I, P, P, P, P, P, P, COLL_FN, P, P, Z, P], I),
         "hyd_check_candidates": ([P, P, I, P, I, C.POINTER(C.c_int)], I),
         "hyd_status_string": ([I], C.c_char_p),
         "hyd_last_cuda_error": ([], C.c_char_p),
@@ -91,7 +96,7 @@ def lib():
         "hyd_gather_winners_ragged": ([P, P, P, P, P, P, I, P, I, I, I, I, P, P, P, P, P], I),
         "hyd_assign_workspace_ragged": ([I, I, I, I, I, I, I], Z),
         "hyd_assign_key_offset_ragged": ([I, I, I, I, I, I, I], Z),
-        "hyd_assign_host_ragged": ([P, I, P, I, P, I, I, P, P, I, I, P, P, P, P, P, P, REDUCE_FN, P, P, Z, P], I),
+        "hyd_assign_host_ragged": ([P, I, P, I, P, I, I, P, P, I, I, P, P, P, P, P, P, COLL_FN, P, P, Z, P], I),
         "hyd_eq3_exact": ([P, P, I, I, I, P, I, P, P, I, P, P, I, C.c_uint64, P, P, P, P, P, P], I),
         "hyd_eq1_exact": ([P, P, I, I, I, P, I, P, I, I, P, P, P, P, I, C.c_uint64, P, P, P, P, P, P], I),
         "hyd_dp_workspace": ([I, I], Z),
@@ -99,6 +104,9 @@ def lib():
         "hyd_alg1_workspace": ([I], Z),
         "hyd_alg1_permutations": ([U64, I, I, I, P, P], I),
         "hyd_dispatch_alg1": ([P, P, I, I, I, P, I, P, P, I, I, I, P, P, P, P, P, P, P, P, Z, P], I),
+        "hyd_dp_candidates": ([P, P, I, P, I, P, P, P, P], I),
+        "hyd_pipe_index": ([P, P, I, I, I, P, I, P, P, I, I, P, P, P, P, P, P], I),
+        "hyd_pipe_index_ragged": ([P, P, I, P, I, I, I, P, I, P, P, I, I, P, P, P, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -220,8 +228,8 @@ def assign_key_offset_ragged(n_iter, n_total, batch_max, n_schemes, k_pad, n_can
 
 def assign_host_ragged(len_host_ptr, n_iter, off_host_ptr, batch_max, schemes_host_ptr, n_schemes, k_pad,
                        cand_host_ptr, cand_np_host_ptr, n_cand, cand_offset, key_host_ptr, win_pipe_ptr, win_mb_ptr,
-                       win_v_ptr, win_ptime_ptr, status_ptr, reduce_cb, ws, stream=None):
-    cb = reduce_cb if reduce_cb is not None else REDUCE_FN(0)
+                       win_v_ptr, win_ptime_ptr, status_ptr, coll_cb, ws, stream=None):
+    cb = coll_cb if coll_cb is not None else COLL_FN(0)
     _check(lib().hyd_assign_host_ragged(len_host_ptr, n_iter, off_host_ptr, batch_max, schemes_host_ptr, n_schemes,
                                         k_pad, cand_host_ptr, cand_np_host_ptr, n_cand, cand_offset, key_host_ptr,
                                         win_pipe_ptr, win_mb_ptr, win_v_ptr, win_ptime_ptr, status_ptr, cb, None,
@@ -263,6 +271,11 @@ def dp_propose(lengths, n_seq, schemes, n_schemes, step, J, n_gpus, scale, t_num
            "hyd_dp_propose")
 
 
+def dp_candidates(rows, keep, J, schemes, n_schemes, cand, cand_np, n_out, stream=None):
+    _check(lib().hyd_dp_candidates(_dev(rows), _dev(keep), J, _dev(schemes), n_schemes, _dev(cand), _dev(cand_np),
+                                   _dev(n_out), _stream(stream)), "hyd_dp_candidates")
+
+
 def alg1_workspace(n_iter) -> int:
     return int(lib().hyd_alg1_workspace(n_iter))
 
@@ -278,6 +291,21 @@ def dispatch_alg1(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, ca
                                    _dev(cand), _dev(cand_np), n_cand, max_np, trials, _dev(order), _dev(best),
                                    _dev(pipe), _dev(lb), _dev(stats), _dev(members), _dev(status), _dev(ws),
                                    ws.numel() * ws.element_size(), _stream(stream)), "hyd_dispatch_alg1")
+
+
+def pipe_index(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, pipe, lb,
+               stats, members, status, stream=None):
+    _check(lib().hyd_pipe_index(_dev(sorted_len), _dev(cost), n_iter, batch, k_pad, _dev(schemes), n_schemes,
+                                _dev(cand), _dev(cand_np), n_cand, max_np, _dev(pipe), _dev(lb), _dev(stats),
+                                _dev(members), _dev(status), _stream(stream)), "hyd_pipe_index")
+
+
+def pipe_index_ragged(sorted_len, cost, n_iter, off, n_total, batch_max, k_pad, schemes, n_schemes, cand, cand_np,
+                      n_cand, max_np, pipe, lb, stats, members, status, stream=None):
+    _check(lib().hyd_pipe_index_ragged(_dev(sorted_len), _dev(cost), n_iter, _dev(off), n_total, batch_max, k_pad,
+                                       _dev(schemes), n_schemes, _dev(cand), _dev(cand_np), n_cand, max_np,
+                                       _dev(pipe), _dev(lb), _dev(stats), _dev(members), _dev(status),
+                                       _stream(stream)), "hyd_pipe_index_ragged")
 
 
 def select_best(makespan, n_iter, n_cand, cand_offset, key, status, stream=None):
@@ -302,9 +330,9 @@ def assign_key_offset(n_iter, batch, n_schemes, k_pad, n_cand, max_np) -> int:
 
 def assign_host(len_host_ptr, n_iter, batch, schemes_host_ptr, n_schemes, k_pad, cand_host_ptr, cand_np_host_ptr,
                 n_cand, cand_offset, key_host_ptr, win_pipe_ptr, win_mb_ptr, win_v_ptr, win_ptime_ptr,
-                status_ptr, reduce_cb, ws, stream=None):
-    """hyd_assign_host with HOST pointers (ints); ``reduce_cb`` is a REDUCE_FN or None."""
-    cb = reduce_cb if reduce_cb is not None else REDUCE_FN(0)
+                status_ptr, coll_cb, ws, stream=None):
+    """hyd_assign_host with HOST pointers (ints); ``coll_cb`` is a COLL_FN or None (one rank)."""
+    cb = coll_cb if coll_cb is not None else COLL_FN(0)
     _check(lib().hyd_assign_host(len_host_ptr, n_iter, batch, schemes_host_ptr, n_schemes, k_pad, cand_host_ptr,
                                  cand_np_host_ptr, n_cand, cand_offset, key_host_ptr, win_pipe_ptr, win_mb_ptr,
                                  win_v_ptr, win_ptime_ptr, status_ptr, cb, None, _dev(ws),

@@ -2,7 +2,9 @@
 Alg. 1, against facts that do not come from the oracle itself.
 
 * Philox4x32-10: the published known-answer vectors (tests/golden/philox4x32_10_kat.json).
-* The trial permutation (reading 21): a permutation; uniform over S_3.
+* The trial permutation (readings 20-21): a literal transcription of reading 20 on an
+  independently written Philox4x32-10 (itself checked against the known-answer vectors); a
+  permutation; uniform over S_3.
 * One trial: a literal Python transcription of the pseudo-code (dispatch matrix m_ij, l_max
   as the max over m_ij * l_i, E' through the closed-form cost App. C.2, O_max as the
   max over every other pipeline, strict < so the first j wins).
@@ -65,6 +67,43 @@ def test_permutation_depends_on_every_key_part():
     assert oracle.alg1_permutation(1, 3, 3, 64).tolist() != base
     assert oracle.alg1_permutation(1, 2, 4, 64).tolist() != base
     assert oracle.alg1_permutation(1 << 40, 2, 3, 64).tolist() != oracle.alg1_permutation(0, 2, 3, 64).tolist()
+
+
+# Philox4x32-10 written out independently of the oracle (Salmon et al., SC'11: multipliers
+# 0xD2511F53 / 0xCD9E8D57, Weyl key increments 0x9E3779B9 / 0xBB67AE85, ten rounds), itself
+# checked against the published known-answer vectors before it is used below.
+def _philox_py(ctr, key):
+    c, k = [int(x) for x in ctr], [int(x) for x in key]
+    for _ in range(10):
+        p0, p1 = 0xD2511F53 * c[0], 0xCD9E8D57 * c[2]
+        c = [(p1 >> 32) ^ c[1] ^ k[0], p1 & 0xFFFFFFFF, (p0 >> 32) ^ c[3] ^ k[1], p0 & 0xFFFFFFFF]
+        k = [(k[0] + 0x9E3779B9) & 0xFFFFFFFF, (k[1] + 0xBB67AE85) & 0xFFFFFFFF]
+    return c
+
+
+def _fisher_yates_reading20(seed, t, trial, B):
+    """DESIGN.md reading 20, literally: start from the identity over the B sorted positions; for
+    k = B-1 down to 1: r = Philox4x32-10(counter (floor(k/4), t, trial, 0), key (seed mod 2^32,
+    floor(seed / 2^32))) word (k mod 4); j = floor(r (k+1) / 2^32); swap(order[k], order[j])."""
+    order = list(range(B))
+    key = (seed & 0xFFFFFFFF, seed >> 32)
+    for k in range(B - 1, 0, -1):
+        r = _philox_py((k // 4, t, trial, 0), key)[k % 4]
+        j = (r * (k + 1)) >> 32
+        order[k], order[j] = order[j], order[k]
+    return order
+
+
+def test_permutation_literal_transcription():
+    kat = json.load(open(os.path.join(GOLD, "philox4x32_10_kat.json")))
+    for v in kat["vectors"]:  # the transcription's generator is the published one
+        out = _philox_py([int(x, 16) for x in v["ctr"]], [int(x, 16) for x in v["key"]])
+        assert out == [int(x, 16) for x in v["out"]]
+    for seed, t, trial, B in [(12345, 7, 0, 5), (12345, 7, 3, 5), (2024, 0, 99, 5), ((7 << 32) | 9, 513, 255, 5),
+                              (1, 2, 3, 17), (99, 1023, 17, 64), (5, 6, 7, 513)]:
+        want = _fisher_yates_reading20(seed, t, trial, B)
+        got = oracle.alg1_permutation(seed, t, trial, B).tolist()
+        assert got == want, (seed, t, trial, B, got, want)
 
 
 def alg1_trial_literal(sorted_len, schemes, cand_row, order):

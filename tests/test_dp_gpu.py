@@ -39,6 +39,13 @@ def check(env, lens, schemes, step, J, N, scale):
         assert np.array_equal(counts[j], c.astype(np.uint16)) if ok else (counts[j] == 0).all()
     assert [tuple(int(x) for x in r) for r in sel] == rows
     assert int(P.status.item()) == st
+    # hyd_dp_candidates: each proposed row as a canonical candidate (MaxLen desc, index asc)
+    ml = schemes["max_len"].astype(np.int64)
+    order = sorted(range(len(schemes)), key=lambda k: (-ml[k], k))
+    assert cand.shape[0] == len(rows)
+    for m, r in enumerate(rows):
+        ks = [k for k in order for _ in range(r[k])]
+        assert int(cnp[m]) == len(ks) and cand[m, : len(ks)].tolist() == ks and (cand[m, len(ks):] == 0xFF).all()
     return sel, cand, cnp
 
 
@@ -80,3 +87,11 @@ def test_dp_full_grid_runs(env):
     for nu in range(2, 641, 37):
         assert tn[nu, 256] * td[nu - 1, 256] <= tn[nu - 1, 256] * td[nu, 256] or td[nu - 1, 256] == 0
     assert int(P.status.item()) == 0
+
+
+def test_dp_parity_paper_grid(env):
+    """The paper's own grid (P:713 footnote: n and d in steps of 0.1, l in steps of 128 tokens to
+    the 32K context; 64 GPUs) on config 6's 1024-iteration length sample -- the bench --dp
+    workload -- bit-exact against the enumerating oracle (~4.7e9 transitions on the CPU)."""
+    W = w.make_workload(6, n_cand=2, n_iter=1024)
+    check(env, np.ascontiguousarray(W.lengths), W.schemes, 128, 256, 64, 10)

@@ -164,3 +164,23 @@ def test_strategy_reproduces_objective_and_rounding_budget():
             assert max(vals) == frac(tn[N * scale, j], td[N * scale, j]) and used <= N * scale
         for r in rows:
             assert int((np.array(r) * g).sum()) <= N and sum(r) >= 1
+
+
+def test_round_hand_worked():
+    """Reading 27 ("round and adjust to include all nearby integer solutions") by hand.
+    Schemes: k0 = <2,1,1> (2 GPUs), k1 = <4,1,1> (4 GPUs), k2 = <1,1,1> (1 GPU); scale 10.
+    d = (1.5, 2.3, 1.0): k0 and k1 are non-integer (q = 0, 1), k2 stays 1.  Combinations
+      m=0 floor/floor (1,2,1): 2+8+1 = 11 GPUs;  m=1 ceil k0 (2,2,1): 13;
+      m=2 ceil k1 (1,3,1): 15;  m=3 both (2,3,1): 17.
+    With N = 16 GPUs and top scheme k1: m = 0, 1, 2 kept, m = 3 over budget.
+    d = (1.5, 0.7, 1.0), top k1: floor(0.7) = 0 drops the top scheme (m = 0, 1); m=2 (1,1,1) = 7
+    and m=3 (2,1,1) = 9 GPUs -> N = 8 keeps only m = 2, N = 9 keeps m = 2, 3.
+    Seven non-integer schemes need 2^7 = 128 > 64 combinations: nothing (flagged)."""
+    sch = np.concatenate([w.make_scheme(tp=2, max_len=4096, b_q32=1 << 32), w.make_scheme(tp=4, max_len=8192, b_q32=1 << 32),
+                          w.make_scheme(tp=1, max_len=2048, b_q32=1 << 32)])
+    got = oracle.dp_round([15, 23, 10], 1, sch, 16, 10)
+    assert got == [(0, (1, 2, 1)), (1, (2, 2, 1)), (2, (1, 3, 1))]
+    assert oracle.dp_round([15, 7, 10], 1, sch, 8, 10) == [(2, (1, 1, 1))]
+    assert oracle.dp_round([15, 7, 10], 1, sch, 9, 10) == [(2, (1, 1, 1)), (3, (2, 1, 1))]
+    sch7 = np.concatenate([w.make_scheme(max_len=1000 + k, b_q32=1 << 32) for k in range(7)])
+    assert oracle.dp_round([5] * 7, 0, sch7, 64, 10) is None

@@ -1,9 +1,12 @@
-"""N > 1 host logic on CPU: candidate/iteration sharding, key packing and the
-allreduce-MIN argmin (a6), over torch.distributed gloo with world sizes 2 and 3.
+"""N > 1 host logic on CPU: candidate/iteration sharding, key packing, the allreduce-MIN
+argmin (a6) and the winner-row exchange, over torch.distributed gloo with world sizes 2 and 3.
 
 Each rank computes its shard's keys with the CPU oracle (standing in for the GPU path,
 which is parity-checked separately) and reduces them with the product's own
-``assign.reduce_keys``; the result must equal the single-process selection."""
+``assign.reduce_keys``; the result must equal the single-process selection.  Then each rank
+fills the zero-initialised winner-row block (pipe | mb | v | ptime per iteration, original
+sequence order) for the iterations its candidates won and ``assign.share_rows`` sums it: every
+rank must end with the single-process winners' plans (include/hyd.h hyd_assign_host)."""
 import os
 import socket
 
@@ -40,6 +43,8 @@ def _worker(rank, world, port, cfg, n_cand, n_iter, out):
         if sh.needs_reduce:
             assign.reduce_keys(key)
             full = key
+            block = _win_block(r, key.numpy(), sh.cand_lo, sub.n_cand)
+            out[("rows", rank)] = assign.share_rows(torch.from_numpy(block)).numpy().tobytes()
         else:  # iteration shards: gather the disjoint slices (off the metric path)
             full = torch.full((W.n_iter,), -1, dtype=torch.int64)
             full[sh.iter_lo:sh.iter_hi] = key
@@ -47,6 +52,27 @@ def _worker(rank, world, port, cfg, n_cand, n_iter, out):
         out[rank] = full.numpy().tolist()
     finally:
         dist.destroy_process_group()
+
+
+def _win_block(r, key, cand_lo, n_cand):
+    """Winner rows of the iterations whose winner lies in [cand_lo, cand_lo + n_cand), zeros
+    elsewhere, as one int32 block: pipe u8 [It][B] | mb u16 [It][B] | v u16 [It][32] | ptime u64."""
+    It, B = r["perm"].shape
+    pipe = np.zeros((It, B), np.uint8)
+    mb = np.zeros((It, B), np.uint16)
+    v = np.zeros((It, 32), np.uint16)
+    pt = np.zeros((It, 32), np.uint64)
+    for t in range(It):
+        if key[t] == 2**63 - 1:
+            continue
+        c = int(key[t] & ((1 << 20) - 1)) - cand_lo
+        if 0 <= c < n_cand:
+            pipe[t, r["perm"][t]] = r["pipe"][c, t]
+            mb[t, r["perm"][t]] = r["mb"][c, t]
+            v[t], pt[t] = r["v"][c, t], r["ptime"][c, t]
+    raw = b"".join(x.tobytes() for x in (pipe, mb, v, pt))
+    raw += b"\0" * (-len(raw) % 4)
+    return np.frombuffer(raw, np.int32).copy()
 
 
 @pytest.mark.parametrize("world,cfg,n_cand,n_iter", [(2, 4, 37, 3), (3, 2, 20, 4), (2, 1, 1, 6), (3, 3, 5, 2)])
@@ -60,6 +86,11 @@ def test_sharded_argmin_matches_single(world, cfg, n_cand, n_iter, oracle_lib):
     ref = oracle_lib.assign_batch(W)["key"]
     for r in range(world):
         assert np.array_equal(np.array(out[r], dtype=np.int64), ref), (r, out[r], ref)
+    full = oracle_lib.assign_batch(W)
+    want = _win_block(full, ref, 0, W.n_cand).tobytes()
+    for r in range(world):
+        if ("rows", r) in out:
+            assert out[("rows", r)] == want, r
     ms, c = assign.decode_key(ref)
     feas = ref != 2**63 - 1
     assert (c[feas] < W.n_cand).all() and (ms[feas] > 0).all()
