@@ -43,6 +43,7 @@ extern "C" {
 
 #define HYD_MAX_ITER 65535
 #define HYD_MAX_BATCH 16384
+#define HYD_SMALL_MAX_BATCH 128 /* hyd_dispatch_pack: largest batch */
 #define HYD_MAX_SCHEMES 64
 #define HYD_MAX_PIPES 32
 #define HYD_MAX_PP 1024
@@ -169,6 +170,20 @@ int hyd_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int b
              uint64_t* ptime, uint64_t* makespan, uint32_t* status, void* ws, size_t ws_bytes,
              void* stream);
 
+/* ---- a3 + a4 fused for small batches ------------------------------------------------------
+ * hyd_dispatch_pack: the same results as hyd_dispatch followed by hyd_pack -- pipe, lb, mb, v,
+ * ptime, makespan, bit for bit -- in one kernel for batch <= HYD_SMALL_MAX_BATCH sequences and
+ * max_np <= 16 pipelines (the paper's token-budget iterations), without the
+ * stats / members index (not written).  ws: hyd_dispatch_pack_workspace() bytes; the u64 at ws
+ * byte 0 counts the (sequence, micro-batch) evaluations performed (diagnostic).  Larger batches
+ * or candidates return HYD_E_INVALID (use hyd_dispatch + hyd_pack). */
+size_t hyd_dispatch_pack_workspace(void);
+int hyd_dispatch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch, int k_pad,
+                      const hyd_scheme* schemes, int n_schemes, const uint8_t* cand, const uint8_t* cand_np,
+                      int n_cand, int max_np, uint8_t* pipe, uint64_t* lb, uint16_t* mb, uint16_t* v,
+                      uint64_t* ptime, uint64_t* makespan, uint32_t* status, void* ws, size_t ws_bytes,
+                      void* stream);
+
 /* ---- a5: selection ---------------------------------------------------------------------
  * key[t] = min over c of (makespan[t][c] << 20 | (c + cand_offset)) among feasible
  * candidates with makespan < 2^43 (others: HYD_F_KEY_RANGE); INT64_MAX if none.  The
@@ -279,6 +294,12 @@ int hyd_pipe_index_ragged(const uint32_t* sorted_len, const uint32_t* cost, int 
                           const uint8_t* cand_np, int n_cand, int max_np, const uint8_t* pipe,
                           uint64_t* lb, hyd_pipe_stats* stats, uint32_t* members, uint32_t* status,
                           void* stream);
+int hyd_dispatch_pack_ragged(const uint32_t* sorted_len, const uint32_t* cost, int n_iter,
+                             const uint32_t* offsets, int n_total, int batch_max, int k_pad,
+                             const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
+                             const uint8_t* cand_np, int n_cand, int max_np, uint8_t* pipe, uint64_t* lb,
+                             uint16_t* mb, uint16_t* v, uint64_t* ptime, uint64_t* makespan,
+                             uint32_t* status, void* ws, size_t ws_bytes, void* stream);
 int hyd_gather_winners_ragged(const int64_t* key, const uint32_t* perm, const uint8_t* pipe,
                               const uint16_t* mb, const uint16_t* v, const uint64_t* ptime,
                               int n_iter, const uint32_t* offsets, int n_total, int batch_max,

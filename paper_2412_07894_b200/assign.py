@@ -87,7 +87,7 @@ class Assigner:
     """
 
     def __init__(self, schemes, cand, cand_np, n_iter, batch, k_pad, cand_offset=0, device=None, trials=0,
-                 seed=0, offsets=None):
+                 seed=0, offsets=None, fused=None):
         import torch
 
         self.torch = torch
@@ -145,6 +145,10 @@ class Assigner:
         self.ws = torch.empty((max(hyd.pack_workspace(It, B, Cn, self.max_np), 1),), dtype=u8, device=dev)
         self.disp_ws = torch.empty((max(hyd.dispatch_workspace(It), 1),), dtype=u8, device=dev)
         self.trials, self.seed = int(trials), int(seed)
+        # a3 + a4 in one kernel for small batches (include/hyd.h hyd_dispatch_pack); no stats/members
+        small = B <= hyd.SMALL_MAX_BATCH and self.max_np <= 16 and not self.trials
+        self.fused = small if fused is None else (bool(fused) and small)
+        self.small_ws = torch.zeros((hyd.dispatch_pack_workspace(),), dtype=u8, device=dev)
         if self.trials:
             self.order = torch.empty((It, self.trials, B), dtype=torch.int16, device=dev)
             self.best = torch.empty((Cn, It), dtype=torch.int64, device=dev)
@@ -157,6 +161,12 @@ class Assigner:
             N = self.n_total
             hyd.cost_table_ragged(len_dev, It, self.off, N, B, self.schemes, K, kp, self.sorted_len, self.perm,
                                   self.cost, self.status, stream)
+            if self.fused:
+                hyd.dispatch_pack_ragged(self.sorted_len, self.cost, It, self.off, N, B, kp, self.schemes, K,
+                                         self.cand, self.cand_np, Cn, self.max_np, self.pipe, self.lb, self.mb, self.v,
+                                         self.ptime, self.makespan, self.status, self.small_ws, stream)
+                hyd.select_best(self.makespan, It, Cn, self.cand_offset, self.key, self.status, stream)
+                return self.key
             hyd.dispatch_ragged(self.sorted_len, self.cost, It, self.off, N, B, kp, self.schemes, K, self.cand,
                                 self.cand_np, Cn, self.max_np, self.pipe, self.lb, self.stats, self.members,
                                 self.status, self.disp_ws, stream)
@@ -166,6 +176,12 @@ class Assigner:
             hyd.select_best(self.makespan, It, Cn, self.cand_offset, self.key, self.status, stream)
             return self.key
         hyd.cost_table(len_dev, It, B, self.schemes, K, kp, self.sorted_len, self.perm, self.cost, self.status, stream)
+        if self.fused:
+            hyd.dispatch_pack(self.sorted_len, self.cost, It, B, kp, self.schemes, K, self.cand, self.cand_np, Cn,
+                              self.max_np, self.pipe, self.lb, self.mb, self.v, self.ptime, self.makespan, self.status,
+                              self.small_ws, stream)
+            hyd.select_best(self.makespan, It, Cn, self.cand_offset, self.key, self.status, stream)
+            return self.key
         if self.trials:
             hyd.alg1_permutations(self.seed, It, B, self.trials, self.order, stream)
             hyd.dispatch_alg1(self.sorted_len, self.cost, It, B, kp, self.schemes, K, self.cand, self.cand_np, Cn,
@@ -203,6 +219,8 @@ class Assigner:
     def eq1_exact(self, pair_c, pair_t, pair_j, node_limit=1 << 24, stream=None):
         """NEXT-4: exact Eq. 1 optimum of the listed pipelines of the LAST run() (its dispatch);
         include/hyd.h hyd_eq1_exact.  Returns numpy (v, obj, nodes, proved)."""
+        if self.fused:
+            raise hyd.HydError("eq1_exact reads the dispatch's members: build the Assigner with fused=False")
         torch = self.torch
         It, B, K, kp, Cn = self.n_iter, self.batch, self.n_schemes, self.k_pad, self.n_cand
         mk = lambda x: torch.as_tensor(np.asarray(x, np.int32), device=self.dev)
@@ -219,8 +237,12 @@ class Assigner:
                 nodes.cpu().numpy().view(np.uint64), proved.cpu().numpy().astype(bool))
 
     def pack_counters(self) -> dict:
-        """Work counter written by the last hyd_pack (include/hyd.h: u64 at ws offset 16)."""
+        """Work counter written by the last hyd_pack (include/hyd.h: u64 at ws offset 16), or by
+        the fused small-batch kernel (u64 at its ws offset 0)."""
         self.torch.cuda.synchronize(self.dev)
+        if self.fused:
+            return {"bin_evals": int(self.small_ws[0:8].cpu().numpy().view(np.uint64)[0]), "queued_tasks": 0,
+                    "handoff": None}
         w = self.ws[0:256].cpu().numpy().view(np.uint64)
         names = ["sumt16", "va16", "bottom16", "cand16", "sumt32", "bottom32", "cand32", "overflow",
                  "clk_records", "clk_phase1", "clk_phase1b", "clk_walk", "clk_phase2", "clk_phase3",

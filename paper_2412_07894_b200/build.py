@@ -10,8 +10,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libhyd.so")
-SOURCES = ["sort_cost.cu", "dispatch.cu", "alg1.cu", "pack.cu", "select.cu", "index.cu", "dp.cu", "bb.cu", "api.cu"]
-HEADERS = ["hyd_internal.cuh"]
+SOURCES = ["sort_cost.cu", "dispatch.cu", "alg1.cu", "pack.cu", "select.cu", "index.cu", "small.cu", "dp.cu", "bb.cu", "api.cu"]
+HEADERS = ["hyd_internal.cuh", "search.cuh"]
 
 
 def nvcc() -> str:

@@ -21,6 +21,9 @@ int launch_pack(const uint32_t*, const uint32_t*, int, int, const uint32_t*, siz
 int launch_pipe_index(const uint32_t*, const uint32_t*, int, int, const uint32_t*, size_t, int, const hyd_scheme*,
                       int, const uint8_t*, const uint8_t*, int, int, const uint8_t*, uint64_t*, hyd_pipe_stats*,
                       uint32_t*, uint32_t*, cudaStream_t);
+int launch_small(const uint32_t*, const uint32_t*, int, int, const uint32_t*, size_t, int, const hyd_scheme*, int,
+                 const uint8_t*, const uint8_t*, int, int, uint8_t*, uint64_t*, uint16_t*, uint16_t*, uint64_t*,
+                 uint64_t*, uint32_t*, void*, cudaStream_t);
 int launch_select(const uint64_t*, int, int, int, int64_t*, uint32_t*, cudaStream_t);
 int launch_gather(const int64_t*, const uint32_t*, const uint8_t*, const uint16_t*, const uint16_t*,
                   const uint64_t*, int, int, const uint32_t*, size_t, int, int, uint8_t*, uint16_t*,
@@ -368,6 +371,40 @@ int hyd_pack_ragged(const uint32_t* sorted_len, const uint32_t* cost, int n_iter
                      makespan, status, ws, ws_bytes, (cudaStream_t)stream);
 }
 
+size_t hyd_dispatch_pack_workspace(void) { return 256; }
+
+static bool small_ok(int batch, int max_np) { return batch <= HYD_SMALL_MAX_BATCH && max_np <= 16; }
+
+int hyd_dispatch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch, int k_pad,
+                      const hyd_scheme* schemes, int n_schemes, const uint8_t* cand, const uint8_t* cand_np,
+                      int n_cand, int max_np, uint8_t* pipe, uint64_t* lb, uint16_t* mb, uint16_t* v,
+                      uint64_t* ptime, uint64_t* makespan, uint32_t* status, void* ws, size_t ws_bytes,
+                      void* stream) {
+  if (!sorted_len || !cost || !schemes || !cand || !cand_np || !pipe || !lb || !mb || !v || !ptime || !makespan ||
+      !status || !common_ok(n_iter, batch, n_schemes, k_pad) || !cand_ok(n_cand, max_np) || !small_ok(batch, max_np))
+    return HYD_E_INVALID;
+  if (!ws || ws_bytes < hyd_dispatch_pack_workspace()) return HYD_E_WORKSPACE;
+  return launch_small(sorted_len, cost, n_iter, batch, nullptr, (size_t)n_iter * batch, k_pad, schemes, n_schemes,
+                      cand, cand_np, n_cand, max_np, pipe, lb, mb, v, ptime, makespan, status, ws,
+                      (cudaStream_t)stream);
+}
+
+int hyd_dispatch_pack_ragged(const uint32_t* sorted_len, const uint32_t* cost, int n_iter,
+                             const uint32_t* offsets, int n_total, int batch_max, int k_pad,
+                             const hyd_scheme* schemes, int n_schemes, const uint8_t* cand,
+                             const uint8_t* cand_np, int n_cand, int max_np, uint8_t* pipe, uint64_t* lb,
+                             uint16_t* mb, uint16_t* v, uint64_t* ptime, uint64_t* makespan,
+                             uint32_t* status, void* ws, size_t ws_bytes, void* stream) {
+  if (!sorted_len || !cost || !offsets || !schemes || !cand || !cand_np || !pipe || !lb || !mb || !v || !ptime ||
+      !makespan || !status || n_total < 0 || !common_ok(n_iter, batch_max, n_schemes, k_pad) ||
+      !cand_ok(n_cand, max_np) || !small_ok(batch_max, max_np))
+    return HYD_E_INVALID;
+  if (!ws || ws_bytes < hyd_dispatch_pack_workspace()) return HYD_E_WORKSPACE;
+  return launch_small(sorted_len, cost, n_iter, batch_max, offsets, (size_t)n_total, k_pad, schemes, n_schemes,
+                      cand, cand_np, n_cand, max_np, pipe, lb, mb, v, ptime, makespan, status, ws,
+                      (cudaStream_t)stream);
+}
+
 int hyd_select_best(const uint64_t* makespan, int n_iter, int n_cand, int cand_offset,
                     int64_t* key, uint32_t* status, void* stream) {
   if (!makespan || !key || !status || n_iter < 0 || n_iter > HYD_MAX_ITER || n_cand < 0 || cand_offset < 0 ||
@@ -492,12 +529,18 @@ static int assign_host_impl(const uint32_t* len_host, int n_iter, const uint32_t
   if (rc) return rc;
   auto* pst = static_cast<hyd_pipe_stats*>(D(L.stats));
   auto* mem = static_cast<uint32_t*>(D(L.members));
-  rc = launch_dispatch(sorted, cost, n_iter, batch, off, N, k_pad, sch, n_schemes, cand, cnp, n_cand, max_np,
-                       pipe, static_cast<uint64_t*>(D(L.lb)), pst, mem, st, D(L.disp_ws), s);
-  if (rc) return rc;
-  rc = launch_pack(sorted, cost, n_iter, batch, off, N, k_pad, sch, n_schemes, cand, cnp, n_cand, max_np,
-                   pipe, pst, mem, mb, vv, pt, ms, st, D(L.pack_ws), L.pack_bytes, s);
-  if (rc) return rc;
+  if (batch <= HYD_SMALL_MAX_BATCH && max_np <= 16) {  // a3 + a4 in one kernel (hyd_dispatch_pack)
+    rc = launch_small(sorted, cost, n_iter, batch, off, N, k_pad, sch, n_schemes, cand, cnp, n_cand, max_np, pipe,
+                      static_cast<uint64_t*>(D(L.lb)), mb, vv, pt, ms, st, D(L.disp_ws), s);
+    if (rc) return rc;
+  } else {
+    rc = launch_dispatch(sorted, cost, n_iter, batch, off, N, k_pad, sch, n_schemes, cand, cnp, n_cand, max_np,
+                         pipe, static_cast<uint64_t*>(D(L.lb)), pst, mem, st, D(L.disp_ws), s);
+    if (rc) return rc;
+    rc = launch_pack(sorted, cost, n_iter, batch, off, N, k_pad, sch, n_schemes, cand, cnp, n_cand, max_np,
+                     pipe, pst, mem, mb, vv, pt, ms, st, D(L.pack_ws), L.pack_bytes, s);
+    if (rc) return rc;
+  }
   rc = launch_select(ms, n_iter, n_cand, cand_offset, key, st, s);
   if (rc) return rc;
   if (coll && coll(key, It, HYD_COLL_MIN_I64, coll_user, stream) != 0) return HYD_E_REDUCE;

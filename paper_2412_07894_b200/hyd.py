@@ -53,6 +53,9 @@ EXPORTS = (
     "hyd_pipe_index",
     "hyd_pipe_index_ragged",
     "hyd_dp_candidates",
+    "hyd_dispatch_pack_workspace",
+    "hyd_dispatch_pack",
+    "hyd_dispatch_pack_ragged",
 )
 
 
@@ -104,6 +107,9 @@ def lib():
         "hyd_alg1_workspace": ([I], Z),
         "hyd_alg1_permutations": ([U64, I, I, I, P, P], I),
         "hyd_dispatch_alg1": ([P, P, I, I, I, P, I, P, P, I, I, I, P, P, P, P, P, P, P, P, Z, P], I),
+        "hyd_dispatch_pack_workspace": ([], Z),
+        "hyd_dispatch_pack": ([P, P, I, I, I, P, I, P, P, I, I, P, P, P, P, P, P, P, P, Z, P], I),
+        "hyd_dispatch_pack_ragged": ([P, P, I, P, I, I, I, P, I, P, P, I, I, P, P, P, P, P, P, P, P, Z, P], I),
         "hyd_dp_candidates": ([P, P, I, P, I, P, P, P, P], I),
         "hyd_pipe_index": ([P, P, I, I, I, P, I, P, P, I, I, P, P, P, P, P, P], I),
         "hyd_pipe_index_ragged": ([P, P, I, P, I, I, I, P, I, P, P, I, I, P, P, P, P, P, P], I),
@@ -306,6 +312,30 @@ def pipe_index_ragged(sorted_len, cost, n_iter, off, n_total, batch_max, k_pad, 
                                        _dev(schemes), n_schemes, _dev(cand), _dev(cand_np), n_cand, max_np,
                                        _dev(pipe), _dev(lb), _dev(stats), _dev(members), _dev(status),
                                        _stream(stream)), "hyd_pipe_index_ragged")
+
+
+SMALL_MAX_BATCH = 128
+
+
+def dispatch_pack_workspace() -> int:
+    return int(lib().hyd_dispatch_pack_workspace())
+
+
+def dispatch_pack(sorted_len, cost, n_iter, batch, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, pipe, lb,
+                  mb, v, ptime, makespan, status, ws, stream=None):
+    _check(lib().hyd_dispatch_pack(_dev(sorted_len), _dev(cost), n_iter, batch, k_pad, _dev(schemes), n_schemes,
+                                   _dev(cand), _dev(cand_np), n_cand, max_np, _dev(pipe), _dev(lb), _dev(mb), _dev(v),
+                                   _dev(ptime), _dev(makespan), _dev(status), _dev(ws), ws.numel() * ws.element_size(),
+                                   _stream(stream)), "hyd_dispatch_pack")
+
+
+def dispatch_pack_ragged(sorted_len, cost, n_iter, off, n_total, batch_max, k_pad, schemes, n_schemes, cand, cand_np,
+                         n_cand, max_np, pipe, lb, mb, v, ptime, makespan, status, ws, stream=None):
+    _check(lib().hyd_dispatch_pack_ragged(_dev(sorted_len), _dev(cost), n_iter, _dev(off), n_total, batch_max, k_pad,
+                                          _dev(schemes), n_schemes, _dev(cand), _dev(cand_np), n_cand, max_np,
+                                          _dev(pipe), _dev(lb), _dev(mb), _dev(v), _dev(ptime), _dev(makespan),
+                                          _dev(status), _dev(ws), ws.numel() * ws.element_size(), _stream(stream)),
+           "hyd_dispatch_pack_ragged")
 
 
 def select_best(makespan, n_iter, n_cand, cand_offset, key, status, stream=None):

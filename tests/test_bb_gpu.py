@@ -80,7 +80,7 @@ def test_eq1_exact_parity(env, B, D):
     never above the heuristic's ptime."""
     O, assign = env["oracle"], env["assign"]
     W = small_workload(B, D, 30, 2, 100 + B)
-    A = assign.Assigner(W.schemes, W.cand, W.cand_np, W.n_iter, W.batch, W.k_pad)
+    A = assign.Assigner(W.schemes, W.cand, W.cand_np, W.n_iter, W.batch, W.k_pad, fused=False)  # reads members
     A.run(assign.lengths_to_device(W.lengths))
     g = A.numpy()
     pc, pt, pj = [], [], []

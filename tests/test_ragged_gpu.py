@@ -22,8 +22,9 @@ def env():
     return dict(torch=torch, oracle=oracle, assign=assign, hyd=hyd)
 
 
-def run_gpu(env, W):
-    A = env["assign"].Assigner(W.schemes, W.cand, W.cand_np, W.n_iter, W.batch, W.k_pad, offsets=W.offsets)
+def run_gpu(env, W, fused=None):
+    A = env["assign"].Assigner(W.schemes, W.cand, W.cand_np, W.n_iter, W.batch, W.k_pad, offsets=W.offsets,
+                               fused=fused)
     A.run(env["assign"].lengths_to_device(W.lengths))
     return A, A.numpy()
 
@@ -39,10 +40,13 @@ def compare(g, o, tag):
     assert g["status"] == o["status"], (tag, g["status"], o["status"])
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("n_cand,n_iter", [(133, 6), (300, 3), (1, 9)])
-def test_ragged_parity_cfg6(env, n_cand, n_iter):
+def test_ragged_parity_cfg6(env, n_cand, n_iter, fused):
+    """Both code paths: hyd_dispatch_pack (one kernel) and hyd_dispatch + hyd_pack."""
     W = w.make_workload(6, n_cand=n_cand, n_iter=n_iter)
-    _, g = run_gpu(env, W)
+    A, g = run_gpu(env, W, fused=fused)
+    assert A.fused == fused
     compare(g, env["oracle"].assign_batch_ragged(W), f"cfg6-{n_cand}x{n_iter}")
 
 
@@ -57,6 +61,11 @@ def test_ragged_edges(env):
     W = w.Workload(0, "ragged-edge", L, base.schemes, base.cand, base.cand_np, base.k_pad, offsets=off)
     _, g = run_gpu(env, W)
     compare(g, env["oracle"].assign_batch_ragged(W), "ragged-edges")
+    W2 = w.Workload(0, "ragged-edge-small", np.ascontiguousarray(L[: off[4]]), base.schemes, base.cand, base.cand_np,
+                    base.k_pad, offsets=off[:5].copy())  # batches <= 17: the fused kernel
+    A2, g2 = run_gpu(env, W2)
+    assert A2.fused
+    compare(g2, env["oracle"].assign_batch_ragged(W2), "ragged-edges-fused")
 
 
 def test_uniform_as_ragged_matches_uniform_path(env):
