@@ -732,7 +732,9 @@ def verify_multi(W, sh, A, H, world, rank, dev):
     if H is not None:
         rows_ok = bool(np.array_equal(H.key.numpy(), ref["key"][lo:hi]))
         for k in ("win_pipe", "win_mb", "win_v", "win_ptime"):
-            rows_ok = rows_ok and bool(np.array_equal(getattr(H, k).numpy(), ref[k][lo:hi]))
+            # ragged rows are [N_total] (candidate shards only: every rank holds every iteration)
+            want = ref[k] if (W.ragged and k in ("win_pipe", "win_mb")) else ref[k][lo:hi]
+            rows_ok = rows_ok and bool(np.array_equal(getattr(H, k).numpy(), want))
     flags = torch.tensor([int(keys_ok), int(rows_ok)], dtype=torch.int32, device=dev)
     dist.all_reduce(flags, op=dist.ReduceOp.MIN)
     return {"keys_equal_one_rank": bool(flags[0].item()), "winner_rows_equal_one_rank": bool(flags[1].item()),
