@@ -28,18 +28,30 @@ FLAGS = [
 ]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "hyd.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None) -> str:
-    if not force and not _stale():
-        return LIB
-    bdir = os.path.join(HERE, "build")
+DEBUG_LIB = os.path.join(HERE, "libhyd_debug.so")
+
+
+def build_debug(force: bool = False) -> str:
+    """libhyd_debug.so: the same sources with -DHYD_DEBUG_CHECKS (device bounds checks); loaded
+    instead of libhyd.so when HYD_LIB points at it (tools/sanitize_cases.py)."""
+    if not force and os.path.exists(DEBUG_LIB) and not _stale(DEBUG_LIB):
+        return DEBUG_LIB
+    return build(force=True, extra=["-DHYD_DEBUG_CHECKS"], out=DEBUG_LIB, bdir_name="build_debug")
+
+
+def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None, out: str = LIB,
+          bdir_name: str = "build") -> str:
+    if not force and not _stale(out):
+        return out
+    bdir = os.path.join(HERE, bdir_name)
     os.makedirs(bdir, exist_ok=True)
     objs = []
     for src in SOURCES:
@@ -49,10 +61,10 @@ def build(force: bool = False, verbose: bool = False, extra: list[str] | None = 
             print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)
         objs.append(obj)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = out + f".tmp{os.getpid()}"
     subprocess.check_call([nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", tmp])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

@@ -97,6 +97,7 @@ __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
 #pragma unroll
       for (int j = 0; j < DP; ++j) {
         if (j < np) {
+          HYD_CHECK(j < mstride);
           mbits[(size_t)(i >> 5) * mstride + j] = bits[j];
           // cf_j = U_j << 16 | (index of the first (= longest) member + 1), B <= 16384
           const uint32_t f = (cf[j] & 0xFFFFu) == 0u && bits[j] != 0u ? w0 + __ffs(bits[j]) : 0u;

@@ -9,6 +9,26 @@
 #define HYD_LEN_LIMIT (1u << 24)
 #define HYD_MAKESPAN_LIMIT (1ull << 43)
 
+// Debug builds (libhyd_debug.so, -DHYD_DEBUG_CHECKS; tools/sanitize_cases.py): bounds checks on
+// the shared-memory and global indices the kernels compute; a failed check prints its site and
+// traps the kernel (the call then returns HYD_E_CUDA).  compute-sanitizer is closed on this GPU
+// pool, so this build is the memory-safety check of the test plan.
+#ifdef HYD_DEBUG_CHECKS
+#include <cstdio>
+#define HYD_CHECK(cond)                                                                      \
+  do {                                                                                       \
+    if (!(cond)) {                                                                           \
+      printf("HYD_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+             (int)blockIdx.x, (int)threadIdx.x);                                             \
+      __trap();                                                                              \
+    }                                                                                        \
+  } while (0)
+#else
+#define HYD_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace hyd {
 
 // Launch bookkeeping (diagnostics only): counts kernels this library launched.

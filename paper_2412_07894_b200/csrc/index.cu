@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(kIndexWarps * 32)
         u += __popc(m);
         s_sum += sl_;
         t_sum += (uint64_t)tlo + ((uint64_t)thi << 16);
+        HYD_CHECK(j < max_np && w < nwords);
         if (!infeasible) mbits[(size_t)w * max_np + j] = m;
       }
     }

@@ -199,6 +199,9 @@ struct LaneUnit {
   uint32_t qw, cur, wbase, nxtw;
   uint32_t V, thr, mx, k, M;
   uint32_t tb;  // STAGED: shared-window address of the cost column k (row 0)
+#ifdef HYD_DEBUG_CHECKS
+  uint32_t bt;  // the iteration's sequences (member indices must stay below)
+#endif
   int e;
   bool write;
   bool F;  // capacity-free: no placement of this run can exceed MaxLen before it completes or aborts
@@ -248,6 +251,7 @@ __device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, uint3
   const uint32_t i = valid ? u.wbase + (uint32_t)(__ffs(u.cur) - 1) : 0u;
   u.cur &= u.cur - 1u;
   // STAGED: 32-bit shared-window addresses (sbase: lengths; u.tb + 4 kp i: the cost of row i)
+  HYD_CHECK(!valid || i < u.bt);
   const uint32_t tau = STAGED ? ld_shared_u32(u.tb + i * kp4) : cst[(size_t)i * kp + u.k];
   const uint32_t l = FREE ? 0u : (STAGED ? ld_shared_u32(sbase + i * 4u) : slen[i]);
   uint32_t m0;
@@ -405,6 +409,7 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
     const int ub = min(31, (int)(s.U >> 3));
     const int bk = (VM == 16 && s.va <= 8) ? ub : 32 + ub;  // heavier class first, then larger U
     R.perm[r] = (uint16_t)bk;  // bucket, replaced by the order below
+    HYD_CHECK(bk >= 0 && bk < NB && r < ncap);
     atomicAdd(&s_hist[bk], 1);
   }
   __syncthreads();
@@ -476,6 +481,7 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
       int pos = 0;
       if (lane == leader && bk >= 0) pos = atomicAdd(&s_hist[bk], __popc(peers));
       pos = __shfl_sync(HYD_FULL, pos, leader) + __popc(peers & ((1u << lane) - 1u));
+      HYD_CHECK(bk < 0 || (pos >= 0 && pos < nrec));
       if (bk >= 0) R.list2[pos] = (uint32_t)r;
     }
     __syncthreads();
@@ -537,6 +543,10 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
     u.write = write;
     u.F = F;
     u.tb = sbase + ((uint32_t)B + u.k) * 4u;
+#ifdef HYD_DEBUG_CHECKS
+    u.bt = (uint32_t)B;
+    HYD_CHECK(r >= 0 && r < ncap && u.k < (uint32_t)kp);
+#endif
     unit_start<VM>(u, V, thr);
   };
   // Lanes pull consecutive units of a list sorted by (class, U) -- so the units a warp holds at
@@ -766,8 +776,10 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
         const uint32_t V = (uint32_t)__ffs(m);
         const uint32_t w = ((uint32_t)r << 16) | V;
         if (VM == 16 && V <= 8) {
+          HYD_CHECK(i_lo >= n_lo || p_lo + i_lo < ncap);
           if (i_lo < n_lo) R.list2[p_lo + i_lo++] = w;
         } else {
+          HYD_CHECK(i_hi >= n_hi || p_hi + i_hi < ncap);
           if (i_hi < n_hi) R.list2[p_hi + i_hi++] = w;
         }
       }
@@ -776,8 +788,10 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
     run_units(
         std::true_type{}, std::integral_constant<int, 2>{}, s_n2b,
         [&](int q) {
+          HYD_CHECK(q < ncap);
           const uint32_t w = R.list2[q];
           const int r = (int)(w >> 16);
+          HYD_CHECK(r < nrec);
           const uint32_t V = w & 0xFFFFu;
           const uint32_t thr = unit_thr(r, V, R.key[r] >> 16);
           load_unit(r, V, thr, false, thr <= s_cap[R.k[r]]);
@@ -1005,6 +1019,7 @@ __device__ __forceinline__ bool lpt_warp(const uint32_t* __restrict__ mw, uint32
             tk[r] += h ? l : 0u;
           }
         } else {
+          HYD_CHECK(bstar < V);
           scr_t[bstar] += (uint64_t)tau;
           scr_k[bstar] += l;
         }

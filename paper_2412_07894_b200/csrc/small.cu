@@ -106,6 +106,7 @@ __device__ __forceinline__ bool run_keys(const uint32_t* __restrict__ mw, int nw
       }
       mx = max(mx, (KT)((mk >> 4) + tau));
       if (mx > thr_k) return false;
+      HYD_CHECK(i < HYD_SMALL_MAX_BATCH);
       if (write) mbs[i] = (uint8_t)(mk & 15u);
     }
   }
@@ -141,6 +142,7 @@ __device__ __noinline__ bool run_generic(const uint32_t* __restrict__ mw, int nw
         }
       ev += V;
       if (bb == 0xFFFFFFFFu) return false;
+      HYD_CHECK(bb < V && V <= HYD_SMALL_MAX_BATCH && i < HYD_SMALL_MAX_BATCH);
       tm[bb] += tau;
       tok[bb] += l;
       mx = max(mx, tm[bb]);
@@ -187,6 +189,7 @@ __device__ __forceinline__ void small_dispatch(const uint32_t* __restrict__ sl, 
       mult[j] = hit ? 1u : mult[j];
       S[j] += hit ? l : 0u;
     }
+    HYD_CHECK(bj < (uint32_t)DP && i < HYD_SMALL_MAX_BATCH);
     mem[bj * kSmallWords + (i >> 5)] |= 1u << (i & 31);
     if (words) {
       word |= bj << (8 * (i & 3));

@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhyd.so")
+# HYD_LIB: an alternative build of the same sources (libhyd_debug.so, device bounds checks)
+LIB_PATH = os.environ.get("HYD_LIB") or os.path.join(HERE, "libhyd.so")
 
 HYD_OK = 0
 STATUS_BITS = {1: "OVERFLOW", 2: "ZERO_COST", 4: "BAD_LENGTH", 8: "KEY_RANGE", 16: "NOT_CANONICAL", 32: "BAD_PIPE"}
