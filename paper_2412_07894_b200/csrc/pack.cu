@@ -75,6 +75,8 @@ struct PackArgs {
   unsigned long long* queue;
   unsigned long long q_cap;
   uint32_t* flags;  // [It*C*mnp bits] tasks handed from the VMAX-16 to the VMAX-32 lane pass
+  uint32_t* list32;   // [It][C*mnp] the flagged tasks of each iteration, compacted (c*mnp + j)
+  uint32_t* count32;  // [It] their number
   uint64_t* scr_time;  // [kBigWarps][B]
   uint32_t* scr_tok;   // [kBigWarps][B]
 };
@@ -289,11 +291,16 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
   __shared__ uint32_t s_ml[HYD_MAX_SCHEMES], s_pp[HYD_MAX_SCHEMES], s_ul[HYD_MAX_SCHEMES];
   __shared__ uint32_t s_cap[HYD_MAX_SCHEMES];  // floor(alpha_k MaxLen_k), see min_keys
   const int kp = a.k_pad;
-  const int t = blockIdx.y, c0 = blockIdx.x * tc;
+  // VMAX 16: CTA = (candidate tile, iteration); VMAX 32: CTA = (chunk of <= ncap of the
+  // iteration's flagged tasks from the compacted list, iteration), task ids c * mnp + j (c0 = 0)
+  const int t = blockIdx.y, c0 = VM == 16 ? blockIdx.x * tc : 0;
+  const int chunk0 = VM == 32 ? blockIdx.x * ncap : 0;
+  const int nchunk = VM == 32 ? min(ncap, (int)a.count32[t] - chunk0) : 0;
+  if (VM == 32 && nchunk <= 0) return;
   const int B = geo_bt(a.off, a.batch, t);  // this iteration's sequences
   const size_t tbase = geo_base(a.off, a.batch, t);
   const int tid = threadIdx.x, lane = tid & 31;
-  const int ncl = min(tc, a.n_cand - c0);
+  const int ncl = VM == 16 ? min(tc, a.n_cand - c0) : a.n_cand;
   const int ntile = ncl * mnp;  // task ids of the tile
   const uint32_t nwords = (uint32_t)a.nwords;           // member row stride (largest batch)
   const uint32_t nwords_t = (uint32_t)((B + 31) >> 5);  // words of this iteration
@@ -360,13 +367,10 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
     }
   };
   // ---- task records (parallel, compacted), bucketed by (class, U) for LPT-order processing
-  for (int e = tid; e < ntile; e += kLaneThreads) {
+  for (int q = tid; q < (VM == 16 ? ntile : nchunk); q += kLaneThreads) {
+    const int e = VM == 16 ? q : (int)a.list32[(size_t)t * ((size_t)a.n_cand * mnp) + chunk0 + q];
     const int c = c0 + e / mnp, j = e % mnp;
     if (j >= (int)a.cand_np[c]) continue;
-    if (VM == 32) {
-      const size_t bit = fbase + e;
-      if (!((a.flags[bit >> 5] >> (bit & 31)) & 1u)) continue;
-    }
     const hyd_pipe_stats* sp = a.stats + (fbase + e - j);
     if (VM == 16 && sp[0].u == 0xFFFFFFFFu) continue;  // infeasible pair: rows written below
     const hyd_pipe_stats st = sp[j];
@@ -392,7 +396,7 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
       continue;
     }
     const int r = atomicAdd(&s_nrec, 1);
-    if (r >= ncap) {  // record space full (wide tiles of the VM = 32 pass)
+    if (r >= ncap) {  // record space full (cannot happen: tiles / chunks hold at most ncap tasks)
       atomicAdd(a.why + 7, 1ull);
       to_queue(c, j);
       continue;
@@ -863,6 +867,46 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
   if (ev) atomicAdd(a.evals, (unsigned long long)ev);
 }
 
+// The tasks the VMAX-16 pass flagged, per iteration, as a compacted list in ascending task id
+// (c * mnp + j): one CTA per iteration, block-wide scan of per-thread counts of 32-task groups.
+__global__ void __launch_bounds__(256) k_flag_list(const uint32_t* __restrict__ flags, int n_cand, int mnp,
+                                                   uint32_t* __restrict__ list32, uint32_t* __restrict__ count32) {
+  __shared__ int s_w[8];
+  __shared__ int s_base;
+  const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const size_t n = (size_t)n_cand * mnp, bit0 = (size_t)t * n;
+  uint32_t* out = list32 + (size_t)t * n;
+  if (tid == 0) s_base = 0;
+  __syncthreads();
+  for (size_t g0 = 0; g0 < n; g0 += 256 * 32) {
+    const size_t e0 = g0 + (size_t)tid * 32;  // this thread's 32 tasks
+    uint32_t bits = 0u;
+    if (e0 < n) {
+      const size_t b = bit0 + e0, w = b >> 5, sh = b & 31;
+      const size_t last = bit0 + min(n, e0 + 32) - 1;  // the group's last task bit
+      bits = flags[w] >> sh;
+      if (sh && (last >> 5) > w) bits |= flags[w + 1] << (32 - sh);
+      if (n - e0 < 32) bits &= (1u << (n - e0)) - 1u;
+    }
+    int x = __popc(bits);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(HYD_FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    int wbase = s_base;
+    for (int q = 0; q < warp; ++q) wbase += s_w[q];
+    int pos = wbase + x - __popc(bits);
+    for (uint32_t m = bits; m; m &= m - 1u) out[pos++] = (uint32_t)(e0 + __ffs(m) - 1);
+    __syncthreads();
+    if (tid == 255) s_base = wbase + x;
+    __syncthreads();
+  }
+  if (tid == 0) count32[t] = (uint32_t)s_base;
+}
+
 // ------------------------------------------------------------------ LPT, one warp per pipeline
 template <typename TT>
 __device__ __forceinline__ TT warp_min(TT x);
@@ -1174,7 +1218,8 @@ static size_t flag_bytes(int n_iter, int n_cand, int max_np) {
 size_t pack_workspace(int n_iter, int batch, int n_cand, int max_np) {
   const size_t cap = (size_t)n_iter * n_cand * dp_of(max_np);
   return align256(256) + align256(cap * 8) + align256((size_t)kBigWarps * batch * 8) +
-         align256((size_t)kBigWarps * batch * 4) + align256(flag_bytes(n_iter, n_cand, max_np));
+         align256((size_t)kBigWarps * batch * 4) + align256(flag_bytes(n_iter, n_cand, max_np)) +
+         align256((size_t)n_iter * n_cand * max_np * 4) + align256((size_t)n_iter * 4);
 }
 
 template <bool STAGED, int VM>
@@ -1235,6 +1280,10 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
   a.scr_tok = reinterpret_cast<uint32_t*>(w);
   w += align256((size_t)kBigWarps * batch * 4);
   a.flags = reinterpret_cast<uint32_t*>(w);
+  w += align256(flag_bytes(n_iter, n_cand, max_np));
+  a.list32 = reinterpret_cast<uint32_t*>(w);
+  w += align256((size_t)n_iter * n_cand * max_np * 4);
+  a.count32 = reinterpret_cast<uint32_t*>(w);
 
   cudaError_t e = cudaMemsetAsync(a.q_count, 0, 256, s);
   if (e != cudaSuccess) return record_cuda_error(e);
@@ -1263,9 +1312,12 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
           : launch_lanes<false, 16>(grid1, smem1, s, a, tc1, max_np, ncap1);
   note_launch();
   if (e != cudaSuccess) return record_cuda_error(e);
-  // (at most 2048 candidates per CTA: wide iterations flag more tasks than one CTA's records hold)
-  const int tc2 = max(1, min(n_cand, min(2048, 65535 / max_np)));
-  dim3 grid2((n_cand + tc2 - 1) / tc2, n_iter);
+  // the flagged tasks of each iteration, compacted; VMAX-32 CTAs take chunks of <= ncap2 of them
+  // (CTAs past an iteration's count exit at once)
+  k_flag_list<<<n_iter, 256, 0, s>>>(a.flags, n_cand, max_np, a.list32, a.count32);
+  note_launch();
+  const int tc2 = 0;
+  dim3 grid2((unsigned)(((size_t)n_cand * max_np + ncap2 - 1) / ncap2), n_iter);
   e = st2 ? launch_lanes<true, 32>(grid2, smem2, s, a, tc2, max_np, ncap2)
           : launch_lanes<false, 32>(grid2, smem2, s, a, tc2, max_np, ncap2);
   note_launch();
