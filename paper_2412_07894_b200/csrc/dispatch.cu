@@ -146,11 +146,7 @@ __device__ __forceinline__ uint32_t packed_pick(const uint32_t (&tau)[DP], uint3
   uint32_t m[DP];
 #pragma unroll
   for (int j = 0; j < DP; ++j) m[j] = tau[j] * (EMPTY ? mults[j] : one_sh) + key[j];
-#pragma unroll
-  for (int w = DP / 2; w > 0; w >>= 1)
-#pragma unroll
-    for (int j = 0; j < w; ++j) m[j] = min(m[j], m[j + w]);
-  const uint32_t mk = m[0];
+  const uint32_t mk = min_tree3<DP>(m);
   const uint32_t bj = mk & (uint32_t)(DP - 1);
 #pragma unroll
   for (int j = 0; j < DP; ++j) {

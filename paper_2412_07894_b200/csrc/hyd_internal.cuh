@@ -97,6 +97,25 @@ __device__ __forceinline__ uint32_t eval_cost(uint64_t a, uint64_t b, uint64_t c
   return t;
 }
 
+// min of m[0..N) as a ternary tree: ptxas fuses min(min(a, b), c) into one 3-input VIMNMX3, so
+// N keys take about N/2 instructions instead of N - 1 (e.g. 8 -> 4, 16 -> 8, 32 -> 17).
+// Overwrites m.
+template <int N, int A>
+__device__ __forceinline__ uint32_t min_tree3(uint32_t (&m)[A]) {
+  static_assert(N >= 1 && N <= A, "min_tree3 size");
+  if constexpr (N == 1) {
+    return m[0];
+  } else if constexpr (N == 2) {
+    return min(m[0], m[1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < N / 3; ++i) m[i] = min(min(m[3 * i], m[3 * i + 1]), m[3 * i + 2]);
+    if constexpr (N % 3 == 1) m[N / 3] = m[N - 1];
+    if constexpr (N % 3 == 2) m[N / 3] = min(m[N - 2], m[N - 1]);
+    return min_tree3<(N + 2) / 3, A>(m);
+  }
+}
+
 __device__ __forceinline__ int next_pow2_ge(int x) {
   int p = 1;
   while (p < x) p <<= 1;

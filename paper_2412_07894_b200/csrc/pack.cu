@@ -101,15 +101,10 @@ constexpr int pow2_ceil(int n) { return n <= 1 ? 1 : 2 * pow2_ceil((n + 1) / 2);
 template <int N, int VM>
 __device__ __forceinline__ uint32_t argmin_keys(const uint32_t (&keys)[VM],
                                                 const uint32_t (&rem)[VM], uint32_t l) {
-  constexpr int P = pow2_ceil(N);  // padded with never-chosen keys (folded away)
-  uint32_t m[P];
+  uint32_t m[N];
 #pragma unroll
-  for (int b = 0; b < P; ++b) m[b] = b < N ? keys[b] | ((rem[b] - l) & 0x80000000u) : 0xFFFFFFFFu;
-#pragma unroll
-  for (int w = P / 2; w > 0; w >>= 1)
-#pragma unroll
-    for (int b = 0; b < w; ++b) m[b] = min(m[b], m[b + w]);
-  return m[0];
+  for (int b = 0; b < N; ++b) m[b] = keys[b] | ((rem[b] - l) & 0x80000000u);
+  return min_tree3<N>(m);
 }
 
 // place the item in the bin whose key is mk (no bin when mk = 0xFFFFFFFF): one compare and two
@@ -137,15 +132,10 @@ __device__ __forceinline__ void place_key(uint32_t (&keys)[VM], uint32_t (&rem)[
 // which can only let a later masked step see a bin as fitting -- and every bin fits for them).
 template <int N, int VM>
 __device__ __forceinline__ uint32_t min_keys(const uint32_t (&keys)[VM]) {
-  constexpr int P = pow2_ceil(N);
-  uint32_t m[P];
+  uint32_t m[N];
 #pragma unroll
-  for (int b = 0; b < P; ++b) m[b] = b < N ? keys[b] : 0xFFFFFFFFu;
-#pragma unroll
-  for (int w = P / 2; w > 0; w >>= 1)
-#pragma unroll
-    for (int b = 0; b < w; ++b) m[b] = min(m[b], m[b + w]);
-  return m[0];
+  for (int b = 0; b < N; ++b) m[b] = keys[b];
+  return min_tree3<N>(m);
 }
 
 template <int N, int VM>

@@ -90,11 +90,16 @@ __device__ __forceinline__ bool run_keys(const uint32_t* __restrict__ mw, int nw
       KT m[N];
 #pragma unroll
       for (int b = 0; b < N; ++b) m[b] = keys[b] | ((KT)((rem[b] - l) >> 31) << HB);
+      KT mk;
+      if constexpr (sizeof(KT) == 4) {
+        mk = min_tree3<N>(m);
+      } else {
 #pragma unroll
-      for (int wd = N / 2; wd > 0; wd >>= 1)
+        for (int wd = N / 2; wd > 0; wd >>= 1)
 #pragma unroll
-        for (int b = 0; b < wd; ++b) m[b] = min(m[b], m[b + wd]);
-      const KT mk = m[0];
+          for (int b = 0; b < wd; ++b) m[b] = min(m[b], m[b + wd]);
+        mk = m[0];
+      }
       ev += V;
       if (mk >> HB) return false;
       const KT add = (KT)tau << 4;
