@@ -15,7 +15,8 @@
 // (one LDS/STS per sequence); U_j and tau_max,j from the membership bitmap words, which are
 // flushed every 32 sequences.
 // A per-CTA bound on every load picks the arithmetic: packed u32 keys (packed_run, MODE 0
-// kernel) when loads < 2^(31 - log2 DP), else u32 or u64 sums (dispatch_run, MODE 1 kernel).
+// kernel) when loads < 2^(31 - log2 DP), else u32 sums (dispatch_run, MODE 1 kernel) when loads
+// < 2^32, else u64 sums (MODE 2 kernel) -- three kernels so each carries only its own registers.
 // Outputs: pipe[c][t][i] (4 decisions per u32 store), lb[c][t] = max_j base_j, stats.
 #include "hyd_internal.cuh"
 
@@ -370,12 +371,12 @@ int launch_iter_bound(const uint32_t* cost, int n_iter, int batch, const uint32_
   return e == cudaSuccess ? HYD_OK : record_cuda_error(e);
 }
 
-// MODE 0: CTAs whose load bound admits packed keys; MODE 1: the others (u32 / u64 sums).  Both
+// MODE 0: CTAs whose load bound admits packed keys; MODE 1: u32 sums; MODE 2: u64 sums.  All
 // kernels are launched; each reads the same per-iteration bounds and leaves the other's CTAs
 // alone (before staging anything), so the common packed case runs with the packed kernel's
 // smaller register footprint.
 template <int DP, bool STAGED, int MODE>
-__global__ void __launch_bounds__(kDispatchThreads, (MODE == 0 && DP == 8) ? 5 : 1)
+__global__ void __launch_bounds__(kDispatchThreads, (MODE == 0 && DP == 8) ? 5 : MODE == 1 ? 3 : 1)
     k_dispatch(const uint32_t* __restrict__ sorted_len, const uint32_t* __restrict__ cost,
                int n_iter, int batch, const uint32_t* __restrict__ off, size_t n_total, int k_pad,
                const hyd_scheme* __restrict__ schemes,
@@ -402,7 +403,7 @@ __global__ void __launch_bounds__(kDispatchThreads, (MODE == 0 && DP == 8) ? 5 :
   const bool narrow = bound < 0xFFFFFFFFull;
   constexpr int SHK = DP <= 2 ? 1 : DP <= 4 ? 2 : DP <= 8 ? 3 : DP <= 16 ? 4 : 5;
   const bool packed = bound < (1ull << (31 - SHK));  // keys (load << SHK | j) stay below 2^31
-  if ((MODE == 0) != packed) return;  // the other kernel owns this CTA
+  if (MODE != (packed ? 0 : narrow ? 1 : 2)) return;  // another kernel owns this CTA
   const size_t base0 = geo_base(off, batch, t0);  // first row of the CTA's iterations
   if (STAGED && off) {  // ragged: rows need not be 16-byte aligned
     for (int e = tid; e < B; e += kDispatchThreads) sm[e] = __ldg(sorted_len + base0 + e);
@@ -490,44 +491,43 @@ __global__ void __launch_bounds__(kDispatchThreads, (MODE == 0 && DP == 8) ? 5 :
   uint32_t* mbits = members + srow * max_np * nwords;  // word w of pipeline j at [w * max_np + j]
   unsigned long long* ssum = s_sum + tid;
   uint64_t lbv = 0ull;
-  uint64_t base64[DP];
   uint32_t cf[DP];
+  hyd_pipe_stats* st = stats + srow * max_np;
+  auto write_stats = [&](const auto& base) {
+    lb[row] = lbv;
+#pragma unroll
+    for (int j = 0; j < DP; ++j) {
+      if (j < np) {
+        const uint32_t first = cf[j] & 0xFFFFu;  // 0: no member
+        const uint32_t tm = !first ? 0u
+                            : TRANS ? sm[(size_t)tt * B + ((size_t)lt * k_pad + kk[j]) * Bp + first - 1u]
+                                    : cs[(size_t)(first - 1u) * k_pad + kk[j]];
+        hyd_pipe_stats e;
+        e.u = cf[j] >> 16;
+        e.tau_max = tm;
+        e.s = ssum[j * kDispatchThreads];
+        e.sum_t = (uint64_t)base[j] - (uint64_t)tm * (pp[j] - 1u);  // base_j = C_j + E_j
+        st[j] = e;
+      }
+    }
+  };
   if constexpr (MODE == 0) {
     const unsigned amask = __activemask();
     const uint32_t* cst = TRANS ? sm + (size_t)tt * B + (size_t)lt * k_pad * Bp : cs;
     uint32_t base[DP];
     packed_run<DP, TRANS>(sl, cst, B, TRANS ? Bp : k_pad, ml, pp, kk, prow, ssum, mbits, np, max_np,
                           lbv, base, cf, amask);
-#pragma unroll
-    for (int j = 0; j < DP; ++j) base64[j] = base[j];
+    write_stats(base);
+  } else if constexpr (MODE == 1) {
+    uint32_t base[DP];
+    dispatch_run<DP, uint32_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, ssum, mbits, np, max_np, lbv, base,
+                               cf);
+    write_stats(base);
   } else {
-    if (narrow) {
-      uint32_t base[DP];
-      dispatch_run<DP, uint32_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, ssum, mbits, np,
-                                        max_np, lbv, base, cf);
-#pragma unroll
-      for (int j = 0; j < DP; ++j) base64[j] = base[j];
-    } else {
-      dispatch_run<DP, uint64_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, ssum, mbits, np,
-                                        max_np, lbv, base64, cf);
-    }
-  }
-  lb[row] = lbv;
-  hyd_pipe_stats* st = stats + srow * max_np;
-#pragma unroll
-  for (int j = 0; j < DP; ++j) {
-    if (j < np) {
-      const uint32_t first = cf[j] & 0xFFFFu;  // 0: no member
-      const uint32_t tm = !first ? 0u
-                          : TRANS ? sm[(size_t)tt * B + ((size_t)lt * k_pad + kk[j]) * Bp + first - 1u]
-                                  : cs[(size_t)(first - 1u) * k_pad + kk[j]];
-      hyd_pipe_stats e;
-      e.u = cf[j] >> 16;
-      e.tau_max = tm;
-      e.s = ssum[j * kDispatchThreads];
-      e.sum_t = base64[j] - (uint64_t)tm * (pp[j] - 1u);  // base_j = C_j + E_j
-      st[j] = e;
-    }
+    uint64_t base[DP];
+    dispatch_run<DP, uint64_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, ssum, mbits, np, max_np, lbv, base,
+                               cf);
+    write_stats(base);
   }
 }
 
@@ -560,15 +560,20 @@ static cudaError_t launch_dp(bool staged, dim3 grid, size_t smem_stage, cudaStre
   const size_t cols = (size_t)DP * kDispatchThreads * 8;
   const size_t smem = staged ? ((smem_stage + 15) & ~(size_t)15) + cols : cols;
   cudaError_t e;
+#define HYD_LAUNCH_MODE(ST, MD)                                                                            \
+  launch_mode<DP, ST, MD>(grid, smem, s, sorted_len, cost, n_iter, batch, off, n_total, k_pad, schemes,   \
+                          n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, \
+                          bounds)
   if (staged) {
-    e = launch_mode<DP, true, 0>(grid, smem, s, sorted_len, cost, n_iter, batch, off, n_total, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds);
-    if (e == cudaSuccess)
-      e = launch_mode<DP, true, 1>(grid, smem, s, sorted_len, cost, n_iter, batch, off, n_total, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds);
+    e = HYD_LAUNCH_MODE(true, 0);
+    if (e == cudaSuccess) e = HYD_LAUNCH_MODE(true, 1);
+    if (e == cudaSuccess) e = HYD_LAUNCH_MODE(true, 2);
   } else {
-    e = launch_mode<DP, false, 0>(grid, smem, s, sorted_len, cost, n_iter, batch, off, n_total, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds);
-    if (e == cudaSuccess)
-      e = launch_mode<DP, false, 1>(grid, smem, s, sorted_len, cost, n_iter, batch, off, n_total, k_pad, schemes, n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, bounds);
+    e = HYD_LAUNCH_MODE(false, 0);
+    if (e == cudaSuccess) e = HYD_LAUNCH_MODE(false, 1);
+    if (e == cudaSuccess) e = HYD_LAUNCH_MODE(false, 2);
   }
+#undef HYD_LAUNCH_MODE
   return e;
 }
 
