@@ -63,6 +63,18 @@ def test_host_validation_is_synchronous(hyd):
     assert L.hyd_dispatch_alg1(P, P, 1, 16, 4, P, 1, P, P, 1, 2, 0, P, P, P, P, P, P, P, P, 4096, None) == -1
     assert L.hyd_dispatch_alg1(P, P, 1, 16, 4, P, 1, P, P, 1, 2, 4, P, P, P, P, P, P, P, None, 0, None) == -6
     assert L.hyd_alg1_workspace(1024) >= 1024 * 8
+    # iterations map to a grid dimension: n_iter <= HYD_MAX_ITER (65535)
+    assert L.hyd_cost_table(P, 65536, 16, P, 1, 4, P, P, P, P, None) == -1
+    assert L.hyd_select_best(P, 65536, 10, 0, P, P, None) == -1
+    # the fused small-batch kernel: batch <= 128, <= 16 pipelines, workspace
+    Z = L.hyd_dispatch_pack_workspace()
+    assert L.hyd_dispatch_pack(P, P, 1, 129, 4, P, 1, P, P, 1, 2, P, P, P, P, P, P, P, P, Z, None) == -1
+    assert L.hyd_dispatch_pack(P, P, 1, 64, 4, P, 1, P, P, 1, 17, P, P, P, P, P, P, P, P, Z, None) == -1
+    assert L.hyd_dispatch_pack(P, P, 1, 64, 4, P, 1, P, P, 1, 8, P, P, P, P, P, P, P, None, 0, None) == -6
+    # hyd_pipe_index / hyd_dp_candidates argument checks
+    assert L.hyd_pipe_index(P, P, 1, 16, 4, P, 1, P, P, 1, 33, P, P, P, P, P, None) == -1
+    assert L.hyd_pipe_index(P, P, 1, 16, 4, P, 1, P, P, 1, 2, None, P, P, P, P, None) == -1
+    assert L.hyd_dp_candidates(P, P, 0, P, 1, P, P, P, None) == -1
 
 
 def test_workspace_sizes(hyd):
