@@ -8,8 +8,7 @@
 //   * dispatch (HYD-H1; Eq. 2/3 P:634-650, Alg. 1's rule P:1131-1144):
 //     base_j = C_j + E_j and mult_j = PP_j while pipeline j is empty, 1 after, so a candidate
 //     load is one multiply-add, new_j = base_j + tau mult_j; j* = argmin (new_j, j) over
-//     MaxLen_j >= l (J_i); packed u32 keys (k_dispatch's MODE 0) or u32 sums when a
-//     per-CTA bound on every load allows, else u64;
+//     MaxLen_j >= l (J_i); u32 arithmetic when a per-CTA bound on every load allows;
 //     decisions go straight to the pipe row and to per-pipeline membership words in shared
 //     memory, token sums S_j and base_j to a per-thread shared record;
 //   * pack (Eq. 1 P:604-607 over App. D's range P:1097): per pipeline the exact pruned V search
@@ -222,87 +221,6 @@ __device__ __forceinline__ void small_dispatch(const uint32_t* __restrict__ sl, 
   lb_out = m;
 }
 
-// The same dispatch with packed keys (when every load of the iteration is below 2^(31 - SH) - 1,
-// SH = log2 DP; k_dispatch's MODE 0): key_j = (C_j + E_j) << SH | j, a candidate is one
-// multiply-add, new_j = key_j + tau mult_j (mult_j = PP_j << SH while j is empty, 1 << SH after),
-// the argmin is a ternary min tree that also yields j*, and the winner's new key is the minimum.
-// Feasibility (MaxLen_j >= l, a suffix of the canonical order that shrinks as the sorted lengths
-// fall) is bit 31 of the key, released when l drops to MaxLen_j.
-template <int DP>
-__device__ __forceinline__ void small_dispatch_packed(const uint32_t* __restrict__ sl,
-                                                      const uint32_t* __restrict__ sc, int B, int kp, int np,
-                                                      const uint32_t (&ml)[DP], const uint32_t (&pp)[DP],
-                                                      const uint32_t (&kk)[DP], uint32_t* __restrict__ mem,
-                                                      const PipeRec& rec, uint8_t* __restrict__ prow,
-                                                      uint64_t& lb_out) {
-  constexpr int SH = DP <= 2 ? 1 : DP <= 4 ? 2 : DP <= 8 ? 3 : DP <= 16 ? 4 : 5;
-  const uint32_t one = 1u << SH;
-  uint32_t key[DP], mult[DP], S[DP];
-  uint32_t pend = 0u;  // largest MaxLen among still-infeasible pipelines (0: none)
-  const uint32_t l0 = sl[0];
-#pragma unroll
-  for (int j = 0; j < DP; ++j) {
-    const bool used = j < np, feas = used && ml[j] >= l0;
-    key[j] = !used ? 0x7FFFFFFFu : feas ? (uint32_t)j : (0x80000000u | (uint32_t)j);
-    mult[j] = used ? pp[j] << SH : 0u;
-    if (used && !feas) pend = max(pend, ml[j]);
-    S[j] = 0u;
-  }
-  const bool words = ((size_t)prow & 3) == 0;
-  uint32_t word = 0u;
-  for (int i = 0; i < B; ++i) {
-    const uint32_t l = sl[i];
-    if (l <= pend) {  // rare: pipelines become feasible as l drops to their MaxLen
-      uint32_t p2 = 0u;
-#pragma unroll
-      for (int j = 0; j < DP; ++j)
-        if (j < np && (key[j] >> 31) != 0u) {
-          if (ml[j] >= l) key[j] &= 0x7FFFFFFFu;
-          else p2 = max(p2, ml[j]);
-        }
-      pend = p2;
-    }
-    const uint32_t* crow = sc + i * kp;
-    uint32_t m[DP];
-#pragma unroll
-    for (int j = 0; j < DP; ++j) m[j] = crow[kk[j]] * mult[j] + key[j];
-    const uint32_t mk = min_tree3<DP>(m);
-    const uint32_t bj = mk & (uint32_t)(DP - 1);
-#pragma unroll
-    for (int j = 0; j < DP; ++j) {
-      const bool hit = (uint32_t)j == bj;
-      key[j] = hit ? mk : key[j];
-      mult[j] = hit ? one : mult[j];
-      S[j] += hit ? l : 0u;
-    }
-    HYD_CHECK(bj < (uint32_t)np && i < HYD_SMALL_MAX_BATCH);
-    mem[bj * kSmallWords + (i >> 5)] |= 1u << (i & 31);
-    if (words) {
-      word |= bj << (8 * (i & 3));
-      if ((i & 3) == 3 || i == B - 1) {
-        if ((i & 3) == 3) {
-          *reinterpret_cast<uint32_t*>(prow + (i & ~3)) = word;
-        } else {
-          for (int q = i & ~3; q <= i; ++q) prow[q] = (uint8_t)(word >> (8 * (q & 3)));
-        }
-        word = 0u;
-      }
-    } else {
-      prow[i] = (uint8_t)bj;
-    }
-  }
-  uint64_t mx = 0ull;
-#pragma unroll
-  for (int j = 0; j < DP; ++j)
-    if (j < np) {
-      const uint32_t base = key[j] >> SH;
-      mx = max(mx, (uint64_t)base);
-      rec.s(j) = S[j];
-      rec.b(j) = (unsigned long long)base;
-    }
-  lb_out = mx;
-}
-
 template <int DP>
 __global__ void __launch_bounds__(kSmallThreads) k_assign_small(SmallArgs a) {
   extern __shared__ __align__(16) uint32_t sm[];
@@ -355,8 +273,6 @@ __global__ void __launch_bounds__(kSmallThreads) k_assign_small(SmallArgs a) {
   }
   __syncthreads();
   const bool narrow = s_sum + s_max < 0xFFFFFFFFull;
-  constexpr int SHK = DP <= 2 ? 1 : DP <= 4 ? 2 : DP <= 8 ? 3 : DP <= 16 ? 4 : 5;
-  const bool packed = s_sum + s_max < (1ull << (31 - SHK)) - 1ull;  // keys (load << SHK | j) < 2^31 - 1
 
   const bool active = c < a.n_cand;
   int np = 0;
@@ -393,8 +309,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_assign_small(SmallArgs a) {
   uint8_t* prow = a.pipe + (size_t)c * a.n_total + tbase;
   if (feasible) {
     uint64_t lbv;
-    if (packed) small_dispatch_packed<DP>(sl, sc, B, kp, np, ml, pp, kk, mem, rec, prow, lbv);
-    else if (narrow) small_dispatch<DP, uint32_t>(sl, sc, B, kp, np, ml, pp, kk, mem, rec, prow, lbv);
+    if (narrow) small_dispatch<DP, uint32_t>(sl, sc, B, kp, np, ml, pp, kk, mem, rec, prow, lbv);
     else small_dispatch<DP, uint64_t>(sl, sc, B, kp, np, ml, pp, kk, mem, rec, prow, lbv);
     a.lb[row] = lbv;
   } else if (active) {
