@@ -18,6 +18,8 @@
 // kernel) when loads < 2^(31 - log2 DP), else u32 sums (dispatch_run, MODE 1 kernel) when loads
 // < 2^32, else u64 sums (MODE 2 kernel) -- three kernels so each carries only its own registers.
 // Outputs: pipe[c][t][i] (4 decisions per u32 store), lb[c][t] = max_j base_j, stats.
+#include <type_traits>
+
 #include "hyd_internal.cuh"
 
 namespace hyd {
@@ -117,6 +119,96 @@ __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
       prow[i] = (uint8_t)bj;
     }
   }
+  s_sum[pbj * kDispatchThreads] += pl;  // the last decision's S_j
+  uint64_t m = 0ull;
+#pragma unroll
+  for (int j = 0; j < DP; ++j)
+    if (j < np) m = max(m, (uint64_t)base[j]);
+  lb_out = m;
+}
+
+// dispatch_run for iterations too long to stage whole (config 5: 8192 sequences x 20 schemes):
+// the CTA's threads (one iteration, tt = 1) copy windows of kDispatchWin sequences' lengths and
+// cost rows into shared memory together, then each live thread runs its steps from there, so
+// every cost read is a shared-memory load instead of an L2 round trip.  All threads of the CTA
+// take part in the copies and barriers; `live` threads (a feasible candidate) also decide.
+constexpr int kDispatchWin = 512;
+
+template <int DP, typename TT>
+__device__ __forceinline__ void dispatch_run_win(bool live, const uint32_t* __restrict__ g_sl,
+                                                 const uint32_t* __restrict__ g_cs, uint32_t* __restrict__ wsm,
+                                                 int B, int k_pad, const uint32_t (&ml)[DP],
+                                                 const uint32_t (&pp)[DP], const uint32_t (&kk)[DP],
+                                                 uint8_t* __restrict__ prow, unsigned long long* s_sum,
+                                                 uint32_t* __restrict__ mbits, int np, int mstride,
+                                                 uint64_t& lb_out, TT (&base)[DP], uint32_t (&cf)[DP]) {
+  const int tid = threadIdx.x;
+  uint32_t mult[DP], bits[DP];
+  uint32_t ml_min = 0xFFFFFFFFu;
+#pragma unroll
+  for (int j = 0; j < DP; ++j) {  // unused slots: base = max, mult = 0 -> never strictly best
+    base[j] = j < np ? (TT)0 : (TT)~(TT)0;
+    mult[j] = j < np ? pp[j] : 0u;
+    bits[j] = 0u;
+    cf[j] = 0u;
+    if (j < np) ml_min = min(ml_min, ml[j]);
+  }
+  const bool words = (B & 3) == 0 && ((size_t)prow & 3) == 0;
+  uint32_t word = 0u;
+  uint32_t pbj = 0u, pl = 0u;  // S_j one step late (as in packed_step)
+  uint32_t* wl = wsm;                 // [kDispatchWin] lengths
+  uint32_t* wc = wsm + kDispatchWin;  // [kDispatchWin][k_pad] cost rows
+  const bool vec = (((size_t)g_cs & 15) == 0) && (k_pad & 3) == 0;
+  for (int w0 = 0; w0 < B; w0 += kDispatchWin) {
+    const int n = min(kDispatchWin, B - w0);
+    __syncthreads();  // the previous window is consumed
+    for (int e = tid; e < n; e += kDispatchThreads) wl[e] = __ldg(g_sl + w0 + e);
+    if (vec) {
+      const uint4* src = reinterpret_cast<const uint4*>(g_cs + (size_t)w0 * k_pad);
+      uint4* dst = reinterpret_cast<uint4*>(wc);
+      for (int e = tid; e < n * k_pad / 4; e += kDispatchThreads) dst[e] = __ldg(src + e);
+    } else {
+      for (int e = tid; e < n * k_pad; e += kDispatchThreads) wc[e] = __ldg(g_cs + (size_t)w0 * k_pad + e);
+    }
+    __syncthreads();
+    if (!live) continue;
+    for (int q = 0; q < n; ++q) {
+      const int i = w0 + q;
+      const unsigned long long sold = s_sum[pbj * kDispatchThreads];
+      const uint32_t l = wl[q];
+      const uint32_t* crow = wc + q * k_pad;
+      const uint32_t bit = 1u << (i & 31);
+      const uint32_t bj =
+          l > ml_min ? dispatch_step<DP, TT, true>(l, crow, true, ml, kk, base, mult, bits, bit)
+                     : dispatch_step<DP, TT, false>(l, crow, true, ml, kk, base, mult, bits, bit);
+      s_sum[pbj * kDispatchThreads] = sold + pl;  // S_j column of this thread
+      pbj = bj;
+      pl = l;
+      if ((i & 31) == 31 || i == B - 1) {  // flush one membership word per pipeline
+        const uint32_t wb = (uint32_t)(i & ~31);
+#pragma unroll
+        for (int j = 0; j < DP; ++j) {
+          if (j < np) {
+            HYD_CHECK(j < mstride);
+            mbits[(size_t)(i >> 5) * mstride + j] = bits[j];
+            const uint32_t f = (cf[j] & 0xFFFFu) == 0u && bits[j] != 0u ? wb + __ffs(bits[j]) : 0u;
+            cf[j] += (__popc(bits[j]) << 16) + f;
+          }
+          bits[j] = 0u;
+        }
+      }
+      if (words) {
+        word |= bj << (8 * (i & 3));
+        if ((i & 3) == 3) {
+          *reinterpret_cast<uint32_t*>(prow + (i & ~3)) = word;
+          word = 0u;
+        }
+      } else {
+        prow[i] = (uint8_t)bj;
+      }
+    }
+  }
+  if (!live) return;
   s_sum[pbj * kDispatchThreads] += pl;  // the last decision's S_j
   uint64_t m = 0ull;
 #pragma unroll
@@ -389,10 +481,13 @@ __global__ void __launch_bounds__(kDispatchThreads, (MODE == 0 && DP == 8) ? 5 :
   // dynamic smem: [stage if STAGED] [s_sum u64 columns]; stage = [tt][B] lengths, then the
   // costs: MODE 1 as global rows [tt][B][k_pad]; MODE 0 transposed [tt][k_pad][Bp], Bp = B | 1
   constexpr bool TRANS = STAGED && MODE == 0;
+  // general sums on an iteration too long to stage: window staging (one iteration per CTA)
+  constexpr bool WIN = !STAGED && MODE != 0;
   // ragged batches (off != nullptr) run with tt = 1: B = this iteration's sequences
   const int B = off ? geo_bt(off, batch, blockIdx.y) : batch;
   const int Bp = B | 1;
-  const size_t stage_words = STAGED ? dispatch_stage_words(tt, batch, k_pad) : 0;
+  const size_t stage_words =
+      STAGED ? dispatch_stage_words(tt, batch, k_pad) : WIN ? (size_t)kDispatchWin * (1 + k_pad) : 0;
   unsigned long long* s_sum = reinterpret_cast<unsigned long long*>(sm + ((stage_words + 3) & ~(size_t)3));
   const int tid = threadIdx.x;
   const int c0 = blockIdx.x * ct, t0 = blockIdx.y * tt;
@@ -444,7 +539,10 @@ __global__ void __launch_bounds__(kDispatchThreads, (MODE == 0 && DP == 8) ? 5 :
 
   const int lt = tid / ct, lc = tid - lt * ct;
   const int c = c0 + lc, t = t0 + lt;
-  if (lt >= tt || c >= n_cand || t >= n_iter || B == 0) return;
+  // (WIN: every thread stays for the CTA's window copies; tt == 1 there)
+  const bool active = !(lt >= tt || c >= n_cand || t >= n_iter || B == 0);
+  if (!WIN && !active) return;
+  if (WIN && (B == 0 || t0 >= n_iter)) return;  // CTA-uniform
 
   const size_t tbase = geo_base(off, batch, t);
   const uint32_t* sl = STAGED ? sm + (size_t)lt * B : sorted_len + tbase;
@@ -453,7 +551,7 @@ __global__ void __launch_bounds__(kDispatchThreads, (MODE == 0 && DP == 8) ? 5 :
   uint8_t* prow = pipe + (size_t)c * n_total + tbase;  // = row * B for uniform batches
 
   // candidate: pipelines in canonical order; unused lanes get MaxLen 0 (never feasible)
-  const int np = cand_np[c];
+  const int np = active ? cand_np[c] : 0;
   uint32_t ml[DP], pp[DP], kk[DP];
   bool ok = np >= 1 && np <= DP;
   uint32_t prev_ml = 0xFFFFFFFFu, prev_k = 0;
@@ -479,14 +577,15 @@ __global__ void __launch_bounds__(kDispatchThreads, (MODE == 0 && DP == 8) ? 5 :
       }
     }
   }
-  if (!ok) flag(status, HYD_F_NOT_CANONICAL);
+  if (active && !ok) flag(status, HYD_F_NOT_CANONICAL);
   const size_t srow = (size_t)t * n_cand + c;  // iteration-major stats / members row
-  if (!ok || sl[0] > ml[0]) {  // infeasible candidate for this iteration
+  const bool live = active && ok && sl[0] <= ml[0];
+  if (active && !live) {  // infeasible candidate for this iteration
     for (int i = 0; i < B; ++i) prow[i] = 0xFF;
     lb[row] = ~0ull;
     stats[srow * max_np].u = 0xFFFFFFFFu;
-    return;
   }
+  if (!WIN && !live) return;
   const int nwords = (batch + 31) >> 5;  // row stride: words of the largest batch
   uint32_t* mbits = members + srow * max_np * nwords;  // word w of pipeline j at [w * max_np + j]
   unsigned long long* ssum = s_sum + tid;
@@ -518,6 +617,13 @@ __global__ void __launch_bounds__(kDispatchThreads, (MODE == 0 && DP == 8) ? 5 :
     packed_run<DP, TRANS>(sl, cst, B, TRANS ? Bp : k_pad, ml, pp, kk, prow, ssum, mbits, np, max_np,
                           lbv, base, cf, amask);
     write_stats(base);
+  } else if constexpr (WIN) {
+    using TT = typename std::conditional<MODE == 1, uint32_t, uint64_t>::type;
+    TT base[DP];
+    // the CTA's iteration t0 (threads past n_cand have lt >= 1 and point elsewhere): windows of it
+    dispatch_run_win<DP, TT>(live, sorted_len + base0, cost + base0 * k_pad, sm, B, k_pad, ml, pp, kk, prow, ssum,
+                             mbits, np, max_np, lbv, base, cf);
+    if (live) write_stats(base);
   } else if constexpr (MODE == 1) {
     uint32_t base[DP];
     dispatch_run<DP, uint32_t>(sl, cs, STAGED, B, k_pad, ml, pp, kk, prow, ssum, mbits, np, max_np, lbv, base,
@@ -558,10 +664,11 @@ static cudaError_t launch_dp(bool staged, dim3 grid, size_t smem_stage, cudaStre
                              int ct, int tt, uint8_t* pipe, uint64_t* lb, hyd_pipe_stats* stats,
                              uint32_t* members, uint32_t* status, const uint64_t* bounds) {
   const size_t cols = (size_t)DP * kDispatchThreads * 8;
-  const size_t smem = staged ? ((smem_stage + 15) & ~(size_t)15) + cols : cols;
+  const size_t win = (((size_t)kDispatchWin * (1 + k_pad) * 4 + 15) & ~(size_t)15) + cols;  // MODE 1/2, not staged
   cudaError_t e;
 #define HYD_LAUNCH_MODE(ST, MD)                                                                            \
-  launch_mode<DP, ST, MD>(grid, smem, s, sorted_len, cost, n_iter, batch, off, n_total, k_pad, schemes,   \
+  launch_mode<DP, ST, MD>(grid, ST ? ((smem_stage + 15) & ~(size_t)15) + cols : MD ? win : cols, s,      \
+                          sorted_len, cost, n_iter, batch, off, n_total, k_pad, schemes,                  \
                           n_schemes, cand, cand_np, n_cand, max_np, ct, tt, pipe, lb, stats, members, status, \
                           bounds)
   if (staged) {
@@ -589,12 +696,13 @@ int launch_dispatch(const uint32_t* sorted_len, const uint32_t* cost, int n_iter
   const int rb = launch_iter_bound(cost, n_iter, batch, off, k_pad, schemes, n_schemes, bounds, s);
   if (rb != HYD_OK) return rb;
   const int ct = n_cand < kDispatchThreads ? n_cand : kDispatchThreads;
-  const int tt = off ? 1 : kDispatchThreads / ct;  // ragged batches: one iteration per CTA
+  int tt = off ? 1 : kDispatchThreads / ct;  // ragged batches: one iteration per CTA
   const size_t smem = dispatch_stage_words(tt, batch, k_pad) * 4;
   const int dp = max_np <= 2 ? 2 : max_np <= 4 ? 4 : max_np <= 8 ? 8 : max_np <= 16 ? 16 : 32;
   const size_t static_smem = (size_t)dp * kDispatchThreads * 8 + 64;
   // stage when the rows fit comfortably (leaves room for several CTAs per SM)
   const bool staged = smem + static_smem <= 96 * 1024 && (off || (batch % 4) == 0);
+  if (!staged) tt = 1;  // the window-staged general kernels take one iteration per CTA
   dim3 grid((n_cand + ct - 1) / ct, (n_iter + tt - 1) / tt);
   cudaError_t e;
   switch (dp) {
