@@ -1108,6 +1108,58 @@ __device__ __forceinline__ bool lpt_warp_packed(const uint32_t* __restrict__ mw,
   return true;
 }
 
+// LPT(V <= 32 R) with packed keys over R bins per lane (b = lane + 32 r): key = time << S | b,
+// S = 5 + log2 R, bins that cannot take the sequence masked to 0xFFFFFFFF by a select (so keys
+// use all 32 bits: sum T < 2^(32 - S) - 1); per sequence one lane-local min, ONE redux.sync and a
+// compare-and-add per bin -- the same rule and result as lpt_warp (least-time fitting bin,
+// smallest index), with one warp reduction in the dependent chain instead of two.
+template <int R>
+__device__ __forceinline__ bool lpt_warp_packed_r(const uint32_t* __restrict__ mw, uint32_t nwords, uint32_t mstride,
+                                                  uint32_t V, uint32_t M, const uint32_t* __restrict__ sl,
+                                                  const uint32_t* __restrict__ cs, int kp, uint32_t k, uint64_t thr64,
+                                                  bool write, uint16_t* __restrict__ mrow, uint64_t& maxbin,
+                                                  uint64_t& evals) {
+  constexpr int S = R == 1 ? 5 : R == 2 ? 6 : 7;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t thr = thr64 > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)thr64;
+  uint32_t key[R], rem[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t b = lane + 32u * r;
+    key[r] = b < V ? b : 0xFFFFFFFFu;  // unused bins are always masked
+    rem[r] = M;                        // MaxLen - tokens of bin b
+  }
+  uint32_t mx = 0;
+  MemberStream ms;
+  ms_open(ms, mw, nwords, mstride);
+  uint32_t cidx = 0, cl = 0, ctau = 0, n;
+  while ((n = ms_next32(ms, sl, cs, kp, k, cidx, cl, ctau)) != 0) {
+    for (uint32_t q = 0; q < n; ++q) {
+      const uint32_t l = __shfl_sync(HYD_FULL, cl, q);
+      const uint32_t tau = __shfl_sync(HYD_FULL, ctau, q);
+      const uint32_t iq = __shfl_sync(HYD_FULL, cidx, q);
+      uint32_t mk = 0xFFFFFFFFu;
+#pragma unroll
+      for (int r = 0; r < R; ++r) mk = min(mk, rem[r] >= l ? key[r] : 0xFFFFFFFFu);
+      const uint32_t m = __reduce_min_sync(HYD_FULL, mk);
+      evals += V;
+      if (m == 0xFFFFFFFFu) return false;  // no bin fits
+      const uint32_t add = tau << S;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const bool h = key[r] == m;
+        key[r] = h ? key[r] + add : key[r];
+        rem[r] = h ? rem[r] - l : rem[r];
+      }
+      if (write && (m & 31u) == lane) mrow[iq] = (uint16_t)(m & ((1u << S) - 1u));
+      mx = max(mx, (m >> S) + tau);
+      if (mx > thr) return false;
+    }
+  }
+  maxbin = mx;
+  return true;
+}
+
 template <typename TT>
 __device__ __forceinline__ bool lpt_warp_dispatch(const uint32_t* mw, uint32_t nwords, uint32_t mstride, uint32_t V,
                                                   uint32_t M, const uint32_t* sl, const uint32_t* cs,
@@ -1160,15 +1212,25 @@ __global__ void __launch_bounds__(256) k_pack_big(PackArgs a) {
       search_init(s);
       const bool narrow = s.sumT < 0xFFFFFFFFull;
       const bool packed = s.sumT < (1ull << 26) && s.M < 0x80000000u;  // lpt_warp_packed's keys
+      // the select-masked packed keys of lpt_warp_packed_r: V <= 64 with sum T < 2^26 - 1, V <= 128
+      // with sum T < 2^25 - 1
+      const bool packed2 = s.sumT < (1ull << 26) - 1ull, packed4 = s.sumT < (1ull << 25) - 1ull;
       uint32_t V, wV = 0;
       bool first = true;
       while ((V = search_next(s)) != 0) {
         const uint64_t thr = first ? ~0ull : search_thr_approx(s, V);
         uint64_t mx = 0;
-        const bool ok = (packed && V <= 32u)
-                            ? lpt_warp_packed(mw, nwords_t, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, ev)
-                        : narrow ? lpt_warp_dispatch<uint32_t>(mw, nwords_t, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, scr_t, scr_k, ev)
-                               : lpt_warp_dispatch<uint64_t>(mw, nwords_t, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, scr_t, scr_k, ev);
+        bool ok;
+        if (packed && V <= 32u)
+          ok = lpt_warp_packed(mw, nwords_t, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, ev);
+        else if (packed2 && V <= 64u)
+          ok = lpt_warp_packed_r<2>(mw, nwords_t, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, ev);
+        else if (packed4 && V <= 128u)
+          ok = lpt_warp_packed_r<4>(mw, nwords_t, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, ev);
+        else if (narrow)
+          ok = lpt_warp_dispatch<uint32_t>(mw, nwords_t, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, scr_t, scr_k, ev);
+        else
+          ok = lpt_warp_dispatch<uint64_t>(mw, nwords_t, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, scr_t, scr_k, ev);
         if (ok && first) wV = V;
         first = false;
         if (ok && search_improves(s, V, mx)) search_take(s, V, mx);
@@ -1177,6 +1239,10 @@ __global__ void __launch_bounds__(256) k_pack_big(PackArgs a) {
         uint64_t mx = 0;
         if (packed && s.vbest <= 32u)
           lpt_warp_packed(mw, nwords_t, (uint32_t)a.mnp, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, ev);
+        else if (packed2 && s.vbest <= 64u)
+          lpt_warp_packed_r<2>(mw, nwords_t, (uint32_t)a.mnp, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, ev);
+        else if (packed4 && s.vbest <= 128u)
+          lpt_warp_packed_r<4>(mw, nwords_t, (uint32_t)a.mnp, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, ev);
         else if (narrow) lpt_warp_dispatch<uint32_t>(mw, nwords_t, (uint32_t)a.mnp, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, scr_t, scr_k, ev);
         else lpt_warp_dispatch<uint64_t>(mw, nwords_t, (uint32_t)a.mnp, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, scr_t, scr_k, ev);
       }
