@@ -803,7 +803,7 @@ def roofline(name, ms, W, A, pk, how, local_ci, world=1):
             dev_ops = 6.0 * A.dispatch_evals(A._lens_host)
             ops, ops_exec = ops + dev_ops, ops_exec + dev_ops
         achieved = ops / (ms / 1000.0) / 1e9
-        traffic, src = ncu_traffic(W.cfg, ("k_pack_",))
+        traffic, src = ncu_traffic(W.cfg, ("k_assign_small",) if A.fused else ("k_pack_", "k_flag_list"))
         if world > 1:  # the committed ncu capture is of the N = 1 launch: not this shard's
             traffic, src = None, "n/a at N > 1 (ncu captures are single-GPU)"
         return {"kernel": "dispatch + pack fused (k_assign_small)" if A.fused else "pack (k_pack_lanes + k_pack_big)",
