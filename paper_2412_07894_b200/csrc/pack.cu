@@ -46,6 +46,11 @@ constexpr size_t kLaneSmem32 = 110 * 1024;  // VMAX 32 pass: 2 CTAs per SM
 constexpr int kLaneEpoch = 24;     // sequences per lane between bookkeeping phases
 constexpr int kBigRMax = 8;       // k_pack_big: register bins per lane (V <= 256)
 constexpr int kBigWarps = 3584;   // persistent warps of k_pack_big (scratch slots): 148 SMs x 24
+// A short warp queue (at most kSplitTasks pipelines) runs split: every task's reference run, then
+// its surviving V as independent units spread over all warps, then the winners' re-runs -- so the
+// queue's duration is a few runs, not its longest sequential search.
+constexpr int kSplitTasks = 16384;
+constexpr int kSplitUnits = 1 << 20;
 
 struct PackArgs {
   const uint32_t* sorted_len;
@@ -75,6 +80,9 @@ struct PackArgs {
   unsigned long long* queue;
   unsigned long long q_cap;
   uint32_t* flags;  // [It*C*mnp bits] tasks handed from the VMAX-16 to the VMAX-32 lane pass
+  unsigned long long* sp_key;  // [kSplitTasks] split warp queue: best (obj << 16 | V) per queued task
+  uint32_t* sp_wv;             // [kSplitTasks] the V whose mb the reference run wrote (0: task done in A)
+  unsigned long long* units;   // [kSplitUnits] (task << 16 | V) candidate runs of the split queue
   uint32_t* list32;   // [It][C*mnp] the flagged tasks of each iteration, compacted (c*mnp + j)
   uint32_t* count32;  // [It] their number
   uint64_t* scr_time;  // [kBigWarps][B]
@@ -1173,89 +1181,222 @@ __device__ __forceinline__ bool lpt_warp_dispatch(const uint32_t* mw, uint32_t n
   return lpt_warp<0, TT>(mw, nwords, mstride, V, M, sl, cs, kp, k, thr, write, mrow, maxbin, st, sk, ev);
 }
 
+// One queued task's geometry and search inputs (k_pack_big and its split phases).
+struct BigTask {
+  int c, t, j;
+  size_t row, srow, tbase;
+  uint32_t nwords_t, k;
+  const uint32_t *sl, *cs, *mw;
+  uint16_t* mrow;
+  Search s;
+  bool narrow, packed, packed2, packed4;
+};
+
+__device__ __forceinline__ void big_task(const PackArgs& a, unsigned long long e, BigTask& b) {
+  b.c = (int)(e >> 37);
+  b.t = (int)((e >> 5) & 0xFFFFFFFFull);
+  b.j = (int)(e & 31);
+  b.row = (size_t)b.c * a.n_iter + b.t;
+  b.srow = ((size_t)b.t * a.n_cand + b.c) * a.mnp + b.j;
+  b.tbase = geo_base(a.off, a.batch, b.t);
+  b.nwords_t = (uint32_t)((geo_bt(a.off, a.batch, b.t) + 31) >> 5);
+  b.sl = a.sorted_len + b.tbase;
+  b.cs = a.cost + b.tbase * a.k_pad;
+  b.mw = a.members + (b.srow - b.j) * a.nwords + b.j;  // word-major rows of (t, c)
+  b.k = a.cand[(size_t)b.c * HYD_MAX_PIPES + b.j];
+  const hyd_pipe_stats st = a.stats[b.srow];
+  Search& s = b.s;
+  s.M = a.schemes[b.k].max_len;
+  s.P = a.schemes[b.k].pp;
+  s.UL = a.schemes[b.k].util_len;
+  s.U = st.u;
+  s.S = st.s;
+  s.sumT = st.sum_t;
+  s.tau_max = st.tau_max;
+  b.mrow = a.mb + (size_t)b.c * a.n_total + b.tbase;
+  b.narrow = s.sumT < 0xFFFFFFFFull;
+  b.packed = s.sumT < (1ull << 26) && s.M < 0x80000000u;  // lpt_warp_packed's keys
+  // the select-masked packed keys of lpt_warp_packed_r: V <= 64 with sum T < 2^26 - 1, V <= 128
+  // with sum T < 2^25 - 1
+  b.packed2 = s.sumT < (1ull << 26) - 1ull;
+  b.packed4 = s.sumT < (1ull << 25) - 1ull;
+}
+
+// LPT(V) of the task on the fastest warp path that holds it
+__device__ __forceinline__ bool big_run(const PackArgs& a, const BigTask& b, uint32_t V, uint64_t thr, bool write,
+                                        uint64_t& mx, uint64_t* scr_t, uint32_t* scr_k, uint64_t& ev) {
+  const uint32_t mnp = (uint32_t)a.mnp, M = b.s.M;
+  const int kp = a.k_pad;
+  if (b.packed && V <= 32u)
+    return lpt_warp_packed(b.mw, b.nwords_t, mnp, V, M, b.sl, b.cs, kp, b.k, thr, write, b.mrow, mx, ev);
+  if (b.packed2 && V <= 64u)
+    return lpt_warp_packed_r<2>(b.mw, b.nwords_t, mnp, V, M, b.sl, b.cs, kp, b.k, thr, write, b.mrow, mx, ev);
+  if (b.packed4 && V <= 128u)
+    return lpt_warp_packed_r<4>(b.mw, b.nwords_t, mnp, V, M, b.sl, b.cs, kp, b.k, thr, write, b.mrow, mx, ev);
+  if (b.narrow)
+    return lpt_warp_dispatch<uint32_t>(b.mw, b.nwords_t, mnp, V, M, b.sl, b.cs, kp, b.k, thr, write, b.mrow, mx,
+                                       scr_t, scr_k, ev);
+  return lpt_warp_dispatch<uint64_t>(b.mw, b.nwords_t, mnp, V, M, b.sl, b.cs, kp, b.k, thr, write, b.mrow, mx, scr_t,
+                                     scr_k, ev);
+}
+
+__device__ __forceinline__ void big_outputs(const PackArgs& a, const BigTask& b, uint32_t vbest, uint64_t best) {
+  if ((threadIdx.x & 31) == 0) {
+    a.v[b.row * HYD_MAX_PIPES + b.j] = (uint16_t)vbest;
+    a.ptime[b.row * HYD_MAX_PIPES + b.j] = best;
+    atomicMax(reinterpret_cast<unsigned long long*>(a.makespan + (size_t)b.t * a.n_cand + b.c),
+              (unsigned long long)best);
+  }
+}
+
 // Persistent warps over the queue: one pipeline per warp, the sequential exact search
-// (V_a, ascending scan with the exact pruning, extension above the range).
-__global__ void __launch_bounds__(256) k_pack_big(PackArgs a) {
-  const int B = a.batch, kp = a.k_pad;
+// (V_a, ascending scan with the exact pruning, extension above the range).  SPLIT (a short queue,
+// k_pack_big_ref): only the reference run V_a and the enqueueing of the V that survive its exact
+// tests (k_pack_big_units runs them, k_pack_big_finish re-runs the winners); a task whose V_a is
+// infeasible, or whose units do not fit the unit queue, finishes sequentially here.  Both kernels
+// are launched; each leaves the queue to the other unless its mode applies.
+template <bool SPLIT>
+__device__ __forceinline__ void big_queue(const PackArgs& a) {
+  const int B = a.batch;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw = blockIdx.x * (blockDim.x >> 5) + warp;  // scratch slot
   uint64_t* scr_t = a.scr_time + (size_t)gw * B;
   uint32_t* scr_k = a.scr_tok + (size_t)gw * B;
   const unsigned long long total = min(*a.q_count, a.q_cap);
+  if ((total <= (unsigned long long)kSplitTasks) != SPLIT) return;
+  unsigned long long* ucount = a.q_count + 19;
   uint64_t ev = 0;
   while (true) {
     unsigned long long task = 0;
     if (lane == 0) task = atomicAdd(a.q_head, 1ull);
     task = __shfl_sync(HYD_FULL, task, 0);
     if (task >= total) break;
-    const unsigned long long e = a.queue[task];
-    const int c = (int)(e >> 37), t = (int)((e >> 5) & 0xFFFFFFFFull), j = (int)(e & 31);
-    const size_t row = (size_t)c * a.n_iter + t;
-    const size_t srow = ((size_t)t * a.n_cand + c) * a.mnp + j;
-    const size_t tbase = geo_base(a.off, a.batch, t);
-    const uint32_t nwords_t = (uint32_t)((geo_bt(a.off, a.batch, t) + 31) >> 5);
-    const uint32_t* sl = a.sorted_len + tbase;
-    const uint32_t* cs = a.cost + tbase * kp;
-    const uint32_t* mw = a.members + (srow - j) * a.nwords + j;  // word-major rows of (t, c)
-    const uint32_t k = a.cand[(size_t)c * HYD_MAX_PIPES + j];
-    const hyd_pipe_stats st = a.stats[srow];
-    Search s;
-    s.M = a.schemes[k].max_len;
-    s.P = a.schemes[k].pp;
-    s.UL = a.schemes[k].util_len;
-    s.U = st.u;
-    s.S = st.s;
-    s.sumT = st.sum_t;
-    s.tau_max = st.tau_max;
-    uint16_t* mrow = a.mb + (size_t)c * a.n_total + tbase;
-    if (s.U) {
-      search_init(s);
-      const bool narrow = s.sumT < 0xFFFFFFFFull;
-      const bool packed = s.sumT < (1ull << 26) && s.M < 0x80000000u;  // lpt_warp_packed's keys
-      // the select-masked packed keys of lpt_warp_packed_r: V <= 64 with sum T < 2^26 - 1, V <= 128
-      // with sum T < 2^25 - 1
-      const bool packed2 = s.sumT < (1ull << 26) - 1ull, packed4 = s.sumT < (1ull << 25) - 1ull;
-      uint32_t V, wV = 0;
-      bool first = true;
-      while ((V = search_next(s)) != 0) {
-        const uint64_t thr = first ? ~0ull : search_thr_approx(s, V);
-        uint64_t mx = 0;
-        bool ok;
-        if (packed && V <= 32u)
-          ok = lpt_warp_packed(mw, nwords_t, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, ev);
-        else if (packed2 && V <= 64u)
-          ok = lpt_warp_packed_r<2>(mw, nwords_t, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, ev);
-        else if (packed4 && V <= 128u)
-          ok = lpt_warp_packed_r<4>(mw, nwords_t, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, ev);
-        else if (narrow)
-          ok = lpt_warp_dispatch<uint32_t>(mw, nwords_t, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, scr_t, scr_k, ev);
-        else
-          ok = lpt_warp_dispatch<uint64_t>(mw, nwords_t, (uint32_t)a.mnp, V, s.M, sl, cs, kp, k, thr, first, mrow, mx, scr_t, scr_k, ev);
-        if (ok && first) wV = V;
-        first = false;
-        if (ok && search_improves(s, V, mx)) search_take(s, V, mx);
-      }
-      if (s.have && s.vbest != wV) {  // the winner's mb was not written by the first run
-        uint64_t mx = 0;
-        if (packed && s.vbest <= 32u)
-          lpt_warp_packed(mw, nwords_t, (uint32_t)a.mnp, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, ev);
-        else if (packed2 && s.vbest <= 64u)
-          lpt_warp_packed_r<2>(mw, nwords_t, (uint32_t)a.mnp, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, ev);
-        else if (packed4 && s.vbest <= 128u)
-          lpt_warp_packed_r<4>(mw, nwords_t, (uint32_t)a.mnp, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, ev);
-        else if (narrow) lpt_warp_dispatch<uint32_t>(mw, nwords_t, (uint32_t)a.mnp, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, scr_t, scr_k, ev);
-        else lpt_warp_dispatch<uint64_t>(mw, nwords_t, (uint32_t)a.mnp, s.vbest, s.M, sl, cs, kp, k, ~0ull, true, mrow, mx, scr_t, scr_k, ev);
-      }
-    } else {
-      s.best = 0;
-      s.vbest = 0;
+    BigTask b;
+    big_task(a, a.queue[task], b);
+    Search& s = b.s;
+    if (!s.U) {
+      if (SPLIT && lane == 0) a.sp_wv[task] = 0u;
+      big_outputs(a, b, 0u, 0ull);
+      continue;
     }
-    if (lane == 0) {
-      a.v[row * HYD_MAX_PIPES + j] = (uint16_t)s.vbest;
-      a.ptime[row * HYD_MAX_PIPES + j] = s.best;
-      atomicMax(reinterpret_cast<unsigned long long*>(a.makespan + (size_t)t * a.n_cand + c),
-                (unsigned long long)s.best);
+    search_init(s);
+    uint32_t V, wV = 0;
+    bool first = true;
+    if constexpr (SPLIT) {  // the reference run, then the surviving V as units (if they fit)
+      V = search_next(s);  // V_a
+      uint64_t mx = 0;
+      const bool ok = big_run(a, b, V, ~0ull, true, mx, scr_t, scr_k, ev);
+      first = false;
+      if (ok) {
+        wV = V;
+        search_take(s, V, mx);
+        Search q = s;  // count the units the exact tests keep
+        uint32_t n = 0;
+        while (search_next(q) != 0) ++n;
+        unsigned long long at = 0;
+        if (lane == 0) at = n ? atomicAdd(ucount, (unsigned long long)n) : 0ull;
+        at = __shfl_sync(HYD_FULL, at, 0);
+        if (at + n <= (unsigned long long)kSplitUnits) {
+          uint32_t q2 = 0, V2;
+          while ((V2 = search_next(s)) != 0) {
+            if (lane == 0) a.units[at + q2] = (task << 16) | V2;
+            ++q2;
+          }
+          if (lane == 0) {
+            a.sp_key[task] = (s.best << 16) | s.vbest;
+            a.sp_wv[task] = wV;
+          }
+          continue;  // k_pack_big_units / k_pack_big_finish complete this task
+        }
+        // the unit queue is full: finish this task sequentially (below)
+      }
     }
+    while ((V = search_next(s)) != 0) {
+      const uint64_t thr = first ? ~0ull : search_thr_approx(s, V);
+      uint64_t mx = 0;
+      const bool ok = big_run(a, b, V, thr, first, mx, scr_t, scr_k, ev);
+      if (ok && first) wV = V;
+      first = false;
+      if (ok && search_improves(s, V, mx)) search_take(s, V, mx);
+    }
+    if (s.have && s.vbest != wV) {  // the winner's mb was not written by the first run
+      uint64_t mx = 0;
+      big_run(a, b, s.vbest, ~0ull, true, mx, scr_t, scr_k, ev);
+    }
+    if (SPLIT && lane == 0) a.sp_wv[task] = 0u;  // done here
+    big_outputs(a, b, s.vbest, s.best);
+  }
+  if (lane == 0 && ev) atomicAdd(a.evals, (unsigned long long)ev);
+}
+
+__global__ void __launch_bounds__(256, 3) k_pack_big(PackArgs a) { big_queue<false>(a); }
+__global__ void __launch_bounds__(256) k_pack_big_ref(PackArgs a) { big_queue<true>(a); }
+
+// Split queue, step 2: every enqueued (task, V) as an independent LPT(V) run against the task's
+// best so far (abort threshold as in the lanes' phase 2); atomicMin of (obj << 16 | V).
+__global__ void __launch_bounds__(256) k_pack_big_units(PackArgs a) {
+  const unsigned long long total = min(*a.q_count, a.q_cap);
+  if (total > (unsigned long long)kSplitTasks) return;
+  const unsigned long long nunits = min(a.q_count[19], (unsigned long long)kSplitUnits);
+  const int B = a.batch;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + warp;
+  uint64_t* scr_t = a.scr_time + (size_t)gw * B;
+  uint32_t* scr_k = a.scr_tok + (size_t)gw * B;
+  uint64_t ev = 0;
+  while (true) {
+    unsigned long long u = 0;
+    if (lane == 0) u = atomicAdd(a.q_count + 20, 1ull);
+    u = __shfl_sync(HYD_FULL, u, 0);
+    if (u >= nunits) break;
+    const unsigned long long w = a.units[u];
+    const unsigned long long task = w >> 16;
+    const uint32_t V = (uint32_t)(w & 0xFFFFu);
+    BigTask b;
+    big_task(a, a.queue[task], b);
+    Search& s = b.s;
+    unsigned long long cur = 0;
+    if (lane == 0) cur = *reinterpret_cast<volatile unsigned long long*>(a.sp_key + task);
+    cur = __shfl_sync(HYD_FULL, cur, 0);
+    s.have = true;
+    s.best = cur >> 16;
+    s.vbest = (uint32_t)(cur & 0xFFFFu);
+    // exact LB test against the current best (the best can only have improved since enqueueing)
+    const uint64_t m = (uint64_t)(s.P - 1 + V);
+    uint64_t ah, al, bh, bl;
+    mul128(s.sumT, m, ah, al);
+    mul128(s.best, (uint64_t)V, bh, bl);
+    if (gt128(ah, al, bh, bl) || (!gt128(bh, bl, ah, al) && V > s.vbest)) continue;
+    uint64_t mx = 0;
+    const bool ok = big_run(a, b, V, search_thr_approx(s, V), false, mx, scr_t, scr_k, ev);
+    if (ok && lane == 0) atomicMin(a.sp_key + task, ((mx * m) << 16) | V);
+  }
+  if (lane == 0 && ev) atomicAdd(a.evals, (unsigned long long)ev);
+}
+
+// Split queue, step 3: per task, the winner's re-run when it is not the reference run (whose mb is
+// written), and the v / ptime / makespan outputs.
+__global__ void __launch_bounds__(256) k_pack_big_finish(PackArgs a) {
+  const unsigned long long total = min(*a.q_count, a.q_cap);
+  if (total > (unsigned long long)kSplitTasks) return;
+  const int B = a.batch;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + warp;
+  uint64_t* scr_t = a.scr_time + (size_t)gw * B;
+  uint32_t* scr_k = a.scr_tok + (size_t)gw * B;
+  uint64_t ev = 0;
+  for (unsigned long long task = gw; task < total; task += (unsigned long long)gridDim.x * (blockDim.x >> 5)) {
+    const uint32_t wv = a.sp_wv[task];
+    if (wv == 0u) continue;  // finished in k_pack_big
+    BigTask b;
+    big_task(a, a.queue[task], b);
+    const unsigned long long key = a.sp_key[task];
+    const uint32_t vbest = (uint32_t)(key & 0xFFFFu);
+    if (vbest != wv) {
+      uint64_t mx = 0;
+      big_run(a, b, vbest, ~0ull, true, mx, scr_t, scr_k, ev);
+    }
+    big_outputs(a, b, vbest, key >> 16);
   }
   if (lane == 0 && ev) atomicAdd(a.evals, (unsigned long long)ev);
 }
@@ -1275,7 +1416,8 @@ size_t pack_workspace(int n_iter, int batch, int n_cand, int max_np) {
   const size_t cap = (size_t)n_iter * n_cand * dp_of(max_np);
   return align256(256) + align256(cap * 8) + align256((size_t)kBigWarps * batch * 8) +
          align256((size_t)kBigWarps * batch * 4) + align256(flag_bytes(n_iter, n_cand, max_np)) +
-         align256((size_t)n_iter * n_cand * max_np * 4) + align256((size_t)n_iter * 4);
+         align256((size_t)n_iter * n_cand * max_np * 4) + align256((size_t)n_iter * 4) +
+         align256((size_t)kSplitTasks * 8) + align256((size_t)kSplitTasks * 4) + align256((size_t)kSplitUnits * 8);
 }
 
 template <bool STAGED, int VM>
@@ -1340,6 +1482,12 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
   a.list32 = reinterpret_cast<uint32_t*>(w);
   w += align256((size_t)n_iter * n_cand * max_np * 4);
   a.count32 = reinterpret_cast<uint32_t*>(w);
+  w += align256((size_t)n_iter * 4);
+  a.sp_key = reinterpret_cast<unsigned long long*>(w);
+  w += align256((size_t)kSplitTasks * 8);
+  a.sp_wv = reinterpret_cast<uint32_t*>(w);
+  w += align256((size_t)kSplitTasks * 4);
+  a.units = reinterpret_cast<unsigned long long*>(w);
 
   cudaError_t e = cudaMemsetAsync(a.q_count, 0, 256, s);
   if (e != cudaSuccess) return record_cuda_error(e);
@@ -1379,8 +1527,15 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
   note_launch();
   if (e != cudaSuccess) return record_cuda_error(e);
 
-  // warp per pipeline for the queue (V > 32, wide sums, infeasible V_a): persistent, no smem
+  // warp per pipeline for the queue (V > 32, wide sums, infeasible V_a): persistent, no smem;
+  // a short queue runs split (reference runs, then every surviving V as a unit, then re-runs)
   k_pack_big<<<kBigWarps / 8, 256, 0, s>>>(a);
+  note_launch();
+  k_pack_big_ref<<<kBigWarps / 8, 256, 0, s>>>(a);
+  note_launch();
+  k_pack_big_units<<<kBigWarps / 8, 256, 0, s>>>(a);
+  note_launch();
+  k_pack_big_finish<<<kBigWarps / 8, 256, 0, s>>>(a);
   note_launch();
   e = cudaGetLastError();
   return e == cudaSuccess ? HYD_OK : record_cuda_error(e);
