@@ -49,8 +49,8 @@ constexpr int kBigWarps = 3584;   // persistent warps of k_pack_big (scratch slo
 // A short warp queue (at most kSplitTasks pipelines) runs split: every task's reference run, then
 // its surviving V as independent units spread over all warps, then the winners' re-runs -- so the
 // queue's duration is a few runs, not its longest sequential search.
-constexpr int kSplitTasks = 16384;
-constexpr int kSplitUnits = 1 << 20;
+constexpr int kSplitTasks = 1 << 21;
+constexpr int kSplitUnits = 1 << 24;
 
 struct PackArgs {
   const uint32_t* sorted_len;
