@@ -73,6 +73,9 @@ struct PackArgs {
   uint64_t* ptime;
   uint64_t* makespan;
   uint32_t* status;
+  // q_count points at a 256-byte counter block (ws bytes [0, 256), zeroed per call): [0] queued
+  // tasks, [1] queue head, [2] evaluations, [3..18] diagnostic counters, [19] split units
+  // reserved, [20] split unit head
   unsigned long long* q_count;
   unsigned long long* q_head;
   unsigned long long* evals;  // (item, bin) evaluations performed (ws bytes [16, 24))
@@ -1308,7 +1311,11 @@ __device__ __forceinline__ void big_queue(const PackArgs& a) {
           }
           continue;  // k_pack_big_units / k_pack_big_finish complete this task
         }
-        // the unit queue is full: finish this task sequentially (below)
+        // the unit queue is full: mark the reserved slots that exist as empty, finish this task
+        // sequentially (below)
+        if (lane == 0)
+          for (unsigned long long q3 = at; q3 < at + n && q3 < (unsigned long long)kSplitUnits; ++q3)
+            a.units[q3] = ~0ull;
       }
     }
     while ((V = search_next(s)) != 0) {
@@ -1350,6 +1357,7 @@ __global__ void __launch_bounds__(256) k_pack_big_units(PackArgs a) {
     u = __shfl_sync(HYD_FULL, u, 0);
     if (u >= nunits) break;
     const unsigned long long w = a.units[u];
+    if (w == ~0ull) continue;  // a slot of a task that finished sequentially
     const unsigned long long task = w >> 16;
     const uint32_t V = (uint32_t)(w & 0xFFFFu);
     BigTask b;
