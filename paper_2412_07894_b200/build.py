@@ -44,7 +44,10 @@ def build_debug(force: bool = False) -> str:
     instead of libhyd.so when HYD_LIB points at it (tools/sanitize_cases.py)."""
     if not force and os.path.exists(DEBUG_LIB) and not _stale(DEBUG_LIB):
         return DEBUG_LIB
-    return build(force=True, extra=["-DHYD_DEBUG_CHECKS"], out=DEBUG_LIB, bdir_name="build_debug")
+    # HYD_SPLIT_TASKS=0: the warp queue takes its sequential path, which the release build uses
+    # only for queues of more than 2 M pipelines -- so the debug cases cover both paths
+    return build(force=True, extra=["-DHYD_DEBUG_CHECKS", "-DHYD_SPLIT_TASKS=0"], out=DEBUG_LIB,
+                 bdir_name="build_debug")
 
 
 def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None, out: str = LIB,

@@ -49,7 +49,10 @@ constexpr int kBigWarps = 3584;   // persistent warps of k_pack_big (scratch slo
 // A short warp queue (at most kSplitTasks pipelines) runs split: every task's reference run, then
 // its surviving V as independent units spread over all warps, then the winners' re-runs -- so the
 // queue's duration is a few runs, not its longest sequential search.
-constexpr int kSplitTasks = 1 << 21;
+#ifndef HYD_SPLIT_TASKS  // the debug build sets 0: its queue always runs the sequential search
+#define HYD_SPLIT_TASKS (1 << 21)
+#endif
+constexpr int kSplitTasks = HYD_SPLIT_TASKS;
 constexpr int kSplitUnits = 1 << 24;
 
 struct PackArgs {
