@@ -496,3 +496,28 @@ def random_small_instance(rng, B, D, K=3, max_pp=3, lmax=64):
     ml0 = int(sch[ks[0]]["max_len"])
     lens = np.minimum(lens, ml0).astype(np.uint32)
     return custom_workload(lens, sch, [ks])
+
+
+def load_config(path: str) -> Workload:
+    """A configuration from its JSON (configs/cfgN.json, tools/export_configs.py): the scheme and
+    candidate tables as stored; the lengths regenerated from the config's seeded generator and
+    checked against the stored SHA-256."""
+    import hashlib
+    import json
+
+    d = json.load(open(path))
+    W = make_workload(int(d["config"]))
+    lens = np.ascontiguousarray(W.lengths, np.uint32)
+    if hashlib.sha256(lens.tobytes()).hexdigest() != d["lengths"]["sha256_lengths"]:
+        raise ValueError(f"{path}: the regenerated lengths do not match the stored hash")
+    sch = np.zeros(len(d["schemes"]), dtype=SCHEME_DTYPE)
+    for i, s in enumerate(d["schemes"]):
+        for k, v in s.items():
+            sch[i][k] = v
+    cand = np.full((len(d["candidates"]), 32), 0xFF, np.uint8)
+    cnp = np.zeros(len(d["candidates"]), np.uint8)
+    for c, row in enumerate(d["candidates"]):
+        cand[c, : len(row)] = row
+        cnp[c] = len(row)
+    return Workload(W.cfg, d["workload"], lens, sch, cand, cnp, int(d["k_pad"]), meta=dict(d["meta"]),
+                    offsets=W.offsets)
