@@ -60,6 +60,8 @@ def lib():
         L.hydref_dispatch.restype = I
         L.hydref_lpt.argtypes = [_u32p, _u32p, I, I, C.c_uint32, _u16p, C.POINTER(C.c_uint64)]
         L.hydref_lpt.restype = I
+        L.hydref_lpt_heap.argtypes = [_u32p, _u32p, I, I, C.c_uint32, _u16p, C.POINTER(C.c_uint64)]
+        L.hydref_lpt_heap.restype = I
         L.hydref_pack_pipeline.argtypes = [
             _u32p, _u32p, I, _voidp, C.POINTER(C.c_uint16), C.POINTER(C.c_uint64), _u16p, U32P,
         ]
@@ -160,12 +162,15 @@ def dispatch(sorted_len, cost_tab, schemes, cand_row):
     return bool(ok), pipe, int(lb.value)
 
 
-def lpt(ell, tau, v, max_len):
+def lpt(ell, tau, v, max_len, heap=False):
+    """LPT(V) with capacity: the plain scan (hydref_lpt) or the heap form (hydref_lpt_heap)
+    that hydref_pack_pipeline's V enumeration uses."""
     ell = np.ascontiguousarray(ell, np.uint32)
     tau = np.ascontiguousarray(tau, np.uint32)
     mb = np.zeros(max(ell.size, 1), np.uint16)
     mx = C.c_uint64(0)
-    ok = lib().hydref_lpt(ell, tau, ell.size, int(v), int(max_len), mb, C.byref(mx))
+    fn = lib().hydref_lpt_heap if heap else lib().hydref_lpt
+    ok = fn(ell, tau, ell.size, int(v), int(max_len), mb, C.byref(mx))
     return bool(ok), mb[: ell.size], int(mx.value)
 
 

@@ -179,6 +179,85 @@ int hydref_lpt(const uint32_t* ell, const uint32_t* tau, int u, int v, uint32_t 
   return ok;
 }
 
+/* The same LPT(V), with the argmin taken from a binary min-heap of the bins ordered by
+ * (time_b, b) instead of a scan: bins leave the heap in increasing (time, b) order, so the
+ * first one whose token count stays <= MaxLen is the scan's b* (least time among fitting bins,
+ * ties to the smallest index).  Bins popped before it do not fit and go back unchanged.
+ * O(U log V) instead of O(U V) per run, which is what lets the V enumeration below cover
+ * config 5 (U up to ~2800, V up to U).  Pinned against hydref_lpt (tests/test_oracle_pins.py). */
+static int heap_less(const uint64_t* time, uint32_t a, uint32_t b) {
+  return time[a] < time[b] || (time[a] == time[b] && a < b);
+}
+
+static void heap_push(uint32_t* h, int* n, const uint64_t* time, uint32_t b) {
+  int i = (*n)++;
+  h[i] = b;
+  while (i > 0 && heap_less(time, h[i], h[(i - 1) / 2])) {
+    uint32_t x = h[i];
+    h[i] = h[(i - 1) / 2];
+    h[(i - 1) / 2] = x;
+    i = (i - 1) / 2;
+  }
+}
+
+static uint32_t heap_pop(uint32_t* h, int* n, const uint64_t* time) {
+  uint32_t top = h[0];
+  h[0] = h[--(*n)];
+  int i = 0;
+  for (;;) {
+    int l = 2 * i + 1, r = l + 1, m = i;
+    if (l < *n && heap_less(time, h[l], h[m])) m = l;
+    if (r < *n && heap_less(time, h[r], h[m])) m = r;
+    if (m == i) break;
+    uint32_t x = h[i];
+    h[i] = h[m];
+    h[m] = x;
+    i = m;
+  }
+  return top;
+}
+
+int hydref_lpt_heap(const uint32_t* ell, const uint32_t* tau, int u, int v, uint32_t max_len,
+                    uint16_t* mb_q, uint64_t* maxbin) {
+  uint64_t* time = (uint64_t*)calloc((size_t)v, sizeof(uint64_t));
+  uint64_t* tok = (uint64_t*)calloc((size_t)v, sizeof(uint64_t));
+  uint32_t* heap = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)v);
+  uint32_t* skipped = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)v);
+  int n = 0, ok = 1;
+  for (int b = 0; b < v; ++b) heap_push(heap, &n, time, (uint32_t)b);
+  for (int q = 0; q < u && ok; ++q) {
+    int bstar = -1, n_skip = 0;
+    while (n > 0) {
+      uint32_t b = heap_pop(heap, &n, time);
+      if (tok[b] + ell[q] <= max_len) {
+        bstar = (int)b;
+        break;
+      }
+      skipped[n_skip++] = b;
+    }
+    for (int s = 0; s < n_skip; ++s) heap_push(heap, &n, time, skipped[s]);
+    if (bstar < 0) {
+      ok = 0;
+      break;
+    }
+    time[bstar] += tau[q];
+    tok[bstar] += ell[q];
+    mb_q[q] = (uint16_t)bstar;
+    heap_push(heap, &n, time, (uint32_t)bstar);
+  }
+  if (ok) {
+    uint64_t m = 0;
+    for (int b = 0; b < v; ++b)
+      if (time[b] > m) m = time[b];
+    *maxbin = m;
+  }
+  free(time);
+  free(tok);
+  free(heap);
+  free(skipped);
+  return ok;
+}
+
 /* Eq. 1: objective = (max_b sum_{i in b} T(l_i)) * (PP - 1 + V).
  * V enumeration restricted to App. D's range:
  *   V_lo = max(ceil(S / MaxLen), 1),  V_hi = min(floor(S / UtilLen), U)
@@ -207,7 +286,7 @@ void hydref_pack_pipeline(const uint32_t* ell, const uint32_t* tau, int u, const
   uint64_t best_v = 0;
   for (uint64_t v = v_lo; v <= v_hi; ++v) {
     uint64_t maxbin;
-    if (!hydref_lpt(ell, tau, u, (int)v, s->max_len, cur, &maxbin)) continue;
+    if (!hydref_lpt_heap(ell, tau, u, (int)v, s->max_len, cur, &maxbin)) continue;
     u128 obj = (u128)maxbin * (u128)(s->pp - 1 + v);
     if (!have || obj < best) {
       have = 1;
@@ -218,7 +297,7 @@ void hydref_pack_pipeline(const uint32_t* ell, const uint32_t* tau, int u, const
   }
   for (uint64_t v = v_hi + 1; !have && v <= (uint64_t)u; ++v) {
     uint64_t maxbin;
-    if (!hydref_lpt(ell, tau, u, (int)v, s->max_len, cur, &maxbin)) continue;
+    if (!hydref_lpt_heap(ell, tau, u, (int)v, s->max_len, cur, &maxbin)) continue;
     have = 1;
     best = (u128)maxbin * (u128)(s->pp - 1 + v);
     best_v = v;

@@ -54,6 +54,10 @@ int hydref_dispatch(const uint32_t* sorted, const uint32_t* cost, int batch, int
  * *maxbin = max bin time on success. */
 int hydref_lpt(const uint32_t* ell, const uint32_t* tau, int u, int v, uint32_t max_len,
                uint16_t* mb_q, uint64_t* maxbin);
+/* The same LPT(V) with the argmin read from a (time, b) min-heap (O(U log V)); identical
+ * results (pinned against hydref_lpt).  hydref_pack_pipeline's V enumeration uses it. */
+int hydref_lpt_heap(const uint32_t* ell, const uint32_t* tau, int u, int v, uint32_t max_len,
+                    uint16_t* mb_q, uint64_t* maxbin);
 
 /* Step 5 -- stage 2 pack of one pipeline (Eq. 1, V enumeration P:616,
  * App. D range P:1097).  ell/tau: the pipeline's items in increasing sorted position.

@@ -1,12 +1,10 @@
 """Full-size parity (north_star: "bit-exact oracle agreement on all five configs"; SURVEY §8(d):
 "no subsampling"): every output array of the CUDA path -- sorted_len, perm, cost, pipe, lb, mb, v,
-ptime, makespan, key -- for EVERY candidate and iteration of BASELINE configs 1-4, config 5's
-first iterations and config 6 (token-budget batches), in the launch
-configuration bench.py times (config 5: the first 1024 candidates x 2 iterations, the oracle's
-unpruned V enumeration taking 13.6 CPU-s per candidate-iteration there), against per-iteration
-digests of the CPU oracle's outputs
-(tests/golden/digests_cfgN.npz, written by tools/make_golden_digests.py, which imports only
-oracle/ and workload/).  Digest = workload/digest.py (BLAKE2b of each iteration's slice)."""
+ptime, makespan, key -- for EVERY candidate and iteration of BASELINE configs 1-6 (config 6:
+token-budget batches), in the launch configuration bench.py times, against per-iteration digests
+of the CPU oracle's outputs (tests/golden/digests_cfgN.npz, written by
+tools/make_golden_digests.py, which imports only oracle/ and workload/).  A golden file that
+covers fewer candidates or iterations than the configuration is checked on that prefix.  Digest = workload/digest.py (BLAKE2b of each iteration's slice)."""
 import os
 
 import numpy as np

@@ -336,6 +336,56 @@ def test_lpt_graham_per_v():
             assert ok and mx >= opt and mx * 3 * V <= (4 * V - 1) * opt
 
 
+def test_lpt_heap_equals_scan():
+    """hydref_lpt_heap (the form the V enumeration runs) gives the plain scan's bins, max bin and
+    feasibility: random instances with binding capacity, many equal times (ties to the smaller
+    bin) and infeasible runs; then hydref_pack_pipeline against an enumeration of V written here
+    over the scan (App. D range, reading 5's extension, reading 6's ties)."""
+    o = _oracle()
+    rng = np.random.default_rng(23)
+    n_inf = n_cap = 0
+    for it in range(600):
+        U = int(rng.integers(1, 120 if it % 3 else 400))
+        ell = np.sort(rng.integers(1, 200, U))[::-1].astype(np.uint32)
+        tau = (ell // 50 + rng.integers(0, 3, U)).astype(np.uint32) + 1 if it % 2 else \
+            rng.integers(1, 6, U).astype(np.uint32)
+        M = int(ell[0]) + int(rng.integers(0, 3 * int(ell[0]) + 1))
+        for V in sorted({1, U, *rng.integers(1, U + 1, 6).tolist()}):
+            a, b = o.lpt(ell, tau, V, M), o.lpt(ell, tau, V, M, heap=True)
+            assert a[0] == b[0]
+            if a[0]:
+                assert np.array_equal(a[1], b[1]) and a[2] == b[2]
+                cap = np.bincount(a[1], weights=ell, minlength=V)
+                n_cap += int(cap.max() > M - int(ell[-1]))
+            else:
+                n_inf += 1
+    assert n_inf > 50 and n_cap > 200  # both regimes exercised
+    for it in range(150):
+        U = int(rng.integers(1, 60))
+        ell = np.sort(rng.integers(1, 300, U))[::-1].astype(np.uint32)
+        tau = rng.integers(1, 9, U).astype(np.uint32)
+        M = int(ell[0]) + int(rng.integers(0, 400))
+        S = int(ell.sum())
+        ul = int(rng.integers(0, 3)) * int(rng.integers(1, 200))
+        pp = int(rng.integers(1, 5))
+        s = linear_scheme(pp=pp, max_len=M, util_len=ul)
+        v_lo = max(-(-S // M), 1)
+        v_hi = max(U if ul == 0 else min(S // ul, U), v_lo)
+        best = None
+        for V in range(v_lo, v_hi + 1):
+            ok, mb, mx = o.lpt(ell, tau, V, M)
+            if ok and (best is None or mx * (pp - 1 + V) < best[0]):
+                best = (mx * (pp - 1 + V), V, mb)
+        V = v_hi + 1
+        while best is None:
+            ok, mb, mx = o.lpt(ell, tau, V, M)
+            if ok:
+                best = (mx * (pp - 1 + V), V, mb)
+            V += 1
+        v, pt, mb, st = o.pack_pipeline(ell, tau, s)
+        assert (pt, v) == best[:2] and np.array_equal(mb, best[2]) and st == 0
+
+
 def test_lpt_infeasible_returns_bottom():
     o = _oracle()
     ok, _, _ = o.lpt([6, 6, 6], [1, 1, 1], 2, 10)  # three 6s into two bins of 10
