@@ -280,6 +280,13 @@ __device__ __forceinline__ uint32_t packed_step(uint32_t l, const uint32_t (&tau
   return bj;
 }
 
+template <int OFF>
+__device__ __forceinline__ uint32_t lds_off(uint32_t addr) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(addr), "n"(OFF));
+  return v;
+}
+
 // TRANS: cost staged in smem as [lt][k][Bp] (cost(i, k) at ct[k * Bp + i] for this thread's lt);
 // else global rows [t][i][k_pad].
 template <int DP, bool TRANS>
@@ -307,6 +314,9 @@ __device__ __forceinline__ void packed_run(const uint32_t* __restrict__ sl,
     cf[j] = 0u;
     pj[j] = TRANS ? cst + (size_t)kk[j] * stride : cst + kk[j];
   }
+  uint32_t pa[DP];  // TRANS: the rows' shared-window addresses
+#pragma unroll
+  for (int j = 0; j < DP; ++j) pa[j] = TRANS ? (uint32_t)__cvta_generic_to_shared(pj[j]) : 0u;
   const bool full_sectors = (B & 31) == 0 && ((size_t)prow & 15) == 0;
   uint32_t pbj = 0u, pl = 0u;  // the decision whose S_j update is pending
   for (int i0 = 0; i0 < B; i0 += 32) {
@@ -324,16 +334,23 @@ __device__ __forceinline__ void packed_run(const uint32_t* __restrict__ sl,
         const int i = i0 + g;
         const uint4 l4 = *reinterpret_cast<const uint4*>(sl + i);
         const uint32_t lq[4] = {l4.x, l4.y, l4.z, l4.w};
+        uint32_t qa[DP];  // shared addresses of row j at sequence i: the 4 steps use immediate offsets
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int j = 0; j < DP; ++j) qa[j] = pa[j] + 4u * (uint32_t)i;
+        auto step = [&](auto uc) {
+          constexpr int U = decltype(uc)::value;
           uint32_t tau[DP];
 #pragma unroll
-          for (int j = 0; j < DP; ++j) tau[j] = pj[j][i + u];
+          for (int j = 0; j < DP; ++j) tau[j] = lds_off<4 * U>(qa[j]);
           if (warp_empty)
-            packed_step<DP, SH, true>(lq[u], tau, key, mults, ml, np, pend, plane, s_sum, pbj, pl);
+            packed_step<DP, SH, true>(lq[U], tau, key, mults, ml, np, pend, plane, s_sum, pbj, pl);
           else
-            packed_step<DP, SH, false>(lq[u], tau, key, mults, ml, np, pend, plane, s_sum, pbj, pl);
-        }
+            packed_step<DP, SH, false>(lq[U], tau, key, mults, ml, np, pend, plane, s_sum, pbj, pl);
+        };
+        step(std::integral_constant<int, 0>{});
+        step(std::integral_constant<int, 1>{});
+        step(std::integral_constant<int, 2>{});
+        step(std::integral_constant<int, 3>{});
       }
       for (int q = n4; q < n; ++q) {
         const int i = i0 + q;
