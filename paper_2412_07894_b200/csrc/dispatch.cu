@@ -33,13 +33,16 @@ __host__ __device__ inline size_t dispatch_stage_words(int tt, int B, int k_pad)
 
 // One sequence step: candidate loads, argmin (new_j, j), branch-free update of pipeline j*.
 // FEAS: test MaxLen_j >= l (only needed while l exceeds the smallest MaxLen of the candidate;
-// lengths are sorted descending, so the tail of the batch skips the test).
-template <int DP, typename TT, bool FEAS>
+// lengths are sorted descending, so the tail of the batch skips the test).  EMPTY: some
+// pipeline of the warp may still be empty (multiplier PP_j); once none is, every used mult_j is
+// 1 and stays 1, so the step skips their updates.  The decision j* is shifted into SH bit
+// planes (plane_b bit q = bit b of the chunk's q-th decision), expanded into membership words
+// once per 32-step chunk (chunk_flush).
+template <int DP, typename TT, bool FEAS, bool EMPTY, int SH>
 __device__ __forceinline__ uint32_t dispatch_step(uint32_t l, const uint32_t* __restrict__ crow,
                                                   bool staged, const uint32_t (&ml)[DP],
                                                   const uint32_t (&kk)[DP], TT (&base)[DP],
-                                                  uint32_t (&mult)[DP], uint32_t (&bits)[DP],
-                                                  uint32_t bit) {
+                                                  uint32_t (&mult)[DP], uint32_t (&plane)[SH]) {
   TT best = (TT)~(TT)0;
   uint32_t bj = 0u;
 #pragma unroll
@@ -56,10 +59,84 @@ __device__ __forceinline__ uint32_t dispatch_step(uint32_t l, const uint32_t* __
   for (int j = 0; j < DP; ++j) {
     const bool hit = (uint32_t)j == bj;
     base[j] = hit ? best : base[j];
-    mult[j] = hit ? 1u : mult[j];
-    bits[j] |= hit ? bit : 0u;
+    if (EMPTY) mult[j] = hit ? 1u : mult[j];
   }
+#pragma unroll
+  for (int b = 0; b < SH; ++b) plane[b] = __funnelshift_r(plane[b], bj >> b, 1);
   return bj;
+}
+
+template <int DP>
+struct DispCfg {
+  static constexpr int SH = DP <= 2 ? 1 : DP <= 4 ? 2 : DP <= 8 ? 3 : DP <= 16 ? 4 : 5;
+};
+
+// true while some used pipeline of some thread of the warp is still empty (mult_j = PP_j > 1)
+template <int DP>
+__device__ __forceinline__ bool warp_any_empty(const uint32_t (&mult)[DP], int np, unsigned amask) {
+  bool e = false;
+#pragma unroll
+  for (int j = 0; j < DP; ++j) e |= j < np && mult[j] > 1u;
+  return __any_sync(amask, e);
+}
+
+// End of a chunk of n <= 32 decisions starting at sequence i0: one membership word per pipeline
+// (word j = the decisions equal to j, from the bit planes) and cf_j = U_j << 16 | first member + 1.
+template <int DP, int SH>
+__device__ __forceinline__ void chunk_flush(uint32_t (&plane)[SH], int n, int i0, int np, int mstride,
+                                            uint32_t* __restrict__ mbits, uint32_t (&cf)[DP]) {
+  if (n < 32) {
+#pragma unroll
+    for (int b = 0; b < SH; ++b) plane[b] >>= 32 - n;
+  }
+  const uint32_t valid = n < 32 ? (1u << n) - 1u : 0xFFFFFFFFu;
+#pragma unroll
+  for (int j = 0; j < DP; ++j) {
+    if (j < np) {
+      uint32_t wj = valid;
+#pragma unroll
+      for (int b = 0; b < SH; ++b) wj &= ((j >> b) & 1) ? plane[b] : ~plane[b];
+      HYD_CHECK(j < mstride);
+      mbits[(size_t)(i0 >> 5) * mstride + j] = wj;
+      const uint32_t f = (cf[j] & 0xFFFFu) == 0u && wj != 0u ? (uint32_t)i0 + __ffs(wj) : 0u;
+      cf[j] += (__popc(wj) << 16) + f;
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < SH; ++b) plane[b] = 0u;
+}
+
+// one 32-step chunk of a thread's decisions: steps i0 .. i0 + n - 1 (ls / crow_of read the
+// sequence's length and cost row)
+template <int DP, typename TT, bool EMPTY, typename LenF, typename RowF>
+__device__ __forceinline__ void dispatch_chunk(int i0, int n, bool staged, uint32_t ml_min,
+                                               const uint32_t (&ml)[DP], const uint32_t (&kk)[DP],
+                                               TT (&base)[DP], uint32_t (&mult)[DP],
+                                               uint32_t (&plane)[DispCfg<DP>::SH], LenF&& len_of,
+                                               RowF&& row_of, uint8_t* __restrict__ prow, bool words,
+                                               unsigned long long* s_sum, uint32_t& pbj, uint32_t& pl) {
+  constexpr int SH = DispCfg<DP>::SH;
+  uint32_t word = 0u;
+  for (int q = 0; q < n; ++q) {
+    const int i = i0 + q;
+    const unsigned long long sold = s_sum[pbj * kDispatchThreads];
+    const uint32_t l = len_of(q);
+    const uint32_t* crow = row_of(q);
+    const uint32_t bj = l > ml_min ? dispatch_step<DP, TT, true, EMPTY, SH>(l, crow, staged, ml, kk, base, mult, plane)
+                                   : dispatch_step<DP, TT, false, EMPTY, SH>(l, crow, staged, ml, kk, base, mult, plane);
+    s_sum[pbj * kDispatchThreads] = sold + pl;  // S_j column of this thread, one step late
+    pbj = bj;
+    pl = l;
+    if (words) {
+      word |= bj << (8 * (i & 3));
+      if ((i & 3) == 3) {
+        *reinterpret_cast<uint32_t*>(prow + (i & ~3)) = word;
+        word = 0u;
+      }
+    } else {
+      prow[i] = (uint8_t)bj;
+    }
+  }
 }
 
 template <int DP, typename TT>
@@ -71,53 +148,30 @@ __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
                                              uint32_t* __restrict__ mbits, int np, int mstride,
                                              uint64_t& lb_out, TT (&base)[DP],
                                              uint32_t (&cf)[DP]) {
-  uint32_t mult[DP], bits[DP];
+  constexpr int SH = DispCfg<DP>::SH;
+  const unsigned amask = __activemask();
+  uint32_t mult[DP], plane[SH];
   uint32_t ml_min = 0xFFFFFFFFu;
 #pragma unroll
   for (int j = 0; j < DP; ++j) {  // unused slots: base = max, mult = 0 -> never strictly best
     base[j] = j < np ? (TT)0 : (TT)~(TT)0;
     mult[j] = j < np ? pp[j] : 0u;
-    bits[j] = 0u;
     cf[j] = 0u;
     if (j < np) ml_min = min(ml_min, ml[j]);
   }
-  const bool words = (B & 3) == 0 && ((size_t)prow & 3) == 0;
-  uint32_t word = 0u;
-  uint32_t pbj = 0u, pl = 0u;  // S_j one step late (as in packed_step)
-  for (int i = 0; i < B; ++i) {
-    const unsigned long long sold = s_sum[pbj * kDispatchThreads];
-    const uint32_t l = sl[i];
-    const uint32_t* crow = cs + (size_t)i * k_pad;
-    const uint32_t bit = 1u << (i & 31);
-    const uint32_t bj =
-        l > ml_min ? dispatch_step<DP, TT, true>(l, crow, staged, ml, kk, base, mult, bits, bit)
-                   : dispatch_step<DP, TT, false>(l, crow, staged, ml, kk, base, mult, bits, bit);
-    s_sum[pbj * kDispatchThreads] = sold + pl;  // S_j column of this thread
-    pbj = bj;
-    pl = l;
-    if ((i & 31) == 31 || i == B - 1) {  // flush one membership word per pipeline
-      const uint32_t w0 = (uint32_t)(i & ~31);
 #pragma unroll
-      for (int j = 0; j < DP; ++j) {
-        if (j < np) {
-          HYD_CHECK(j < mstride);
-          mbits[(size_t)(i >> 5) * mstride + j] = bits[j];
-          // cf_j = U_j << 16 | (index of the first (= longest) member + 1), B <= 16384
-          const uint32_t f = (cf[j] & 0xFFFFu) == 0u && bits[j] != 0u ? w0 + __ffs(bits[j]) : 0u;
-          cf[j] += (__popc(bits[j]) << 16) + f;
-        }
-        bits[j] = 0u;
-      }
-    }
-    if (words) {
-      word |= bj << (8 * (i & 3));
-      if ((i & 3) == 3) {
-        *reinterpret_cast<uint32_t*>(prow + (i & ~3)) = word;
-        word = 0u;
-      }
-    } else {
-      prow[i] = (uint8_t)bj;
-    }
+  for (int b = 0; b < SH; ++b) plane[b] = 0u;
+  const bool words = (B & 3) == 0 && ((size_t)prow & 3) == 0;
+  uint32_t pbj = 0u, pl = 0u;  // S_j one step late (as in packed_step)
+  for (int i0 = 0; i0 < B; i0 += 32) {
+    const int n = min(32, B - i0);
+    auto lf = [&](int q) { return sl[i0 + q]; };
+    auto rf = [&](int q) { return cs + (size_t)(i0 + q) * k_pad; };
+    if (warp_any_empty<DP>(mult, np, amask))
+      dispatch_chunk<DP, TT, true>(i0, n, staged, ml_min, ml, kk, base, mult, plane, lf, rf, prow, words, s_sum, pbj, pl);
+    else
+      dispatch_chunk<DP, TT, false>(i0, n, staged, ml_min, ml, kk, base, mult, plane, lf, rf, prow, words, s_sum, pbj, pl);
+    chunk_flush<DP, SH>(plane, n, i0, np, mstride, mbits, cf);
   }
   s_sum[pbj * kDispatchThreads] += pl;  // the last decision's S_j
   uint64_t m = 0ull;
@@ -132,7 +186,7 @@ __device__ __forceinline__ void dispatch_run(const uint32_t* __restrict__ sl,
 // cost rows into shared memory together, then each live thread runs its steps from there, so
 // every cost read is a shared-memory load instead of an L2 round trip.  All threads of the CTA
 // take part in the copies and barriers; `live` threads (a feasible candidate) also decide.
-constexpr int kDispatchWin = 512;
+constexpr int kDispatchWin = 512;  // a multiple of the 32-step chunk
 
 template <int DP, typename TT>
 __device__ __forceinline__ void dispatch_run_win(bool live, const uint32_t* __restrict__ g_sl,
@@ -142,19 +196,21 @@ __device__ __forceinline__ void dispatch_run_win(bool live, const uint32_t* __re
                                                  uint8_t* __restrict__ prow, unsigned long long* s_sum,
                                                  uint32_t* __restrict__ mbits, int np, int mstride,
                                                  uint64_t& lb_out, TT (&base)[DP], uint32_t (&cf)[DP]) {
+  constexpr int SH = DispCfg<DP>::SH;
   const int tid = threadIdx.x;
-  uint32_t mult[DP], bits[DP];
+  const unsigned amask = __ballot_sync(HYD_FULL, live);
+  uint32_t mult[DP], plane[SH];
   uint32_t ml_min = 0xFFFFFFFFu;
 #pragma unroll
   for (int j = 0; j < DP; ++j) {  // unused slots: base = max, mult = 0 -> never strictly best
     base[j] = j < np ? (TT)0 : (TT)~(TT)0;
     mult[j] = j < np ? pp[j] : 0u;
-    bits[j] = 0u;
     cf[j] = 0u;
     if (j < np) ml_min = min(ml_min, ml[j]);
   }
+#pragma unroll
+  for (int b = 0; b < SH; ++b) plane[b] = 0u;
   const bool words = (B & 3) == 0 && ((size_t)prow & 3) == 0;
-  uint32_t word = 0u;
   uint32_t pbj = 0u, pl = 0u;  // S_j one step late (as in packed_step)
   uint32_t* wl = wsm;                 // [kDispatchWin] lengths
   uint32_t* wc = wsm + kDispatchWin;  // [kDispatchWin][k_pad] cost rows
@@ -172,40 +228,17 @@ __device__ __forceinline__ void dispatch_run_win(bool live, const uint32_t* __re
     }
     __syncthreads();
     if (!live) continue;
-    for (int q = 0; q < n; ++q) {
-      const int i = w0 + q;
-      const unsigned long long sold = s_sum[pbj * kDispatchThreads];
-      const uint32_t l = wl[q];
-      const uint32_t* crow = wc + q * k_pad;
-      const uint32_t bit = 1u << (i & 31);
-      const uint32_t bj =
-          l > ml_min ? dispatch_step<DP, TT, true>(l, crow, true, ml, kk, base, mult, bits, bit)
-                     : dispatch_step<DP, TT, false>(l, crow, true, ml, kk, base, mult, bits, bit);
-      s_sum[pbj * kDispatchThreads] = sold + pl;  // S_j column of this thread
-      pbj = bj;
-      pl = l;
-      if ((i & 31) == 31 || i == B - 1) {  // flush one membership word per pipeline
-        const uint32_t wb = (uint32_t)(i & ~31);
-#pragma unroll
-        for (int j = 0; j < DP; ++j) {
-          if (j < np) {
-            HYD_CHECK(j < mstride);
-            mbits[(size_t)(i >> 5) * mstride + j] = bits[j];
-            const uint32_t f = (cf[j] & 0xFFFFu) == 0u && bits[j] != 0u ? wb + __ffs(bits[j]) : 0u;
-            cf[j] += (__popc(bits[j]) << 16) + f;
-          }
-          bits[j] = 0u;
-        }
-      }
-      if (words) {
-        word |= bj << (8 * (i & 3));
-        if ((i & 3) == 3) {
-          *reinterpret_cast<uint32_t*>(prow + (i & ~3)) = word;
-          word = 0u;
-        }
-      } else {
-        prow[i] = (uint8_t)bj;
-      }
+    for (int q0 = 0; q0 < n; q0 += 32) {
+      const int nq = min(32, n - q0);
+      auto lf = [&](int q) { return wl[q0 + q]; };
+      auto rf = [&](int q) { return wc + (q0 + q) * k_pad; };
+      if (warp_any_empty<DP>(mult, np, amask))
+        dispatch_chunk<DP, TT, true>(w0 + q0, nq, true, ml_min, ml, kk, base, mult, plane, lf, rf, prow, words, s_sum, pbj,
+                                     pl);
+      else
+        dispatch_chunk<DP, TT, false>(w0 + q0, nq, true, ml_min, ml, kk, base, mult, plane, lf, rf, prow, words, s_sum,
+                                      pbj, pl);
+      chunk_flush<DP, SH>(plane, nq, w0 + q0, np, mstride, mbits, cf);
     }
   }
   if (!live) return;
