@@ -49,14 +49,15 @@ struct SmallArgs {
   unsigned long long* evals;
 };
 
-// per-thread shared records of the pipelines (structure of arrays, stride kSmallThreads so
+// per-thread shared records of the pipelines (structure of arrays, stride T = CTA threads so
 // lane-consecutive): rs[j] = S_j (tokens), rb[j] = base_j = C_j + E_j; after pipeline j's
 // search, rs[j] = V* and rb[j] = its objective (ptime)
+template <int T>
 struct PipeRec {
   uint32_t* rs;
   unsigned long long* rb;
-  __device__ uint32_t& s(int j) const { return rs[j * kSmallThreads]; }
-  __device__ unsigned long long& b(int j) const { return rb[j * kSmallThreads]; }
+  __device__ uint32_t& s(int j) const { return rs[j * T]; }
+  __device__ unsigned long long& b(int j) const { return rb[j * T]; }
 };
 
 // One LPT(V) run over the members of one pipeline (mw: its membership words), V <= N
@@ -158,11 +159,11 @@ __device__ __noinline__ bool run_generic(const uint32_t* __restrict__ mw, int nw
   return true;
 }
 
-template <int DP, typename TT>
+template <int DP, typename TT, int T>
 __device__ __forceinline__ void small_dispatch(const uint32_t* __restrict__ sl, const uint32_t* __restrict__ sc,
                                                int B, int kp, int np, const uint32_t (&ml)[DP],
                                                const uint32_t (&pp)[DP], const uint32_t (&kk)[DP],
-                                               uint32_t* __restrict__ mem, const PipeRec& rec,
+                                               uint32_t* __restrict__ mem, const PipeRec<T>& rec,
                                                uint8_t* __restrict__ prow, uint64_t& lb_out) {
   TT base[DP];
   uint32_t mult[DP], S[DP];
@@ -221,45 +222,47 @@ __device__ __forceinline__ void small_dispatch(const uint32_t* __restrict__ sl, 
   lb_out = m;
 }
 
-template <int DP>
-__global__ void __launch_bounds__(kSmallThreads) k_assign_small(SmallArgs a) {
+// T = CTA threads (candidates of the iteration per CTA): 128, or 32 when there are at most 32
+// candidates -- one-warp CTAs then keep four times as many (c, t) latency chains resident.
+template <int DP, int T>
+__global__ void __launch_bounds__(T) k_assign_small(SmallArgs a) {
   extern __shared__ __align__(16) uint32_t sm[];
   __shared__ uint32_t s_ml[HYD_MAX_SCHEMES], s_pp[HYD_MAX_SCHEMES], s_ul[HYD_MAX_SCHEMES];
   __shared__ unsigned long long s_sum, s_max;
   const int tid = threadIdx.x, lane = tid & 31;
-  const int t = blockIdx.y, c = blockIdx.x * kSmallThreads + tid;
+  const int t = blockIdx.y, c = blockIdx.x * T + tid;
   const int B = geo_bt(a.off, a.batch, t);
   const size_t tbase = geo_base(a.off, a.batch, t);
   const int kp = a.k_pad;
   // smem: bases [DP][T] u64 | lengths [Bmax] | costs [Bmax][kp] | members [T][DP][W] |
   //       S [DP][T] u32 | mb [T][Bmax] u8
   unsigned long long* rb_all = reinterpret_cast<unsigned long long*>(sm);
-  uint32_t* sl = reinterpret_cast<uint32_t*>(rb_all + kSmallThreads * DP);
+  uint32_t* sl = reinterpret_cast<uint32_t*>(rb_all + T * DP);
   uint32_t* sc = sl + HYD_SMALL_MAX_BATCH;
   uint32_t* mem_all = sc + HYD_SMALL_MAX_BATCH * kp;
-  uint32_t* rs_all = mem_all + kSmallThreads * DP * kSmallWords;
-  uint8_t* mb_all = reinterpret_cast<uint8_t*>(rs_all + kSmallThreads * DP);
+  uint32_t* rs_all = mem_all + T * DP * kSmallWords;
+  uint8_t* mb_all = reinterpret_cast<uint8_t*>(rs_all + T * DP);
   uint32_t* mem = mem_all + tid * DP * kSmallWords;
-  const PipeRec rec{rs_all + tid, rb_all + tid};
+  const PipeRec<T> rec{rs_all + tid, rb_all + tid};
   uint8_t* mbs = mb_all + tid * HYD_SMALL_MAX_BATCH;
 
   if (tid == 0) {
     s_sum = 0ull;
     s_max = 0ull;
   }
-  for (int k = tid; k < a.n_schemes; k += kSmallThreads) {
+  for (int k = tid; k < a.n_schemes; k += T) {
     s_ml[k] = a.schemes[k].max_len;
     s_pp[k] = a.schemes[k].pp;
     s_ul[k] = a.schemes[k].util_len;
   }
-  for (int e = tid; e < B; e += kSmallThreads) sl[e] = __ldg(a.sorted_len + tbase + e);
-  for (int e = tid; e < B * kp; e += kSmallThreads) sc[e] = __ldg(a.cost + tbase * kp + e);
+  for (int e = tid; e < B; e += T) sl[e] = __ldg(a.sorted_len + tbase + e);
+  for (int e = tid; e < B * kp; e += T) sc[e] = __ldg(a.cost + tbase * kp + e);
   for (int e = 0; e < DP * kSmallWords; ++e) mem[e] = 0u;
   __syncthreads();
   // every load of this iteration is below sum_i max_k tau_ik + max tau (PPmax - 1): u32 if < 2^32
   {
     unsigned long long part = 0ull, mxv = 0ull;
-    for (int i = tid; i < B; i += kSmallThreads) {
+    for (int i = tid; i < B; i += T) {
       uint32_t m = 0u;
       for (int k = 0; k < a.n_schemes; ++k) {
         const uint32_t tau = sc[i * kp + k];
@@ -309,8 +312,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_assign_small(SmallArgs a) {
   uint8_t* prow = a.pipe + (size_t)c * a.n_total + tbase;
   if (feasible) {
     uint64_t lbv;
-    if (narrow) small_dispatch<DP, uint32_t>(sl, sc, B, kp, np, ml, pp, kk, mem, rec, prow, lbv);
-    else small_dispatch<DP, uint64_t>(sl, sc, B, kp, np, ml, pp, kk, mem, rec, prow, lbv);
+    if (narrow) small_dispatch<DP, uint32_t, T>(sl, sc, B, kp, np, ml, pp, kk, mem, rec, prow, lbv);
+    else small_dispatch<DP, uint64_t, T>(sl, sc, B, kp, np, ml, pp, kk, mem, rec, prow, lbv);
     a.lb[row] = lbv;
   } else if (active) {
     for (int i = 0; i < B; ++i) prow[i] = 0xFF;
@@ -443,19 +446,24 @@ __global__ void __launch_bounds__(kSmallThreads) k_assign_small(SmallArgs a) {
   }
 }
 
-size_t small_smem(int dp, int k_pad) {
-  return (size_t)kSmallThreads * dp * 8 + (size_t)HYD_SMALL_MAX_BATCH * 4 * (1 + (size_t)k_pad) +
-         (size_t)kSmallThreads * dp * kSmallWords * 4 + (size_t)kSmallThreads * dp * 4 +
-         (size_t)kSmallThreads * HYD_SMALL_MAX_BATCH;
+size_t small_smem(int dp, int k_pad, int T) {
+  return (size_t)T * dp * 8 + (size_t)HYD_SMALL_MAX_BATCH * 4 * (1 + (size_t)k_pad) +
+         (size_t)T * dp * kSmallWords * 4 + (size_t)T * dp * 4 + (size_t)T * HYD_SMALL_MAX_BATCH;
+}
+
+template <int DP, int T>
+static cudaError_t launch_small_t(int n_cand, int n_iter, cudaStream_t s, const SmallArgs& a) {
+  const size_t smem = small_smem(DP, a.k_pad, T);
+  cudaError_t e = cudaFuncSetAttribute(k_assign_small<DP, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const dim3 grid((n_cand + T - 1) / T, n_iter);
+  k_assign_small<DP, T><<<grid, T, smem, s>>>(a);
+  return cudaGetLastError();
 }
 
 template <int DP>
-static cudaError_t launch_small_dp(dim3 grid, cudaStream_t s, const SmallArgs& a) {
-  const size_t smem = small_smem(DP, a.k_pad);
-  cudaError_t e = cudaFuncSetAttribute(k_assign_small<DP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  k_assign_small<DP><<<grid, kSmallThreads, smem, s>>>(a);
-  return cudaGetLastError();
+static cudaError_t launch_small_dp(int n_cand, int n_iter, cudaStream_t s, const SmallArgs& a) {
+  return n_cand <= 32 ? launch_small_t<DP, 32>(n_cand, n_iter, s, a) : launch_small_t<DP, kSmallThreads>(n_cand, n_iter, s, a);
 }
 
 int launch_small(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, int batch, const uint32_t* off,
@@ -488,12 +496,11 @@ int launch_small(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, i
     const cudaError_t e = cudaMemsetAsync(ws, 0, 8, s);
     if (e != cudaSuccess) return record_cuda_error(e);
   }
-  const dim3 grid((n_cand + kSmallThreads - 1) / kSmallThreads, n_iter);
   cudaError_t e;
-  if (max_np <= 2) e = launch_small_dp<2>(grid, s, a);
-  else if (max_np <= 4) e = launch_small_dp<4>(grid, s, a);
-  else if (max_np <= 8) e = launch_small_dp<8>(grid, s, a);
-  else e = launch_small_dp<16>(grid, s, a);
+  if (max_np <= 2) e = launch_small_dp<2>(n_cand, n_iter, s, a);
+  else if (max_np <= 4) e = launch_small_dp<4>(n_cand, n_iter, s, a);
+  else if (max_np <= 8) e = launch_small_dp<8>(n_cand, n_iter, s, a);
+  else e = launch_small_dp<16>(n_cand, n_iter, s, a);
   note_launch();
   return e == cudaSuccess ? HYD_OK : record_cuda_error(e);
 }
