@@ -2,7 +2,9 @@
 // descending, original index ascending) fused with the Q32 fixed-point cost table
 // T(l, P_k) = floor((a_k l^2 + b_k l + c_k) / 2^32)  (App. C.2).
 //
-// One CTA per iteration t.  The B lengths stay in shared memory; an LSD radix sort
+// By batch size: B <= 32 a warp per iteration ranks by shuffles; B <= 256 a warp per iteration
+// runs a register bitonic sort on distinct keys; larger batches use one CTA per iteration t.
+// There the B lengths stay in shared memory; an LSD radix sort
 // over 4-bit digits (as many passes as the iteration's largest length needs) permutes
 // a u16 index array, blocked arrangement + digit-major block scan => stable.  The
 // cost rows are then written as 16-byte vector stores, consecutive threads writing
@@ -194,6 +196,105 @@ __global__ void __launch_bounds__(256) k_sort_cost_warp(const uint32_t* __restri
   if (st && lane == 0) atomicOr(status, st);
 }
 
+// Batches of 33 .. 256 sequences (configurations 2 and 6): a WARP per
+// iteration, a bitonic sort of u64 keys (~l_i) << 32 | i in registers (E per lane, element
+// i = lane * E + e; padding keys ~0 sort last).  The keys are distinct, so ascending key order is
+// exactly (length descending, index ascending) -- the radix sort's stable order -- with no
+// shared memory and no barriers (the CTA radix sort's passes are latency-bound at these sizes).
+template <int E>
+__device__ __forceinline__ void bitonic_warp(uint64_t (&k)[E], int lane) {
+  constexpr int N = 32 * E;
+#pragma unroll
+  for (int size = 2; size <= N; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= E) {  // partner in lane ^ (stride / E), same e
+        const int lm = stride / E;
+        const bool lower = (lane & lm) == 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int i = lane * E + e;
+          const bool asc = (i & size) == 0;
+          const uint64_t o = __shfl_xor_sync(HYD_FULL, k[e], lm);
+          k[e] = (lower == asc) ? min(k[e], o) : max(k[e], o);
+        }
+      } else {  // partner e ^ stride in the same lane
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          if ((e & stride) == 0) {
+            const int i = lane * E + e;
+            const bool asc = (i & size) == 0;
+            const uint64_t x = k[e], y = k[e ^ stride];
+            const uint64_t lo = min(x, y), hi = max(x, y);
+            k[e] = asc ? lo : hi;
+            k[e ^ stride] = asc ? hi : lo;
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int E>
+__global__ void __launch_bounds__(128) k_sort_cost_bitonic(const uint32_t* __restrict__ len, int batch,
+                                                           const uint32_t* __restrict__ off,
+                                                           const hyd_scheme* __restrict__ schemes,
+                                                           int n_schemes, int k_pad, int n_iter,
+                                                           uint32_t* __restrict__ sorted_len,
+                                                           uint32_t* __restrict__ perm,
+                                                           uint32_t* __restrict__ cost,
+                                                           uint32_t* __restrict__ status) {
+  const int t = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= n_iter) return;
+  const int B = geo_bt(off, batch, t);
+  const size_t base = geo_base(off, batch, t);
+  if (off && lane == 0) {  // ragged batches: 1 <= B_t <= batch
+    const int d = (int)(__ldg(off + t + 1) - __ldg(off + t));
+    if (d < 1 || d > batch) atomicOr(status, HYD_F_BAD_LENGTH);
+  }
+  uint64_t k[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = lane * E + e;
+    k[e] = i < B ? ((uint64_t)(~__ldg(len + base + i)) << 32) | (uint32_t)i : ~0ull;
+  }
+  bitonic_warp<E>(k, lane);
+  uint32_t st = 0;
+  const int quads = k_pad >> 2;
+  for (int q = 0; q < quads; ++q) {
+    uint64_t ca[4], cb[4], cc[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int kk = 4 * q + r;
+      ca[r] = kk < n_schemes ? schemes[kk].a_q32 : 0ull;
+      cb[r] = kk < n_schemes ? schemes[kk].b_q32 : 0ull;
+      cc[r] = kk < n_schemes ? schemes[kk].c_q32 : 0ull;
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = lane * E + e;
+      if (i < B) {
+        const uint32_t l = ~(uint32_t)(k[e] >> 32);
+        uint32_t out[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) out[r] = 4 * q + r < n_schemes ? eval_cost(ca[r], cb[r], cc[r], l, st) : 0u;
+        reinterpret_cast<uint4*>(cost + (base + i) * k_pad)[q] = make_uint4(out[0], out[1], out[2], out[3]);
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = lane * E + e;
+    if (i < B) {
+      sorted_len[base + i] = ~(uint32_t)(k[e] >> 32);
+      perm[base + i] = (uint32_t)(k[e] & 0xFFFFFFFFu);
+    }
+  }
+  st = __reduce_or_sync(HYD_FULL, st);
+  if (st && lane == 0) atomicOr(status, st);
+}
+
 size_t sort_cost_smem(int batch, int nt, int n_schemes) {
   return (((size_t)batch * 4 + 16 * (size_t)nt * 4 + (size_t)batch * 4 + 15) & ~(size_t)15) +
          (size_t)n_schemes * 24;
@@ -207,6 +308,14 @@ int launch_sort_cost(const uint32_t* len, int n_iter, int batch, const uint32_t*
   if (batch <= 32) {
     k_sort_cost_warp<<<(n_iter + 7) / 8, 256, 0, s>>>(len, batch, off, schemes, n_schemes, k_pad, n_iter,
                                                       sorted_len, perm, cost, status);
+  } else if (batch <= 256) {  // (at 512 the CTA radix sort is as fast: few warps, long chains)
+    const int g = (n_iter + 3) / 4;
+    if (batch <= 64)
+      k_sort_cost_bitonic<2><<<g, 128, 0, s>>>(len, batch, off, schemes, n_schemes, k_pad, n_iter, sorted_len, perm, cost, status);
+    else if (batch <= 128)
+      k_sort_cost_bitonic<4><<<g, 128, 0, s>>>(len, batch, off, schemes, n_schemes, k_pad, n_iter, sorted_len, perm, cost, status);
+    else
+      k_sort_cost_bitonic<8><<<g, 128, 0, s>>>(len, batch, off, schemes, n_schemes, k_pad, n_iter, sorted_len, perm, cost, status);
   } else if (batch <= 2048) {
     const size_t sm = sort_cost_smem(batch, 256, n_schemes);
     e = cudaFuncSetAttribute(k_sort_cost<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
