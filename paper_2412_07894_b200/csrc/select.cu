@@ -3,7 +3,10 @@
 //
 // k_select: one warp per iteration, lanes stride the makespan row (coalesced 8-byte
 // loads), key = makespan << 20 | c_global (argmin of (makespan, c) == min key), then a
-// 5-step shuffle min.  Across GPUs the caller allreduces key with MIN over NCCL.
+// 5-step shuffle min.  k_select_cta: rows of more than 512 candidates get a CTA each
+// (~16 candidates per thread, shuffle + shared-memory min), so few long rows (config 5: 16
+// iterations x 16 384 candidates) do not serialise on 16 warps.  Across GPUs the caller
+// allreduces key with MIN over NCCL.
 #include "hyd_internal.cuh"
 
 namespace hyd {
@@ -37,6 +40,54 @@ __global__ void __launch_bounds__(256) k_select(const uint64_t* __restrict__ mak
   if (lane == 0) {
     key[w] = best;
     if (st) atomicOr(status, st);
+  }
+}
+
+__device__ __forceinline__ long long select_key(uint64_t m, int c, int cand_offset, uint32_t& st) {
+  if (m == ~0ull) return 0x7FFFFFFFFFFFFFFFll;  // infeasible candidate
+  if (m >= HYD_MAKESPAN_LIMIT) {
+    st |= HYD_F_KEY_RANGE;
+    return 0x7FFFFFFFFFFFFFFFll;
+  }
+  return (long long)((m << HYD_KEY_SHIFT) | (uint64_t)(c + cand_offset));
+}
+
+__global__ void __launch_bounds__(1024) k_select_cta(const uint64_t* __restrict__ makespan, int n_iter,
+                                                     int n_cand, int cand_offset,
+                                                     int64_t* __restrict__ key,
+                                                     uint32_t* __restrict__ status) {
+  __shared__ long long s_best[32];
+  __shared__ uint32_t s_st;
+  const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, nt = blockDim.x;
+  const unsigned long long* row = reinterpret_cast<const unsigned long long*>(makespan) + (size_t)t * n_cand;
+  if (tid == 0) s_st = 0u;
+  long long best = 0x7FFFFFFFFFFFFFFFll;
+  uint32_t st = 0;
+  int c = tid;
+  for (; c + 3 * nt < n_cand; c += 4 * nt) {  // four independent loads in flight per thread
+    const uint64_t m0 = __ldg(row + c), m1 = __ldg(row + c + nt), m2 = __ldg(row + c + 2 * nt),
+                   m3 = __ldg(row + c + 3 * nt);
+    best = min(best, min(min(select_key(m0, c, cand_offset, st), select_key(m1, c + nt, cand_offset, st)),
+                         min(select_key(m2, c + 2 * nt, cand_offset, st), select_key(m3, c + 3 * nt, cand_offset, st))));
+  }
+  for (; c < n_cand; c += nt) best = min(best, select_key(__ldg(row + c), c, cand_offset, st));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(HYD_FULL, best, o));
+  st = __reduce_or_sync(HYD_FULL, st);
+  __syncthreads();  // s_st initialised
+  if (lane == 0) {
+    s_best[tid >> 5] = best;
+    if (st) atomicOr(&s_st, st);
+  }
+  __syncthreads();
+  if (tid < 32) {
+    best = tid < (nt >> 5) ? s_best[tid] : 0x7FFFFFFFFFFFFFFFll;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(HYD_FULL, best, o));
+    if (tid == 0) {
+      key[t] = best;
+      if (s_st) atomicOr(status, s_st);
+    }
   }
 }
 
@@ -76,8 +127,13 @@ __global__ void __launch_bounds__(256) k_gather(const int64_t* __restrict__ key,
 int launch_select(const uint64_t* makespan, int n_iter, int n_cand, int cand_offset, int64_t* key,
                   uint32_t* status, cudaStream_t s) {
   if (n_iter == 0) return HYD_OK;
-  const int blocks = (n_iter * 32 + 255) / 256;
-  k_select<<<blocks, 256, 0, s>>>(makespan, n_iter, n_cand, cand_offset, key, status);
+  if (n_cand > 512) {
+    const int nt = min(1024, ((n_cand + 16 * 32 - 1) / (16 * 32)) * 32);  // ~16 candidates per thread
+    k_select_cta<<<n_iter, nt, 0, s>>>(makespan, n_iter, n_cand, cand_offset, key, status);
+  } else {
+    const int blocks = (n_iter * 32 + 255) / 256;
+    k_select<<<blocks, 256, 0, s>>>(makespan, n_iter, n_cand, cand_offset, key, status);
+  }
   note_launch();
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? HYD_OK : record_cuda_error(e);
