@@ -205,6 +205,7 @@ struct LaneUnit {
   uint32_t qw, cur, wbase, nxtw;
   uint32_t V, thr, mx, k, M;
   uint32_t tb;  // STAGED: shared-window address of the cost column k (row 0)
+  uint32_t pi, pl, pt;  // !STAGED: the next member's index, length and cost, loaded a step early
 #ifdef HYD_DEBUG_CHECKS
   uint32_t bt;  // the iteration's sequences (member indices must stay below)
 #endif
@@ -226,6 +227,7 @@ __device__ __forceinline__ void unit_start(LaneUnit<VM>& u, uint32_t V, uint32_t
   u.qw = 0;
   u.cur = 0;
   u.nxtw = __ldg(u.mw);  // word w of the pipeline at mw[w * mnp]
+  u.pi = 0xFFFFFFFFu;
 }
 
 // Advance the unit by one sequence.  Returns 0 while running, 1 when the run completed,
@@ -258,8 +260,22 @@ __device__ __forceinline__ int unit_step(LaneUnit<VM>& u, uint32_t nwords, uint3
   u.cur &= u.cur - 1u;
   // STAGED: 32-bit shared-window addresses (sbase: lengths; u.tb + 4 kp i: the cost of row i)
   HYD_CHECK(!valid || i < u.bt);
-  const uint32_t tau = STAGED ? ld_shared_u32(u.tb + i * kp4) : cst[(size_t)i * kp + u.k];
-  const uint32_t l = FREE ? 0u : (STAGED ? ld_shared_u32(sbase + i * 4u) : slen[i]);
+  uint32_t tau, l;
+  if constexpr (STAGED) {
+    tau = ld_shared_u32(u.tb + i * kp4);
+    l = FREE ? 0u : ld_shared_u32(sbase + i * 4u);
+  } else {  // L2 reads: this member's were issued a step early; issue the next member's now
+    const bool pre = u.pi == i;
+    tau = pre ? u.pt : cst[(size_t)i * kp + u.k];
+    l = FREE ? 0u : (pre ? u.pl : slen[i]);
+    const uint32_t i2 = u.cur ? u.wbase + (uint32_t)(__ffs(u.cur) - 1)
+                              : (u.qw < nwords && u.nxtw ? u.qw * 32u + (uint32_t)(__ffs(u.nxtw) - 1) : 0xFFFFFFFFu);
+    u.pi = i2;
+    if (i2 != 0xFFFFFFFFu) {  // (the length too in capacity-free steps: the warp's next epoch may be masked)
+      u.pt = cst[(size_t)i2 * kp + u.k];
+      u.pl = slen[i2];
+    }
+  }
   uint32_t m0;
   if constexpr (FREE) {  // capacity cannot bind: plain least-time bin, bin tokens not tracked
     m0 = min_keys<N, VM>(u.keys);
