@@ -41,6 +41,8 @@
 namespace hyd {
 
 constexpr int kLaneThreads = 256;
+// flagged VMAX-32 tasks in all (counted by k_flag_list) up to which the warp queue takes them
+constexpr unsigned long long kFlaggedToQueue = 16384;
 constexpr size_t kLaneSmem16 = 74 * 1024;   // VMAX 16 pass: 3 CTAs per SM
 constexpr size_t kLaneSmem32 = 110 * 1024;  // VMAX 32 pass: 2 CTAs per SM
 constexpr int kLaneEpoch = 24;     // sequences per lane between bookkeeping phases
@@ -78,7 +80,7 @@ struct PackArgs {
   uint32_t* status;
   // q_count points at a 256-byte counter block (ws bytes [0, 256), zeroed per call): [0] queued
   // tasks, [1] queue head, [2] evaluations, [3..18] diagnostic counters, [19] split units
-  // reserved, [20] split unit head
+  // reserved, [20] split unit head, [21] flagged VMAX-32 tasks in all
   unsigned long long* q_count;
   unsigned long long* q_head;
   unsigned long long* evals;  // (item, bin) evaluations performed (ws bytes [16, 24))
@@ -317,6 +319,19 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
   const int chunk0 = VM == 32 ? blockIdx.x * ncap : 0;
   const int nchunk = VM == 32 ? min(ncap, (int)a.count32[t] - chunk0) : 0;
   if (VM == 32 && nchunk <= 0) return;
+  if (VM == 32 && a.q_count[21] <= kFlaggedToQueue) {
+    // few flagged tasks in all (configs 2 and 3: ~1 and ~40 per iteration): a CTA per iteration
+    // would mostly stage and wait, so they go to the warp queue, which runs the same exact
+    // search from scratch (same V*, ptime and mb) right after this pass
+    const size_t lbase = (size_t)blockIdx.y * ((size_t)a.n_cand * mnp) + chunk0;
+    for (int q = threadIdx.x; q < nchunk; q += kLaneThreads) {
+      const int e = (int)a.list32[lbase + q];
+      const unsigned long long slot = atomicAdd(a.q_count, 1ull);
+      if (slot < a.q_cap)
+        a.queue[slot] = ((unsigned long long)(e / mnp) << 37) | ((unsigned long long)blockIdx.y << 5) | (unsigned)(e % mnp);
+    }
+    return;
+  }
   const int B = geo_bt(a.off, a.batch, t);  // this iteration's sequences
   const size_t tbase = geo_base(a.off, a.batch, t);
   const int tid = threadIdx.x, lane = tid & 31;
@@ -890,7 +905,8 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
 // The tasks the VMAX-16 pass flagged, per iteration, as a compacted list in ascending task id
 // (c * mnp + j): one CTA per iteration, block-wide scan of per-thread counts of 32-task groups.
 __global__ void __launch_bounds__(256) k_flag_list(const uint32_t* __restrict__ flags, int n_cand, int mnp,
-                                                   uint32_t* __restrict__ list32, uint32_t* __restrict__ count32) {
+                                                   uint32_t* __restrict__ list32, uint32_t* __restrict__ count32,
+                                                   unsigned long long* __restrict__ total) {
   __shared__ int s_w[8];
   __shared__ int s_base;
   const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -924,7 +940,10 @@ __global__ void __launch_bounds__(256) k_flag_list(const uint32_t* __restrict__ 
     if (tid == 255) s_base = wbase + x;
     __syncthreads();
   }
-  if (tid == 0) count32[t] = (uint32_t)s_base;
+  if (tid == 0) {
+    count32[t] = (uint32_t)s_base;
+    if (s_base) atomicAdd(total, (unsigned long long)s_base);
+  }
 }
 
 // ------------------------------------------------------------------ LPT, one warp per pipeline
@@ -1545,7 +1564,7 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
   if (e != cudaSuccess) return record_cuda_error(e);
   // the flagged tasks of each iteration, compacted; VMAX-32 CTAs take chunks of <= ncap2 of them
   // (CTAs past an iteration's count exit at once)
-  k_flag_list<<<n_iter, 256, 0, s>>>(a.flags, n_cand, max_np, a.list32, a.count32);
+  k_flag_list<<<n_iter, 256, 0, s>>>(a.flags, n_cand, max_np, a.list32, a.count32, a.q_count + 21);
   note_launch();
   const int tc2 = 0;
   dim3 grid2((unsigned)(((size_t)n_cand * max_np + ncap2 - 1) / ncap2), n_iter);
