@@ -427,8 +427,7 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
     }
     if (VM == 16 && s.va > 16u) {
       atomicAdd(a.why + 1, 1ull);
-      if (s.sumT >= LaneCfg<32>::SUMT_LIMIT || s.va > 32u) to_queue(c, j);  // the VMAX-32 pass could not hold it
-      else hand_off_e(e);
+      hand_off_e(e);
       continue;
     }
     const int r = atomicAdd(&s_nrec, 1);
@@ -734,8 +733,7 @@ __global__ void __launch_bounds__(kLaneThreads, VM == 16 ? 3 : 2) k_pack_lanes(P
     R.sum_t[r] = vmask;  // the candidates as a bit set over V (sum_t is not read after this walk)
     if (vmax > (uint32_t)VM) {
       atomicAdd(a.why + (VM == 16 ? 3 : 6), 1ull);
-      if (VM == 16 && vmax > 32u) to_queue(c0 + (int)R.eid[r] / mnp, (int)R.eid[r] % mnp);  // beyond VMAX 32 too
-      else hand_off_e((int)R.eid[r]);
+      hand_off_e((int)R.eid[r]);
       R.state[r] = 1;
       continue;
     }
