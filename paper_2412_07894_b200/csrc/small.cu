@@ -3,7 +3,7 @@
 //
 // For B_t <= HYD_SMALL_MAX_BATCH (128) and at most 16 pipelines per candidate, one THREAD per
 // (c, t) runs stage 1 and stage 2 back to back with everything in registers and shared memory:
-//   * the CTA (128 candidates of one iteration) stages the iteration's sorted lengths and cost
+//   * the CTA (128 candidates of one iteration; 32 when there are at most 32) stages the sorted lengths and cost
 //     rows once;
 //   * dispatch (HYD-H1; Eq. 2/3 P:634-650, Alg. 1's rule P:1131-1144):
 //     base_j = C_j + E_j and mult_j = PP_j while pipeline j is empty, 1 after, so a candidate
