@@ -135,8 +135,12 @@ __global__ void __launch_bounds__(kDpThreads)
       const int mumax = nu / (int)s_g[k];
       const unsigned long long* pk = ppre + (size_t)k * W1;
       const unsigned long long pj = pk[j];
+      const uint64_t g1 = (uint64_t)scale * (pj - pk[j - 1]);  // mu g(1): W_k over the last bucket
       for (int mu = 1 + ((tid - pair) % kDpThreads + kDpThreads) % kDpThreads; mu <= mumax;
            mu += kDpThreads) {
+        // every value of the pair is >= g(1) = g1 / mu (g is non-decreasing in j', f >= 0): a pair
+        // whose bound already exceeds this thread's best cannot win, nor tie (exact pruning)
+        if (q_less(bn, bd, g1, (uint64_t)mu)) continue;
         const size_t rbase = (size_t)(nu - mu * (int)s_g[k]) * W1 + j;  // f(j') = t[rbase - j']
         auto f_at = [&](int jp, uint64_t& fn, uint64_t& fd) {
           fn = t_num[rbase - jp];
