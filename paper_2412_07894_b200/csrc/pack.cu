@@ -46,6 +46,7 @@ constexpr unsigned long long kFlaggedToQueue = 16384;
 constexpr size_t kLaneSmem16 = 74 * 1024;   // VMAX 16 pass: 3 CTAs per SM
 constexpr size_t kLaneSmem32 = 110 * 1024;  // VMAX 32 pass: 2 CTAs per SM
 constexpr int kLaneEpoch = 24;     // sequences per lane between bookkeeping phases
+constexpr int kChunk32 = 400;      // flagged tasks per staged VMAX-32 CTA (measured: 2048 / 512 / 400 / 256)
 constexpr int kBigRMax = 8;       // k_pack_big: register bins per lane (V <= 256)
 constexpr int kBigWarps = 3584;   // persistent warps of k_pack_big (scratch slots): 148 SMs x 24
 // A short warp queue (at most kSplitTasks pipelines) runs split: every task's reference run, then
@@ -1567,9 +1568,12 @@ int launch_pack(const uint32_t* sorted_len, const uint32_t* cost, int n_iter, in
   k_flag_list<<<n_iter, 256, 0, s>>>(a.flags, n_cand, max_np, a.list32, a.count32, a.q_count + 21);
   note_launch();
   const int tc2 = 0;
-  dim3 grid2((unsigned)(((size_t)n_cand * max_np + ncap2 - 1) / ncap2), n_iter);
-  e = st2 ? launch_lanes<true, 32>(grid2, smem2, s, a, tc2, max_np, ncap2)
-          : launch_lanes<false, 32>(grid2, smem2, s, a, tc2, max_np, ncap2);
+  // staged passes take chunks of at most kChunk32 flagged tasks: config 4's ~790 per iteration
+  // then fill two CTAs each, and the pass runs ~7 waves instead of ~3.5 (a shorter tail)
+  const int chunk2 = st2 ? min(ncap2, kChunk32) : ncap2;
+  dim3 grid2((unsigned)(((size_t)n_cand * max_np + chunk2 - 1) / chunk2), n_iter);
+  e = st2 ? launch_lanes<true, 32>(grid2, smem2, s, a, tc2, max_np, chunk2)
+          : launch_lanes<false, 32>(grid2, smem2, s, a, tc2, max_np, chunk2);
   note_launch();
   if (e != cudaSuccess) return record_cuda_error(e);
 
